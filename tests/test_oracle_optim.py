@@ -1,0 +1,268 @@
+"""Pins of the oracle's optimizer steps, clipping and byte model (no GPU).
+
+* P5  absorption: the split storage follows a plain numpy
+      binary32 loop bit-exactly while a 16-bit-only parameter never moves.
+* P6  fp32-master equivalence with event accounting: the residual-compensated
+      trajectory equals the fp32-master trajectory bit-exactly on every element whose split
+      was never lossy, and within a stated drift bound on the rest.
+* P7  special cases / closed forms (first Adam step).
+* P10 library routine: torch.optim.SGD / Adam / AdamW (foreach=False, CPU fp32) reproduce
+      the oracle's fp32-master trajectory within a few binary32 ulps.
+* norm: exact-sum constructions and math.fsum; clip formula closed forms (reading R9).
+* P9  byte model.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+
+
+def f32(x):
+    return np.float32(x)
+
+
+# ----------------------------------------------------------------------------------- P5 --
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+def test_p5_absorption_repair(orc, fmt):
+    n_steps, inc = 1000, f32(1e-4)
+    # plain numpy binary32 sequential accumulation (an fp32 master copy)
+    w_ref = f32(1.0)
+    for _ in range(n_steps):
+        w_ref = f32(w_ref + inc)
+    # SPEC S:252 expects "1.1 within 1e-5": the binary32 result is 1.1000166 (rel 1.5e-5)
+    assert w_ref.view(np.uint32) == 0x3F8CCD58
+    # residual-compensated storage: SGD with lr=1 and grad=-1e-4 (fp32 grad)
+    h, r = orc.split(fmt, np.array([1.0], np.float32))
+    g = np.array([-inc], np.float32)
+    for _ in range(n_steps):
+        orc.sgd_step(fmt, "fp32", h, r, g, None, lr=1.0)
+    assert orc.reconstruct(fmt, h, r)[0].view(np.uint32) == w_ref.view(np.uint32)
+    # 16-bit only: the increment is below half an ulp of 1.0 and is absorbed every time
+    h16 = orc.cast16(fmt, np.array([1.0], np.float32))
+    for _ in range(n_steps):
+        h16 = orc.cast16(fmt, orc.widen(fmt, h16) + inc)
+    assert orc.widen(fmt, h16)[0] == 1.0
+    # SGD direction: 1000 x (-1e-4) from 1.0
+    w_ref = f32(1.0)
+    for _ in range(n_steps):
+        w_ref = f32(w_ref - inc)
+    h, r = orc.split(fmt, np.array([1.0], np.float32))
+    for _ in range(n_steps):
+        orc.sgd_step(fmt, "fp32", h, r, -g, None, lr=1.0)
+    assert orc.reconstruct(fmt, h, r)[0] == w_ref
+
+
+# ----------------------------------------------------------------------------------- P6 --
+def _ulp32(x):
+    x = np.abs(x.astype(np.float64))
+    e = np.floor(np.log2(np.maximum(x, 2.0 ** -126)))
+    return 2.0 ** (e - 23)
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "fp16"])
+@pytest.mark.parametrize("seed", [0xB0B, 2023])
+def test_p6_master_equivalence_adamw(orc, fmt, seed):
+    n, T = 1 << 16, 60
+    hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, adamw=True)
+    w0 = synth.weights(n, 0.02, seed)
+    # fp32 master trajectory
+    wm = w0.copy(); mm = np.zeros(n, np.float32); vm = np.zeros(n, np.float32)
+    # residual-compensated trajectory, stepped as reconstruct -> fp32 update -> split so the
+    # lossy split events can be counted
+    h, r = orc.split(fmt, w0)
+    ms = np.zeros(n, np.float32); vs = np.zeros(n, np.float32)
+    ev0 = orc.reconstruct(fmt, h, r).view(np.uint32) != w0.view(np.uint32)   # initial split
+    k = ev0.astype(np.int64)                  # lossy splits per element
+    t_first = np.where(ev0, 0, T + 1)         # step of the first event
+    j = (ev0 & (np.abs(w0) < 2.0 ** -17)).astype(np.int64)   # events in fp16's saturated range
+    wmax = np.abs(w0).astype(np.float64)
+    # check the one-call step equals the composition on a copy
+    h1, r1, m1, v1 = h.copy(), r.copy(), ms.copy(), vs.copy()
+    for t in range(1, T + 1):
+        g = synth.grads(n, 1e-3, fmt, seed, t)
+        orc.adam_step_master(fmt, wm, g, mm, vm, step=t, **hp)
+        w = orc.reconstruct(fmt, h, r)
+        orc.adam_step_master(fmt, w, g, ms, vs, step=t, **hp)
+        h, r = orc.split(fmt, w)
+        rec = orc.reconstruct(fmt, h, r)
+        ev = rec.view(np.uint32) != w.view(np.uint32)
+        k += ev
+        t_first = np.where(ev & (t_first > T), t, t_first)
+        j += (np.abs(w) < 2.0 ** -17) & ev
+        wmax = np.maximum(wmax, np.abs(w).astype(np.float64))
+        orc.adam_step(fmt, fmt, h1, r1, g, m1, v1, step=t, **hp)
+    assert np.array_equal(h1, h) and np.array_equal(r1, r)
+    assert np.array_equal(m1, ms) and np.array_equal(v1, vs)
+    ws = orc.reconstruct(fmt, h, r)
+    diff = ws.view(np.uint32) != wm.view(np.uint32)
+    no_event = k == 0
+    # zero tolerance where the storage never lost a bit
+    assert not (diff & no_event).any()
+    assert no_event.mean() > 0.9
+    # drift bound for elements with events: each lossy split costs <= 1 ulp32 (or 2^-25 in
+    # fp16's saturated range), each later step adds <= 2 independent roundings
+    d = np.abs(ws.astype(np.float64) - wm.astype(np.float64))
+    bound = (k + 2 * np.maximum(T - t_first, 0)) * _ulp32(wmax) + j * 2.0 ** -25
+    assert (d <= bound + 0.0).all(), (d - bound).max()
+
+
+# ----------------------------------------------------------------------------------- P7 --
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+def test_p7_adam_zero_grad(orc, fmt):
+    n = 4096
+    w0 = synth.weights(n)
+    h, r = orc.split(fmt, w0)
+    g = np.zeros(n, np.uint16)
+    m = np.zeros(n, np.float32); v = np.zeros(n, np.float32)
+    h0, r0 = h.copy(), r.copy()
+    orc.adam_step(fmt, fmt, h, r, g, m, v, lr=1e-3, adamw=False, step=1)
+    assert np.array_equal(h, h0) and np.array_equal(r, r0)
+    # AdamW with g=0 multiplies by (1 - lr*wd) only
+    orc.adam_step(fmt, fmt, h, r, g, m, v, lr=1e-3, weight_decay=0.1, adamw=True, step=2)
+    w = orc.reconstruct(fmt, h0, r0)
+    expect = (w * f32(1.0 - 1e-3 * 0.1)).astype(np.float32)
+    eh, er = orc.split(fmt, expect)
+    assert np.array_equal(h, eh) and np.array_equal(r, er)
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+def test_p7_sgd_special_cases(orc, fmt):
+    n = 4096
+    w0 = synth.weights(n)
+    g16 = synth.grads(n, 1e-2, fmt, 0xB0B, 1)
+    g = orc.widen(fmt, g16)
+    h, r = orc.split(fmt, w0)
+    w = orc.reconstruct(fmt, h, r)
+    # lr = 0: parameter unchanged, momentum buffer updated; carve-out: -0 - (-0) = +0
+    buf = np.zeros(n, np.float32)
+    hh, rr = h.copy(), r.copy()
+    orc.sgd_step(fmt, fmt, hh, rr, g16, buf, lr=0.0, momentum=0.9, first_step=True)
+    assert np.array_equal(hh, h) and np.array_equal(rr, r)
+    assert np.array_equal(buf, g)                       # first step: buffer = clone(grad)
+    # mu = 0, wd = 0: w - lr*g, compared with numpy binary32 arithmetic
+    hh, rr = h.copy(), r.copy()
+    orc.sgd_step(fmt, fmt, hh, rr, g16, None, lr=0.5)
+    expect = (w - f32(0.5) * g).astype(np.float32)
+    eh, er = orc.split(fmt, expect)
+    assert np.array_equal(hh, eh) and np.array_equal(rr, er)
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+def test_p7_first_adam_step_moves_by_lr(orc, fmt):
+    n = 1 << 14
+    w0 = synth.weights(n)
+    g16 = synth.grads(n, 1e-3, fmt, 2023, 1)
+    g = orc.widen(fmt, g16).astype(np.float64)
+    wm = w0.copy()
+    m = np.zeros(n, np.float32); v = np.zeros(n, np.float32)
+    lr, eps = 1e-3, 1e-8
+    orc.adam_step_master(fmt, wm, g16, m, v, lr=lr, eps=eps, adamw=False, step=1)
+    assert np.array_equal(m, (f32(0.1) * g.astype(np.float32)).astype(np.float32))
+    moved = w0.astype(np.float64) - wm.astype(np.float64)
+    expect = lr * g / (np.abs(g) + eps)
+    tol = 8 * _ulp32(np.maximum(np.abs(w0), np.abs(wm))) + 1e-6 * lr
+    assert (np.abs(moved - expect) <= tol).all()
+
+
+# ---------------------------------------------------------------------------------- P10 --
+@pytest.mark.parametrize("kind", ["adamw", "adam_l2", "sgd_m", "sgd_nesterov", "sgd_damp_wd"])
+def test_p10_matches_torch_optim(orc, kind):
+    import torch
+    n, T = 8192, 30
+    w0 = synth.weights(n, 0.02, 0xC0FFEE)
+    p = torch.nn.Parameter(torch.from_numpy(w0.copy()))
+    if kind == "adamw":
+        hp = dict(lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, adamw=True)
+        opt = torch.optim.AdamW([p], lr=1e-3, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1,
+                                foreach=False, fused=False)
+    elif kind == "adam_l2":
+        hp = dict(lr=7e-5, beta1=0.64, beta2=0.999, eps=1e-8, weight_decay=1e-2, adamw=False)
+        opt = torch.optim.Adam([p], lr=7e-5, betas=(0.64, 0.999), eps=1e-8, weight_decay=1e-2,
+                               foreach=False, fused=False)
+    elif kind == "sgd_m":
+        hp = dict(lr=0.3, momentum=0.9, weight_decay=2e-4)
+        opt = torch.optim.SGD([p], lr=0.3, momentum=0.9, weight_decay=2e-4, foreach=False)
+    elif kind == "sgd_nesterov":
+        hp = dict(lr=0.1, momentum=0.9, nesterov=True)
+        opt = torch.optim.SGD([p], lr=0.1, momentum=0.9, nesterov=True, foreach=False)
+    else:
+        hp = dict(lr=0.1, momentum=0.8, dampening=0.3, weight_decay=1e-3)
+        opt = torch.optim.SGD([p], lr=0.1, momentum=0.8, dampening=0.3, weight_decay=1e-3,
+                              foreach=False)
+    w = w0.copy()
+    wmax = np.abs(w0).astype(np.float64)
+    a = np.zeros(n, np.float32); b = np.zeros(n, np.float32)
+    for t in range(1, T + 1):
+        g = synth.grads(n, 1e-2, "fp32", 0xC0FFEE, t)
+        p.grad = torch.from_numpy(g.copy())
+        opt.step()
+        if kind.startswith("adam"):
+            orc.adam_step_master("fp32", w, g, a, b, step=t, **hp)
+        else:
+            orc.sgd_step_master("fp32", w, g, a, first_step=(t == 1), **hp)
+        wmax = np.maximum(wmax, np.abs(w))
+    ref = p.detach().numpy().astype(np.float64)
+    err = np.abs(w.astype(np.float64) - ref)
+    # a few binary32 ulps of the weight per step at most (torch's CPU kernels may contract)
+    assert (err <= 2 * T * _ulp32(wmax)).all(), err.max()
+    assert np.median(err / _ulp32(wmax)) <= 1.0
+
+
+# ------------------------------------------------------------------------------ norm ------
+def test_norm_exact_sum_construction(orc):
+    # all |g| equal to one power of two: every partial sum is exact in any order
+    n = 100_000
+    sign = synth.rng(5, 5).integers(0, 2, size=n).astype(np.float32) * 2 - 1
+    g = (sign * f32(2.0 ** -7)).astype(np.float32)
+    for fmt in ("fp16", "bf16"):
+        g16 = orc.cast16(fmt, g)
+        assert orc.sumsq(fmt, g16) == n * 2.0 ** -14
+        assert orc.sumsq(fmt, g16, grad_scale=0.5) == n * 2.0 ** -16
+    assert orc.sumsq("fp32", g) == n * 2.0 ** -14
+    assert orc.sumsq("fp32", np.zeros(0, np.float32)) == 0.0
+
+
+def test_norm_matches_fsum(orc):
+    g = synth.grads(1 << 18, 1.0, "fp32", 2023, 3)
+    s = orc.sumsq("fp32", g)
+    ref = math.fsum((g.astype(np.float64) ** 2).tolist())
+    assert abs(s - ref) <= 1e-15 * ref
+
+
+def test_clip_coef_closed_forms(orc):
+    # coef = min(1, max_norm / (norm + 1e-6))  (torch clip_grad_norm_, reading R9)
+    assert orc.clip_coef(4.0, 1.0) == f32(1.0 / (2.0 + 1e-6))
+    assert orc.clip_coef(0.25, 1.0) == 1.0
+    # torch's formula clips slightly even at norm == max_norm
+    assert orc.clip_coef(1.0, 1.0) < 1.0
+    assert orc.clip_coef(0.0, 1.0) == 1.0
+    assert math.isnan(orc.clip_coef(float("nan"), 1.0))
+    assert orc.clip_coef(float("inf"), 1.0) == 0.0
+
+
+def test_clip_applied_in_step(orc):
+    n = 1024
+    w0 = synth.weights(n)
+    g = synth.grads(n, 1e-2, "fp32", 1, 1)
+    c = orc.clip_coef(orc.sumsq("fp32", g), 0.01)
+    assert c < 1.0
+    a = w0.copy(); b = w0.copy()
+    m1 = np.zeros(n, np.float32); v1 = np.zeros(n, np.float32)
+    m2 = np.zeros(n, np.float32); v2 = np.zeros(n, np.float32)
+    orc.adam_step_master("fp32", a, g, m1, v1, lr=1e-3, clip_coef=c)
+    orc.adam_step_master("fp32", b, (g * f32(c)).astype(np.float32), m2, v2, lr=1e-3)
+    assert np.array_equal(a, b) and np.array_equal(m1, m2)
+
+
+# ----------------------------------------------------------------------------------- P9 --
+def test_p9_byte_model(orc):
+    # fp32 value + 16-bit copy = 6 B, grad "usually 4 bytes"; P:15 Adam state 8 B
+    assert orc.bytes_per_param("amp", "adam") == 18
+    assert orc.bytes_per_param("amp", "sgd_momentum") == 14
+    # "at least 6 bytes less" with the residual and the fused backward
+    assert orc.bytes_per_param("amp", "adam") - orc.bytes_per_param("ours_fused_backward", "adam") >= 6
+    assert orc.bytes_per_param("ours_fused_backward", "adam") == 12
+    assert orc.bytes_per_param("ours_fused_backward", "sgd_momentum") == 8
+    assert orc.bytes_per_param("ours_multi_tensor", "adam") == 14
