@@ -1,0 +1,186 @@
+/*
+ * mpo.h -- C ABI of the residual-compensated 16-bit optimizer step (arXiv 2309.12381,
+ * "16-bit-only mixed precision"), B200 / sm_100a.
+ *
+ * Citation keys: "P:n" = /root/reference/PAPER.md line n (the section is named alongside),
+ * "R<k>" = a reading of a paper-silent point, listed in DESIGN.md section 3.
+ *
+ * What the library computes (sec. "16bits only Mixed-Precision"): every parameter is
+ * held as a 16-bit value (fp16 or bf16; "the 16bits value used in the computations")
+ * plus a 16-bit residual ("storing only the difference between the two formats").  An
+ * operation reconstructs the fp32 weight from value + residual, "performs the operation in
+ * full precision using the extra bits saved separately and outputs both the updated 16 bits
+ * float and its extra bits".  The operations are the "classic optimizers (Adam and
+ * SGD)", applied either to all parameters "as one only stream of values" (the
+ * fused / multi-tensor form), or per parameter from inside backward, or (not in the
+ * paper; BASELINE.json north_star (c)) to one shard of a flat parameter buffer per GPU.
+ *
+ * Representation (readings R1-R5):
+ *   value    = IEEE-754 round-to-nearest-even of the fp32 weight x to fp16 / bf16 (R2);
+ *              NaN -> 0x7FFF (R4); overflow -> +-Inf (IEEE).
+ *   residual = int16, sat16( bits32(x) - bits32(widen(value)) ), the signed difference of the
+ *              two binary32 bit patterns (R1), saturated to [-32768, 32767] (R3); 0 for NaN/Inf.
+ *   reconstruct(value, residual) = f32( bits32(widen(value)) + residual ); NaN -> 0x7FFFFFFF.
+ *   This is lossless for bf16 except on the 32 640 RNE upper-tie patterns (1 ulp32 low, R3),
+ *   and for fp16 on 2^-16 <= |x| < 65520 (R5).
+ *
+ * Conventions shared by every entry point:
+ *   * All array arguments are DEVICE pointers to caller-owned memory (e.g. torch tensors).
+ *     The library keeps no reference after return and allocates nothing persistent.
+ *   * Every array base pointer must be 16-byte aligned (MPO_EALIGN otherwise); lengths are
+ *     arbitrary (ragged tails are handled element by element).  Arrays must not alias.
+ *   * Calls are ASYNCHRONOUS: they validate, enqueue kernels (and NCCL collectives) on
+ *     `stream` and return.  Asynchronous device faults surface at the caller's next sync.
+ *   * In place on value / residual / optimizer state; gradients are read-only, except that
+ *     mpo_sharded_step reduce-scatters into its grad_flat argument.
+ *   * Hyper-parameters arrive as doubles.  The library derives every kernel scalar on the host
+ *     in double and rounds it ONCE to float (R7); the device never calls pow().
+ *   * Errors are status codes; nothing aborts or throws across the ABI.  mpo_last_error()
+ *     returns a thread-local message describing the last non-OK status (validation errors in
+ *     a tensor table name the offending table index).  NaN/Inf in gradients is NOT an error:
+ *     it propagates into the weights (training-divergence signal left to the caller).
+ *
+ * Two builds of the same sources are shipped: libmpo.so (default FMA contraction) and
+ * libmpo_exact.so (-fmad=false, bit-exact to the CPU oracle for every entry point).
+ */
+#ifndef MPO_H
+#define MPO_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* The stream is a cudaStream_t; declared opaque so this header needs no CUDA include. */
+typedef void* mpo_stream;
+
+typedef enum {
+    MPO_OK = 0,
+    MPO_EINVAL = 1,   /* bad enum, negative size, non-finite hyper-parameter, bad sharding */
+    MPO_EALIGN = 2,   /* an array base pointer is not 16-byte aligned                      */
+    MPO_EDTYPE = 3,   /* value dtype not FP16/BF16, or unsupported grad dtype              */
+    MPO_ECUDA = 4,    /* kernel launch failed (cudaGetLastError)                            */
+    MPO_ENCCL = 5     /* an NCCL call failed (message from ncclGetErrorString)              */
+} mpo_status;
+
+typedef enum { MPO_FP16 = 0, MPO_BF16 = 1, MPO_FP32 = 2 } mpo_dtype;  /* value: FP16|BF16 */
+typedef enum { MPO_SGD = 0, MPO_ADAM = 1 } mpo_optim;
+
+/* One parameter tensor of a multi-tensor table ("one only stream of values").
+ *   value : n 16-bit values (dtype vdt), updated in place
+ *   resid : n int16 residuals, updated in place
+ *   grad  : n gradients (dtype gdt: FP16, BF16 or FP32), read-only
+ *   m     : n fp32 -- SGD momentum buffer, or Adam first moment (NULL for SGD without momentum)
+ *   v     : n fp32 -- Adam second moment (ignored by SGD)
+ *   n     : element count (>= 0)
+ *   hp    : index into the hyper-parameter group array of the call                        */
+typedef struct {
+    void* value;
+    int16_t* resid;
+    const void* grad;
+    float* m;
+    float* v;
+    int64_t n;
+    int32_t hp;
+    int32_t _pad;
+} mpo_tensor;
+
+/* torch.optim.SGD semantics (R6; "classic optimizers"; P:19 drop-in hyper-parameters).
+ * grad_scale multiplies the incoming gradient first (loss-scale unscale, 1/N data-parallel
+ * mean; "every operations on the gradient (eg. clipping or scaling) has to be done
+ * through the optimizer").  first_step != 0: the momentum buffer is initialised to the
+ * gradient (torch's clone on the first step) and is not read. */
+typedef struct {
+    double lr, momentum, dampening, weight_decay, grad_scale;
+    int32_t nesterov, first_step;
+} mpo_sgd_hp;
+
+/* torch.optim.Adam / AdamW semantics (R6).  step is 1-based (bias correction).  adamw != 0:
+ * decoupled decay w *= (1 - lr*weight_decay); else L2 (g += weight_decay*w).
+ * max_grad_norm > 0 enables global-norm clipping (R9; multi-tensor and sharded modes only,
+ * P:93 "prohibits any operation that would require every gradients of the model at the same
+ * time"); the same value must then be given to every group of the call. */
+typedef struct {
+    double lr, beta1, beta2, eps, weight_decay, grad_scale, max_grad_norm;
+    int32_t adamw, _pad;
+    int64_t step;
+} mpo_adam_hp;
+
+/* Largest number of hyper-parameter groups one call may carry. */
+#define MPO_MAX_HP_GROUPS 16
+
+/* Split fp32 weights into (16-bit value, int16 residual) (readings R1-R5).
+ *   vdt   : MPO_FP16 | MPO_BF16
+ *   w     : n fp32 (device, read-only);  value: n 16-bit (device, written);  resid: n int16 */
+mpo_status mpo_split(mpo_dtype vdt, const float* w, void* value, int16_t* resid, int64_t n,
+                     mpo_stream stream);
+
+/* Reconstruct the fp32 weights from value + residual ("performs the operation in full
+ * precision using the extra bits saved separately").  value/resid read-only, w written. */
+mpo_status mpo_reconstruct(mpo_dtype vdt, const void* value, const int16_t* resid, float* w,
+                           int64_t n, mpo_stream stream);
+
+/* Residual-compensated SGD(-momentum) step over a table of nt tensors, one fused launch per
+ * table slice.  hp: nhp groups (1 <= nhp <= MPO_MAX_HP_GROUPS) in HOST memory;
+ * t: nt entries in HOST memory (copied into the launch; not retained). */
+mpo_status mpo_sgd_step(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t, int32_t nt,
+                        const mpo_sgd_hp* hp, int32_t nhp, mpo_stream stream);
+
+/* Residual-compensated Adam/AdamW step over a table of nt tensors.
+ * norm_ws: DEVICE scratch of at least mpo_norm_ws_doubles() doubles, required iff
+ * max_grad_norm > 0 (global-norm clipping: fp64 sum of squares of the scaled gradients over
+ * the whole table, coef = min(1, max_norm / (sqrt(S) + 1e-6)), R9).  On return (stream
+ * order) norm_ws[0] holds S. */
+mpo_status mpo_adam_step(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t, int32_t nt,
+                         const mpo_adam_hp* hp, int32_t nhp, double* norm_ws,
+                         mpo_stream stream);
+
+/* Doubles of device scratch mpo_adam_step / mpo_sharded_step need for clipping. */
+int64_t mpo_norm_ws_doubles(void);
+
+/* Fused backward + optimizer step for ONE parameter, called from its post-accumulate-grad hook
+ * ("operate the optimization step as soon as the gradient is computed").
+ *   kind : MPO_SGD (hp -> mpo_sgd_hp) | MPO_ADAM (hp -> mpo_adam_hp), hp in HOST memory
+ *   one  : the parameter's table entry (its hp field is ignored)
+ * Global operations are impossible here: MPO_EINVAL if max_grad_norm > 0.
+ * The caller frees the gradient right after the call; stream order makes that safe. */
+mpo_status mpo_fused_backward_hook_step(mpo_optim kind, mpo_dtype vdt, mpo_dtype gdt,
+                                        const mpo_tensor* one, const void* hp,
+                                        mpo_stream stream);
+
+/* Data-parallel sharded step (not in the paper, which lists distribution as future work,
+ * P:196; BASELINE.json north_star (c)).  Collective: every rank calls it with the same
+ * arguments except rank and its own buffers.
+ *   nccl_comm   : an ncclComm_t (borrowed, e.g. from torch's ProcessGroupNCCL; never freed)
+ *   value_flat  : n_total 16-bit values, replicated on every rank (all-gathered on return)
+ *   grad_flat   : n_total 16-bit gradients of THIS rank (same dtype as value); overwritten:
+ *                 shard `rank` becomes the reduced (summed) gradient
+ *   resid_shard, m_shard, v_shard : n_total/world entries of this rank's shard (v ignored,
+ *                 m may be NULL, for SGD without momentum)
+ *   n_total     : multiple of 8*world
+ *   hp          : mpo_sgd_hp* | mpo_adam_hp* (HOST); grad_scale should be 1/world for a mean
+ *   norm_ws     : as for mpo_adam_step (clipping: the shard sums are all-reduced in fp64)
+ * Sequence on `stream`: ncclReduceScatter(sum) -> [sumsq + ncclAllReduce] -> step on the shard
+ * -> ncclAllGather of the 16-bit values only. */
+mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t rank, int32_t world,
+                            mpo_dtype vdt, void* value_flat, void* grad_flat,
+                            int16_t* resid_shard, float* m_shard, float* v_shard,
+                            int64_t n_total, const void* hp, double* norm_ws,
+                            mpo_stream stream);
+
+/* Thread-local description of the last non-OK status ("" if none). */
+const char* mpo_last_error(void);
+
+/* 1 if this build was compiled with -fmad=false (bit-exact mode), else 0. */
+int32_t mpo_build_exact(void);
+
+/* Number of kernels this library launched since load (for the bench's gpu_launches claim). */
+int64_t mpo_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPO_H */

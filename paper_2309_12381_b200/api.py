@@ -1,0 +1,230 @@
+"""Thin Python binding of include/mpo.h: the same entry points, torch tensors in, pointers out.
+
+Only argument marshalling happens here (pointer/size/enum extraction, hyper-parameter structs,
+the current CUDA stream); every step of the path runs in libmpo's kernels.  PyTorch supplies
+device memory, streams and process groups.  Citations as in include/mpo.h.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib
+from ._lib import MPO_ADAM, MPO_BF16, MPO_FP16, MPO_FP32, MPO_SGD, AdamHP, MpoError, SgdHP, Tensor
+
+_DT = {torch.float16: MPO_FP16, torch.bfloat16: MPO_BF16, torch.float32: MPO_FP32}
+_VALUE_VIEW = {torch.float16, torch.bfloat16}
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    try:
+        return _DT[dt]
+    except KeyError:
+        raise MpoError(_lib.MPO_EDTYPE, f"unsupported dtype {dt}") from None
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise MpoError(_lib.MPO_EINVAL, "tensor is not on a CUDA device (no CPU path)")
+    if not t.is_contiguous():
+        raise MpoError(_lib.MPO_EINVAL, "tensor is not contiguous")
+    return t.data_ptr()
+
+
+def _lib_of(exact: bool):
+    return _lib.load(exact)
+
+
+# ------------------------------------------------------------------------------------------
+# Hyper-parameter structs
+# ------------------------------------------------------------------------------------------
+@dataclass
+class SgdParams:
+    lr: float
+    momentum: float = 0.0
+    dampening: float = 0.0
+    weight_decay: float = 0.0
+    grad_scale: float = 1.0
+    nesterov: bool = False
+    first_step: bool = False
+
+    def c(self) -> SgdHP:
+        return SgdHP(self.lr, self.momentum, self.dampening, self.weight_decay, self.grad_scale,
+                     int(self.nesterov), int(self.first_step))
+
+
+@dataclass
+class AdamParams:
+    lr: float
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+    grad_scale: float = 1.0
+    max_grad_norm: float = 0.0
+    adamw: bool = True
+    step: int = 1
+
+    def c(self) -> AdamHP:
+        return AdamHP(self.lr, self.beta1, self.beta2, self.eps, self.weight_decay, self.grad_scale,
+                      self.max_grad_norm, int(self.adamw), 0, int(self.step))
+
+
+def _hp_array(hps, kind):
+    if isinstance(hps, (SgdParams, AdamParams)):
+        hps = [hps]
+    arr = (kind * len(hps))()
+    for i, h in enumerate(hps):
+        arr[i] = h.c()
+    return arr, len(hps)
+
+
+# ------------------------------------------------------------------------------------------
+# Multi-tensor table
+# ------------------------------------------------------------------------------------------
+class TensorTable:
+    """A packed mpo_tensor array ("one only stream of values").
+
+    Rows are (value, resid, grad, m, v, hp_index); the tensors are referenced, not copied, and the
+    row pointers are cached so a step does not rebuild the table.  ``set_grads`` refreshes only
+    the gradient pointers."""
+
+    def __init__(self, values: Sequence[torch.Tensor], resids: Sequence[torch.Tensor],
+                 grads: Sequence[Optional[torch.Tensor]], ms: Sequence[Optional[torch.Tensor]],
+                 vs: Sequence[Optional[torch.Tensor]], hp_index: Optional[Sequence[int]] = None):
+        n = len(values)
+        if not (len(resids) == len(grads) == len(ms) == len(vs) == n):
+            raise MpoError(_lib.MPO_EINVAL, "table columns differ in length")
+        self.values, self.resids, self.ms, self.vs = list(values), list(resids), list(ms), list(vs)
+        self.grads = list(grads)
+        self.hp_index = list(hp_index) if hp_index is not None else [0] * n
+        self.arr = (Tensor * max(n, 1))()
+        self.nt = n
+        self.vdt = dtype_code(values[0].dtype) if n else MPO_FP16
+        for i in range(n):
+            v, r = values[i], resids[i]
+            if v.dtype not in _VALUE_VIEW or r.dtype != torch.int16 or v.numel() != r.numel():
+                raise MpoError(_lib.MPO_EDTYPE, f"tensor {i}: value must be fp16/bf16 and resid int16 of equal size")
+            if dtype_code(v.dtype) != self.vdt:
+                raise MpoError(_lib.MPO_EDTYPE, f"tensor {i}: mixed value dtypes in one table")
+            row = self.arr[i]
+            row.value = _ptr(v)
+            row.resid = _ptr(r)
+            row.m = _ptr(ms[i])
+            row.v = _ptr(vs[i])
+            row.n = v.numel()
+            row.hp = self.hp_index[i]
+        self.gdt = None
+        self.set_grads(grads)
+
+    def set_grads(self, grads: Sequence[Optional[torch.Tensor]]):
+        gdt = None
+        for i, g in enumerate(grads):
+            if g is None:
+                raise MpoError(_lib.MPO_EINVAL, f"tensor {i}: missing gradient")
+            if g.numel() != self.arr[i].n:
+                raise MpoError(_lib.MPO_EINVAL, f"tensor {i}: gradient size mismatch")
+            c = dtype_code(g.dtype)
+            if gdt is None:
+                gdt = c
+            elif c != gdt:
+                raise MpoError(_lib.MPO_EDTYPE, f"tensor {i}: mixed gradient dtypes in one table")
+            self.arr[i].grad = _ptr(g)
+        self.grads = list(grads)
+        self.gdt = gdt if gdt is not None else self.vdt
+
+
+# ------------------------------------------------------------------------------------------
+# Entry points (same names as the C ABI)
+# ------------------------------------------------------------------------------------------
+def mpo_split(w: torch.Tensor, fmt: torch.dtype, value: Optional[torch.Tensor] = None,
+              resid: Optional[torch.Tensor] = None, stream=None, exact: bool = False):
+    """fp32 -> (16-bit value, int16 residual)."""
+    if w.dtype != torch.float32:
+        raise MpoError(_lib.MPO_EDTYPE, "split input must be fp32")
+    if value is None:
+        value = torch.empty(w.shape, dtype=fmt, device=w.device)
+    if resid is None:
+        resid = torch.empty(w.shape, dtype=torch.int16, device=w.device)
+    L = _lib_of(exact)
+    _lib.check(L, L.mpo_split(dtype_code(value.dtype), _ptr(w), _ptr(value), _ptr(resid), w.numel(),
+                              _stream(stream)))
+    return value, resid
+
+
+def mpo_reconstruct(value: torch.Tensor, resid: torch.Tensor, out: Optional[torch.Tensor] = None,
+                    stream=None, exact: bool = False) -> torch.Tensor:
+    """(16-bit value, int16 residual) -> fp32."""
+    if out is None:
+        out = torch.empty(value.shape, dtype=torch.float32, device=value.device)
+    if value.numel() != resid.numel() or value.numel() != out.numel():
+        raise MpoError(_lib.MPO_EINVAL, "size mismatch")
+    L = _lib_of(exact)
+    _lib.check(L, L.mpo_reconstruct(dtype_code(value.dtype), _ptr(value), _ptr(resid), _ptr(out), value.numel(),
+                                    _stream(stream)))
+    return out
+
+
+def mpo_sgd_step(table: TensorTable, hps, stream=None, exact: bool = False):
+    """Residual-compensated SGD(-momentum) step over a table."""
+    arr, nhp = _hp_array(hps, SgdHP)
+    L = _lib_of(exact)
+    _lib.check(L, L.mpo_sgd_step(table.vdt, table.gdt, table.arr, table.nt, arr, nhp, _stream(stream)))
+
+
+def mpo_adam_step(table: TensorTable, hps, norm_ws: Optional[torch.Tensor] = None, stream=None,
+                  exact: bool = False):
+    """Residual-compensated Adam/AdamW step over a table; clipping needs norm_ws."""
+    arr, nhp = _hp_array(hps, AdamHP)
+    L = _lib_of(exact)
+    if norm_ws is not None and (norm_ws.dtype != torch.float64 or norm_ws.numel() < norm_ws_doubles()):
+        raise MpoError(_lib.MPO_EINVAL, "norm_ws must be a float64 tensor of norm_ws_doubles() entries")
+    _lib.check(L, L.mpo_adam_step(table.vdt, table.gdt, table.arr, table.nt, arr, nhp, _ptr(norm_ws),
+                                  _stream(stream)))
+
+
+def mpo_fused_backward_hook_step(kind: int, vdt: int, gdt: int, one: Tensor, hp, stream=None,
+                                 exact: bool = False):
+    """One parameter's step from its post-accumulate-grad hook.  ``one`` is an
+    mpo_tensor row, ``hp`` an SgdHP / AdamHP struct (kept by the caller)."""
+    L = _lib_of(exact)
+    _lib.check(L, L.mpo_fused_backward_hook_step(kind, vdt, gdt, C.byref(one), C.byref(hp), _stream(stream)))
+
+
+def mpo_sharded_step(kind: int, comm_ptr: int, rank: int, world: int, value_flat: torch.Tensor,
+                     grad_flat: torch.Tensor, resid_shard: torch.Tensor, m_shard: Optional[torch.Tensor],
+                     v_shard: Optional[torch.Tensor], hp, norm_ws: Optional[torch.Tensor] = None, stream=None,
+                     exact: bool = False):
+    """Data-parallel sharded step: RS(grad) -> shard update -> AG(value) (BASELINE north_star (c))."""
+    if grad_flat.dtype != value_flat.dtype or grad_flat.numel() != value_flat.numel():
+        raise MpoError(_lib.MPO_EINVAL, "grad_flat must match value_flat in dtype and size")
+    L = _lib_of(exact)
+    chp = hp.c() if hasattr(hp, "c") else hp
+    _lib.check(L, L.mpo_sharded_step(kind, comm_ptr, rank, world, dtype_code(value_flat.dtype), _ptr(value_flat),
+                                     _ptr(grad_flat), _ptr(resid_shard), _ptr(m_shard), _ptr(v_shard),
+                                     value_flat.numel(), C.byref(chp), _ptr(norm_ws), _stream(stream)))
+
+
+def norm_ws_doubles(exact: bool = False) -> int:
+    return int(_lib_of(exact).mpo_norm_ws_doubles())
+
+
+def launch_count(exact: bool = False) -> int:
+    return int(_lib_of(exact).mpo_launch_count())
+
+
+def build_exact(exact: bool) -> int:
+    return int(_lib_of(exact).mpo_build_exact())

@@ -1,0 +1,159 @@
+"""The C-ABI boundary on CPU (no GPU): the library loads, exports every symbol include/mpo.h
+declares, validates arguments with the documented status codes before touching the device, and
+the product package never reaches the oracle."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mpo.h")
+PKG = os.path.join(ROOT, "paper_2309_12381_b200")
+
+
+@pytest.fixture(scope="module")
+def libs():
+    from paper_2309_12381_b200 import _build, _lib
+    _build.build()
+    return _lib, _lib.load(False), _lib.load(True)
+
+
+def header_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mpo_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_lists_the_north_star_entry_points():
+    fns = header_functions()
+    for f in ("mpo_split", "mpo_reconstruct", "mpo_sgd_step", "mpo_adam_step", "mpo_fused_backward_hook_step",
+              "mpo_sharded_step"):
+        assert f in fns
+
+
+def test_every_declared_symbol_is_exported(libs):
+    _lib, fma, exact = libs
+    fns = header_functions()
+    assert sorted(_lib.SYMBOLS) == fns
+    for L in (fma, exact):
+        for f in fns:
+            assert hasattr(L, f), f
+
+
+def test_build_flavours(libs):
+    _lib, fma, exact = libs
+    assert fma.mpo_build_exact() == 0
+    assert exact.mpo_build_exact() == 1
+    assert fma.mpo_norm_ws_doubles() >= 2
+
+
+def test_sm100a_sass_present(libs):
+    """The library carries sm_100a SASS (cuobjdump), not just PTX."""
+    import subprocess
+    from paper_2309_12381_b200 import _build
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _build.lib_path(False)],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def _status(L, rc):
+    return rc, L.mpo_last_error().decode()
+
+
+def test_validation_errors(libs):
+    _lib, L, _ = libs
+    T, S, A = _lib.Tensor, _lib.SgdHP, _lib.AdamHP
+    # bad value dtype
+    rc, msg = _status(L, L.mpo_split(_lib.MPO_FP32, 16, 16, 16, 8, None))
+    assert rc == _lib.MPO_EDTYPE and "value dtype" in msg
+    # negative size
+    rc, msg = _status(L, L.mpo_reconstruct(_lib.MPO_BF16, 16, 16, 16, -1, None))
+    assert rc == _lib.MPO_EINVAL
+    # misaligned pointer
+    rc, msg = _status(L, L.mpo_split(_lib.MPO_FP16, 16, 18, 32, 8, None))
+    assert rc == _lib.MPO_EALIGN
+    # n == 0 is a no-op (OK) even with NULL pointers
+    assert L.mpo_split(_lib.MPO_FP16, None, None, None, 0, None) == _lib.MPO_OK
+    # table errors name the offending index
+    tab = (T * 2)()
+    for i in range(2):
+        tab[i].value, tab[i].resid, tab[i].grad, tab[i].m, tab[i].v, tab[i].n = 16, 32, 48, 64, 80, 8
+    tab[1].resid = 34
+    hp = A(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1)
+    rc, msg = _status(L, L.mpo_adam_step(_lib.MPO_BF16, _lib.MPO_BF16, tab, 2, C.byref(hp), 1, None, None))
+    assert rc == _lib.MPO_EALIGN and "tensor 1" in msg
+    tab[1].resid = 32
+    tab[1].hp = 3
+    rc, msg = _status(L, L.mpo_adam_step(_lib.MPO_BF16, _lib.MPO_BF16, tab, 2, C.byref(hp), 1, None, None))
+    assert rc == _lib.MPO_EINVAL and "tensor 1" in msg
+    tab[1].hp = 0
+    # non-finite hyper-parameters rejected
+    bad = A(float("nan"), 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1)
+    rc, msg = _status(L, L.mpo_adam_step(_lib.MPO_BF16, _lib.MPO_BF16, tab, 2, C.byref(bad), 1, None, None))
+    assert rc == _lib.MPO_EINVAL and "non-finite" in msg
+    # step must be >= 1
+    bad = A(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 0)
+    assert L.mpo_adam_step(_lib.MPO_BF16, _lib.MPO_BF16, tab, 2, C.byref(bad), 1, None, None) == _lib.MPO_EINVAL
+    # unsupported grad dtype
+    rc, _ = _status(L, L.mpo_adam_step(_lib.MPO_BF16, 7, tab, 2, C.byref(hp), 1, None, None))
+    assert rc == _lib.MPO_EDTYPE
+    # clipping without a workspace
+    clip = A(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 1.0, 1, 0, 1)
+    assert L.mpo_adam_step(_lib.MPO_BF16, _lib.MPO_BF16, tab, 2, C.byref(clip), 1, None, None) == _lib.MPO_EINVAL
+    # group count out of range
+    assert L.mpo_adam_step(_lib.MPO_BF16, _lib.MPO_BF16, tab, 2, C.byref(hp), 0, None, None) == _lib.MPO_EINVAL
+    # SGD: nesterov without momentum
+    s = S(0.1, 0.0, 0.0, 0.0, 1.0, 1, 0)
+    rc, msg = _status(L, L.mpo_sgd_step(_lib.MPO_FP16, _lib.MPO_FP16, tab, 2, C.byref(s), 1, None))
+    assert rc == _lib.MPO_EINVAL and "nesterov" in msg
+
+
+def test_hook_refuses_global_clipping(libs):
+    """P:93 / P:186: global operations are impossible inside the fused backward."""
+    _lib, L, _ = libs
+    one = _lib.Tensor(16, 32, 48, 64, 80, 8, 0, 0)
+    clip = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 1.0, 1, 0, 1)
+    rc, msg = _status(L, L.mpo_fused_backward_hook_step(_lib.MPO_ADAM, _lib.MPO_BF16, _lib.MPO_BF16, C.byref(one),
+                                                        C.byref(clip), None))
+    assert rc == _lib.MPO_EINVAL and "P:186" in msg
+    assert L.mpo_fused_backward_hook_step(9, _lib.MPO_BF16, _lib.MPO_BF16, C.byref(one), C.byref(clip),
+                                          None) == _lib.MPO_EINVAL
+
+
+def test_sharded_validation(libs):
+    _lib, L, _ = libs
+    hp = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1)
+    args = lambda comm, rank, world, n: (_lib.MPO_ADAM, comm, rank, world, _lib.MPO_BF16, 16, 32, 48, 64, 80, n,
+                                         C.byref(hp), None, None)
+    assert L.mpo_sharded_step(*args(0, 0, 2, 32)) == _lib.MPO_EINVAL          # NULL comm
+    assert L.mpo_sharded_step(*args(1, 2, 2, 32)) == _lib.MPO_EINVAL          # rank >= world
+    rc, msg = _status(L, L.mpo_sharded_step(*args(1, 0, 2, 24)))             # 24 not a multiple of 16
+    assert rc == _lib.MPO_EINVAL and "8*world" in msg
+    assert L.mpo_sharded_step(*args(1, 0, 2, 0)) == _lib.MPO_OK               # empty
+
+
+def test_product_never_touches_the_oracle():
+    """Only tests/, __graft_entry__.smoke() and bench.py's CPU legs may use oracle/."""
+    for dirpath, _, files in os.walk(PKG):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"\boracle\b", src.replace("CPU oracle", "").replace("the oracle", "")), f
+    assert "oracle" not in open(HEADER).read().replace("CPU oracle", "")
+
+
+def test_python_binding_fails_loudly_without_library(tmp_path, monkeypatch):
+    from paper_2309_12381_b200 import _build, _lib
+    monkeypatch.setattr(_build, "lib_path", lambda exact=False: str(tmp_path / "missing.so"))
+    monkeypatch.setattr(_lib, "_libs", {})
+    with pytest.raises(ImportError, match="no CPU fallback"):
+        _lib.load(False)
+
+
+def test_cpu_tensors_are_rejected():
+    import torch
+    from paper_2309_12381_b200 import MpoError, mpo_split
+    with pytest.raises(MpoError, match="CUDA"):
+        mpo_split(torch.zeros(8), torch.bfloat16, value=torch.zeros(8, dtype=torch.bfloat16),
+                  resid=torch.zeros(8, dtype=torch.int16))

@@ -1,0 +1,208 @@
+"""GPU: the three delivery modes agree bitwise (SURVEY 8(c) pin P8) and the optimizer objects
+behave as documented.
+
+* hook mode (step inside backward from post-accumulate-grad hooks) == two-phase
+  backward + multi-tensor step, with no gradient left allocated after backward;
+* sharded step (RS -> shard update -> AG over NCCL) at world_size 1 == unsharded step;
+* the user-facing optimizers reproduce the oracle (exact build).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.nn as nn
+
+import synth
+from gpu_util import host16
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mpo():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2309_12381_b200 as m
+    from paper_2309_12381_b200 import _build
+    _build.build()
+    return m
+
+
+class TinyLM(nn.Module):
+    """GPT-like toy with a tied embedding / output matrix (weight sharing)."""
+
+    def __init__(self, vocab=257, d=64):
+        super().__init__()
+        self.emb = nn.Embedding(vocab, d)
+        self.ln = nn.LayerNorm(d)
+        self.fc1 = nn.Linear(d, 4 * d)
+        self.fc2 = nn.Linear(4 * d, d)
+
+    def forward(self, idx):
+        x = self.emb(idx)
+        x = x + self.fc2(torch.nn.functional.gelu(self.fc1(self.ln(x))))
+        return x @ self.emb.weight.t()
+
+
+def _loss(model, idx):
+    logits = model(idx[:, :-1]).float()
+    return torch.nn.functional.cross_entropy(logits.reshape(-1, logits.shape[-1]), idx[:, 1:].reshape(-1))
+
+
+def _pair(fmt, kind, mpo, **kw):
+    torch.manual_seed(0)
+    a = TinyLM().cuda()
+    b = TinyLM().cuda()
+    b.load_state_dict(a.state_dict())
+    mk = (lambda ps: mpo.ResidualAdamW(ps, fmt=fmt, **kw)) if kind == "adam" else \
+        (lambda ps: mpo.ResidualSGD(ps, fmt=fmt, **kw))
+    return a, b, mk(a.parameters()), mk(b.parameters())
+
+
+@pytest.mark.parametrize("fmt", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("kind", ["adam", "sgd"])
+def test_hook_mode_equals_two_phase(mpo, fmt, kind):
+    kw = dict(lr=1e-3, weight_decay=0.1) if kind == "adam" else dict(lr=0.1, momentum=0.9, weight_decay=1e-4)
+    a, b, oa, ob = _pair(fmt, kind, mpo, **kw)
+    ob.install_backward_hooks()
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    for step in range(4):
+        idx = torch.randint(0, 257, (4, 33), device="cuda", generator=gen)
+        la = _loss(a, idx)
+        la.backward()
+        oa.step()
+        for p in a.parameters():
+            p.grad = None
+        lb = _loss(b, idx)
+        assert torch.equal(la, lb)          # same weights going in
+        lb.backward()
+        for p in b.parameters():
+            assert p.grad is None           # consumed and freed inside backward
+    for (na, pa), (nb, pb) in zip(a.named_parameters(), b.named_parameters()):
+        assert torch.equal(pa.view(torch.int16), pb.view(torch.int16)), na
+        sa, sb = oa.state[pa], ob.state[pb]
+        assert torch.equal(sa["resid"], sb["resid"]), na
+        assert sa["step"] == sb["step"] == 4
+        for k in ("m", "v"):
+            if sa.get(k) is not None:
+                assert torch.equal(sa[k], sb[k]), (na, k)
+
+
+def test_hook_mode_refuses_clipping(mpo):
+    a = TinyLM().cuda()
+    opt = mpo.ResidualAdamW(a.parameters(), fmt=torch.bfloat16, max_grad_norm=1.0)
+    with pytest.raises(mpo.MpoError, match="P:186"):
+        opt.install_backward_hooks()
+
+
+def test_hook_mode_peak_gradient_memory(mpo):
+    """No gradient buffer persists: after backward nothing is held, and backward's peak is below
+    the two-phase peak by roughly the gradient bytes."""
+    torch.manual_seed(0)
+    d = 1024
+    make = lambda: nn.Sequential(*[nn.Linear(d, d, bias=False) for _ in range(8)]).cuda()
+    a, b = make(), make()
+    b.load_state_dict(a.state_dict())
+    oa = mpo.ResidualAdamW(a.parameters(), fmt=torch.bfloat16)
+    ob = mpo.ResidualAdamW(b.parameters(), fmt=torch.bfloat16)
+    ob.install_backward_hooks()
+    x = torch.randn(64, d, device="cuda", dtype=torch.bfloat16)
+    peaks = []
+    for model, opt, hooks in ((a, oa, False), (b, ob, True)):
+        torch.cuda.synchronize()
+        base = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        model(x).float().square().mean().backward()
+        if not hooks:
+            opt.step()
+        torch.cuda.synchronize()
+        peaks.append(torch.cuda.max_memory_allocated() - base)
+        held = sum(p.grad.numel() * 2 for p in model.parameters() if p.grad is not None)
+        assert held == (0 if hooks else 8 * d * d * 2)
+    grad_bytes = 8 * d * d * 2
+    assert peaks[0] - peaks[1] >= grad_bytes - 2 * d * d * 2
+
+
+def test_optimizer_matches_oracle(mpo, orc):
+    """ResidualAdamW / ResidualSGD on fp32 init (split on the GPU) == oracle, 3 steps, exact build."""
+    fmt = "bf16"
+    n = 10007
+    w = synth.weights(n, 0.02, 0xB0B)
+    for kind in ("adam", "sgd"):
+        p = nn.Parameter(torch.from_numpy(w.copy()).cuda())
+        if kind == "adam":
+            opt = mpo.ResidualAdamW([p], lr=1e-3, betas=(0.9, 0.95), weight_decay=0.1, fmt=torch.bfloat16,
+                                    exact=True)
+        else:
+            opt = mpo.ResidualSGD([p], lr=0.05, momentum=0.9, nesterov=True, fmt=torch.bfloat16, exact=True)
+        h, r = orc.split(fmt, w)
+        m = np.zeros(n, np.float32); v = np.zeros(n, np.float32)
+        for t in range(1, 4):
+            g = synth.grads(n, 1e-2, fmt, 0xB0B, t)
+            p.grad = torch.from_numpy(g.view(np.int16).copy()).view(torch.bfloat16).cuda()
+            opt.step()
+            if kind == "adam":
+                orc.adam_step(fmt, fmt, h, r, g, m, v, lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1,
+                              adamw=True, step=t)
+            else:
+                orc.sgd_step(fmt, fmt, h, r, g, m, lr=0.05, momentum=0.9, nesterov=True, first_step=(t == 1))
+        assert np.array_equal(host16(p.data), h)
+        assert np.array_equal(opt.state[p]["resid"].cpu().numpy(), r)
+        w32 = opt.fp32_params()[0].cpu().numpy()
+        assert np.array_equal(w32.view(np.uint32), orc.reconstruct(fmt, h, r).view(np.uint32))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def nccl1():
+    import torch.distributed as dist
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    yield dist
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["adam", "sgd"])
+@pytest.mark.parametrize("clip", [False, True])
+def test_sharded_world1_equals_unsharded(mpo, nccl1, kind, clip):
+    if kind == "sgd" and clip:
+        pytest.skip("clipping is an Adam option")
+    torch.manual_seed(3)
+    shapes = [(33, 17), (4096,), (5,), (128, 64)]
+    src = [torch.randn(s, device="cuda") * 0.02 for s in shapes]
+    pa = [nn.Parameter(t.clone()) for t in src]
+    pb = [nn.Parameter(t.clone()) for t in src]
+    if kind == "adam":
+        hp = mpo.AdamParams(lr=1e-3, weight_decay=0.1, max_grad_norm=0.05 if clip else 0.0)
+        ref = mpo.ResidualAdamW(pa, lr=1e-3, weight_decay=0.1, fmt=torch.bfloat16,
+                                max_grad_norm=0.05 if clip else None)
+    else:
+        hp = mpo.SgdParams(lr=0.1, momentum=0.9)
+        ref = mpo.ResidualSGD(pa, lr=0.1, momentum=0.9, fmt=torch.bfloat16)
+    sh = mpo.ShardedResidualOptimizer(pb, kind=kind, fmt=torch.bfloat16, hp=hp)
+    for t in range(3):
+        grads = [torch.randn(s, device="cuda").to(torch.bfloat16) * 1e-2 for s in shapes]
+        if clip:   # exact-sum construction: every |g| = 2^-7, so S is exact in any order (P8)
+            grads = [torch.sign(g) * 2.0 ** -7 + (g == 0) * 2.0 ** -7 for g in grads]
+            grads = [g.to(torch.bfloat16) for g in grads]
+        for p, g in zip(pa, grads):
+            p.grad = g.clone()
+        sh.zero_grad()
+        for p, g in zip(pb, grads):
+            p.grad.copy_(g)
+        ref.step()
+        sh.step()
+    for a, b in zip(pa, pb):
+        assert torch.equal(a.data.view(torch.int16), b.data.view(torch.int16))

@@ -1,0 +1,371 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bars (BASELINE.json north_star):
+* split / reconstruct: bit-exact, on all 2^32 binary32 patterns, both builds;
+* every step in libmpo_exact.so (-fmad=false): bit-exact (value, residual; m/v bit-exact with
+  any-NaN-equals-any-NaN);
+* every step in libmpo.so (FMA contraction), one step from identical state: value within 1 ulp16,
+  reconstructed fp32 weight within 1e-6 relative (cancellation carve-out: or within 2 ulp32 of
+  the pre-step weight), m and v within 1e-6 relative.
+"""
+import os
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from synth import workloads
+from gpu_util import (TDT, bits32, dev16, dev_grad, devf, devi16, host16, hostf, same_bits_nan_equal,
+                            ulp16_dist)
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "split_examples.txt")
+
+
+@pytest.fixture(scope="module")
+def mpo():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2309_12381_b200 as m
+    from paper_2309_12381_b200 import _build
+    _build.build()
+    return m
+
+
+# ------------------------------------------------------------------------------------------
+# split / reconstruct
+# ------------------------------------------------------------------------------------------
+def _gpu_split(mpo, x_np, fmt, exact):
+    w = devf(x_np)
+    v, r = mpo.mpo_split(w, TDT[fmt], exact=exact)
+    rec = mpo.mpo_reconstruct(v, r, exact=exact)
+    return host16(v), r.cpu().numpy(), hostf(rec)
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+@pytest.mark.parametrize("exact", [False, True])
+def test_split_reconstruct_all_2_32(mpo, orc, fmt, exact):
+    """Exhaustive: every binary32 pattern splits and reconstructs bit-identically to the oracle."""
+    chunk = 1 << 26
+    lock = threading.Lock()
+
+    def one(c):
+        u = np.arange(c * chunk, (c + 1) * chunk, dtype=np.uint64).astype(np.uint32)
+        x = u.view(np.float32)
+        ho, ro = orc.split(fmt, x)
+        reco = orc.reconstruct(fmt, ho, ro)
+        with lock:
+            hg, rg, recg = _gpu_split(mpo, x, fmt, exact)
+        bad = int(np.count_nonzero(hg != ho)) + int(np.count_nonzero(rg != ro))
+        bad += int(np.count_nonzero(bits32(recg) != bits32(reco)))
+        return bad
+
+    with ThreadPoolExecutor(max_workers=max(2, min(16, os.cpu_count() or 2))) as ex:
+        mism = sum(ex.map(one, range(64)))
+    assert mism == 0
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_split_golden_examples(mpo, exact):
+    rows = [l.split() for l in open(GOLDEN) if l.strip() and not l.startswith("#")]
+    for fmt in ("fp16", "bf16"):
+        sel = [r for r in rows if r[0] == fmt]
+        x = np.array([int(r[1], 16) for r in sel], dtype=np.uint32).view(np.float32)
+        h, r, rec = _gpu_split(mpo, x, fmt, exact)
+        assert [int(a) for a in h] == [int(s[2], 16) for s in sel]
+        assert [int(a) for a in r] == [int(s[3]) for s in sel]
+        assert [int(a) for a in bits32(rec)] == [int(s[4], 16) for s in sel]
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 8, 9, 4095, 4097, 100003])
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+def test_split_ragged_sizes(mpo, orc, fmt, n):
+    x = synth.normal_f32(n, 1.0, 0xB0B, 7, n)
+    if n >= 40:
+        x[:36] = synth.edge_f32()
+    ho, ro = orc.split(fmt, x)
+    hg, rg, recg = _gpu_split(mpo, x, fmt, False)
+    assert np.array_equal(hg, ho) and np.array_equal(rg, ro)
+    assert np.array_equal(bits32(recg), bits32(orc.reconstruct(fmt, ho, ro)))
+
+
+# ------------------------------------------------------------------------------------------
+# Adam / AdamW, config C1 (BASELINE configs[0]): 2^20 flat fp16 + residual, 100 steps
+# ------------------------------------------------------------------------------------------
+def _adam_case(mpo, fmt, gfmt, n, seed):
+    w = synth.weights(n, 0.02, seed)
+    h, r = _orc().split(fmt, w)
+    return h, r, np.zeros(n, np.float32), np.zeros(n, np.float32)
+
+
+def _orc():
+    import oracle
+    oracle.build()
+    return oracle
+
+
+def _gpu_adam(mpo, fmt, gfmt, h, r, g, m, v, hp, exact, norm_ws=None):
+    V, R, G, M, Vv = dev16(h, fmt), devi16(r), dev_grad(g, gfmt), devf(m), devf(v)
+    tab = mpo.TensorTable([V], [R], [G], [M], [Vv])
+    mpo.mpo_adam_step(tab, hp, norm_ws=norm_ws, exact=exact)
+    return host16(V), R.cpu().numpy(), M.cpu().numpy(), Vv.cpu().numpy()
+
+
+def _adam_hp_kw(hp):
+    return dict(lr=hp.lr, beta1=hp.beta1, beta2=hp.beta2, eps=hp.eps, weight_decay=hp.weight_decay,
+                adamw=hp.adamw, grad_scale=hp.grad_scale, step=hp.step)
+
+
+@pytest.mark.parametrize("fmt,wd,adamw", [("fp16", 0.0, False), ("fp16", 0.01, True), ("bf16", 0.01, True),
+                                          ("bf16", 0.01, False)])
+def test_adam_c1_bit_exact_100_steps(mpo, orc, fmt, wd, adamw):
+    """configs[0]: 1M-param flat tensor, Adam, 100 steps, every step bit-exact (exact build)."""
+    n, steps = 1 << 20, 100 if fmt == "fp16" and not adamw else 30
+    h, r, m, v = _adam_case(mpo, fmt, fmt, n, 0xB0B)
+    V, R, M, Vv = dev16(h, fmt), devi16(r), devf(m), devf(v)
+    G = torch.empty(n, dtype=TDT[fmt], device="cuda")
+    tab = mpo.TensorTable([V], [R], [G], [M], [Vv])
+    for t in range(1, steps + 1):
+        g = synth.grads(n, 1e-3, fmt, 0xB0B, t)
+        G.copy_(dev16(g, fmt))
+        hp = mpo.AdamParams(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=wd, adamw=adamw, step=t)
+        mpo.mpo_adam_step(tab, hp, exact=True)
+        orc.adam_step(fmt, fmt, h, r, g, m, v, **_adam_hp_kw(hp))
+        if t in (1, 2, steps // 2, steps) or t % 10 == 0:
+            assert np.array_equal(host16(V), h), t
+            assert np.array_equal(R.cpu().numpy(), r), t
+            assert same_bits_nan_equal(M.cpu().numpy(), m), t
+            assert same_bits_nan_equal(Vv.cpu().numpy(), v), t
+
+
+def _check_fma_tolerance(fmt, h_prev, r_prev, hg, rg, ho, ro, mg=None, mo=None, vg=None, vo=None):
+    orc = _orc()
+    assert ulp16_dist(hg, ho, fmt).max(initial=0) <= 1
+    wg = orc.reconstruct(fmt, hg, rg).astype(np.float64)
+    wo = orc.reconstruct(fmt, ho, ro).astype(np.float64)
+    w0 = orc.reconstruct(fmt, h_prev, r_prev).astype(np.float64)
+    fin = np.isfinite(wo)
+    err = np.abs(wg - wo)[fin]
+    ok = (err <= 1e-6 * np.abs(wo[fin])) | (err <= 2 * np.spacing(np.abs(w0[fin]).astype(np.float32)))
+    assert ok.all(), (int((~ok).sum()), float(err.max()))
+    for a, b in ((mg, mo), (vg, vo)):
+        if a is not None:
+            fa = np.isfinite(b)
+            assert (np.abs(a[fa].astype(np.float64) - b[fa]) <= 1e-6 * np.abs(b[fa]) + 1e-30).all()
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+def test_adam_fma_build_within_tolerance(mpo, orc, fmt):
+    """FMA build, one step from identical state, repeated along the oracle's 20-step trajectory."""
+    n = (1 << 20) + 13
+    h, r, m, v = _adam_case(mpo, fmt, fmt, n, 2023)
+    for t in range(1, 21):
+        g = synth.grads(n, 1e-3, fmt, 2023, t)
+        hp = mpo.AdamParams(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, adamw=True, step=t)
+        hg, rg, mg, vg = _gpu_adam(mpo, fmt, fmt, h, r, g, m, v, hp, exact=False)
+        hp_, rp_ = h.copy(), r.copy()
+        orc.adam_step(fmt, fmt, h, r, g, m, v, **_adam_hp_kw(hp))
+        _check_fma_tolerance(fmt, hp_, rp_, hg, rg, h, r, mg, m, vg, v)
+
+
+# ------------------------------------------------------------------------------------------
+# Multi-tensor tables with ragged sizes, several hyper-parameter groups, every grad dtype
+# ------------------------------------------------------------------------------------------
+RAGGED = [0, 1, 7, 8, 9, 64, 4095, 4096, 4097, 12345, 65539, 3]
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+@pytest.mark.parametrize("gfmt", ["same", "fp32", "other"])
+@pytest.mark.parametrize("kind", ["adam", "sgd"])
+def test_multi_tensor_ragged_bit_exact(mpo, orc, fmt, gfmt, kind):
+    gf = fmt if gfmt == "same" else ("fp32" if gfmt == "fp32" else ("bf16" if fmt == "fp16" else "fp16"))
+    sizes = RAGGED
+    hs, rs, gs, ms, vs = [], [], [], [], []
+    for i, n in enumerate(sizes):
+        w = synth.weights(n, 0.05, 0xC0FFEE + i)
+        if n > 40:
+            w[:36] = synth.edge_f32() * np.float32(1e-3)
+        h, r = orc.split(fmt, w)
+        hs.append(h); rs.append(r)
+        gs.append(synth.grads(n, 1e-2, gf, 0xC0FFEE, i))
+        ms.append(synth.normal_f32(n, 1e-3, 5, i)); vs.append(np.abs(synth.normal_f32(n, 1e-5, 6, i)))
+    grp = [i % 3 for i in range(len(sizes))]
+    if kind == "adam":
+        hps = [mpo.AdamParams(lr=1e-3, weight_decay=0.1, adamw=True, step=3),
+               mpo.AdamParams(lr=2e-3, beta1=0.3, beta2=0.95, weight_decay=0.01, adamw=False, step=7, grad_scale=0.5),
+               mpo.AdamParams(lr=5e-4, beta1=0.0, beta2=0.9, eps=1e-6, step=1)]
+    else:
+        hps = [mpo.SgdParams(lr=0.3, momentum=0.9, weight_decay=2e-4),
+               mpo.SgdParams(lr=0.1, momentum=0.9, nesterov=True, grad_scale=0.25),
+               mpo.SgdParams(lr=0.05, momentum=0.5, dampening=0.1, first_step=True, weight_decay=1e-3)]
+    V = [dev16(h, fmt) for h in hs]
+    R = [devi16(r) for r in rs]
+    G = [dev_grad(g, gf) for g in gs]
+    M = [devf(m) for m in ms]
+    W = [devf(v) for v in vs]
+    tab = mpo.TensorTable(V, R, G, M, W if kind == "adam" else [None] * len(sizes), grp)
+    if kind == "adam":
+        mpo.mpo_adam_step(tab, hps, exact=True)
+    else:
+        mpo.mpo_sgd_step(tab, hps, exact=True)
+    for i in range(len(sizes)):
+        hp = hps[grp[i]]
+        if kind == "adam":
+            orc.adam_step(fmt, gf, hs[i], rs[i], gs[i], ms[i], vs[i], **_adam_hp_kw(hp))
+        else:
+            orc.sgd_step(fmt, gf, hs[i], rs[i], gs[i], ms[i], lr=hp.lr, momentum=hp.momentum,
+                         dampening=hp.dampening, weight_decay=hp.weight_decay, grad_scale=hp.grad_scale,
+                         nesterov=hp.nesterov, first_step=hp.first_step)
+        assert np.array_equal(host16(V[i]), hs[i]), i
+        assert np.array_equal(R[i].cpu().numpy(), rs[i]), i
+        assert same_bits_nan_equal(M[i].cpu().numpy(), ms[i]), i
+        if kind == "adam":
+            assert same_bits_nan_equal(W[i].cpu().numpy(), vs[i]), i
+
+
+def test_multi_tensor_equals_per_tensor(mpo):
+    """One launch over the table == one launch per tensor, bitwise (FMA build)."""
+    torch.manual_seed(0)
+    sizes = [4096 * 3 + 8, 17, 64, 8192, 100]
+    mk = lambda: ([torch.randn(n, device="cuda").to(torch.bfloat16) for n in sizes])
+    vals = mk()
+    grads = [torch.randn(n, device="cuda").to(torch.bfloat16) * 1e-2 for n in sizes]
+    res = [torch.randint(-30000, 30000, (n,), device="cuda", dtype=torch.int16) for n in sizes]
+    st = [(torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")) for n in sizes]
+    A = [[t.clone() for t in x] for x in (vals, res, [s[0] for s in st], [s[1] for s in st])]
+    B = [[t.clone() for t in x] for x in (vals, res, [s[0] for s in st], [s[1] for s in st])]
+    hp = mpo.AdamParams(lr=1e-3, weight_decay=0.1, step=1)
+    for step in range(1, 4):
+        hp.step = step
+        mpo.mpo_adam_step(mpo.TensorTable(A[0], A[1], grads, A[2], A[3]), hp)
+        for i in range(len(sizes)):
+            mpo.mpo_adam_step(mpo.TensorTable([B[0][i]], [B[1][i]], [grads[i]], [B[2][i]], [B[3][i]]), hp)
+    for a, b in zip(A, B):
+        for x, y in zip(a, b):
+            assert torch.equal(x.view(torch.int16) if x.dtype == torch.bfloat16 else x,
+                               y.view(torch.int16) if y.dtype == torch.bfloat16 else y)
+
+
+# ------------------------------------------------------------------------------------------
+# Global-norm clipping (config C5 reading R9)
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("target_norm", [4.0, 0.5])
+def test_clip_sumsq_and_hybrid_step(mpo, orc, target_norm):
+    fmt = "fp16"
+    sizes = [1024 * 197 + 5, 3 * 1024 * 1024, 1024, 4096 * 1024 + 3]
+    hs, rs, gs, ms, vs = [], [], [], [], []
+    sig = target_norm / np.sqrt(sum(sizes))
+    for i, n in enumerate(sizes):
+        h, r = orc.split(fmt, synth.weights(n, 0.02, 2023 + i))
+        hs.append(h); rs.append(r); gs.append(synth.grads(n, sig, fmt, 2023, i))
+        ms.append(np.zeros(n, np.float32)); vs.append(np.zeros(n, np.float32))
+    V = [dev16(h, fmt) for h in hs]; R = [devi16(r) for r in rs]; G = [dev16(g, fmt) for g in gs]
+    M = [devf(m) for m in ms]; W = [devf(v) for v in vs]
+    ws = torch.zeros(mpo.norm_ws_doubles(), dtype=torch.float64, device="cuda")
+    hp = mpo.AdamParams(lr=1e-3, max_grad_norm=1.0, step=1)
+    mpo.mpo_adam_step(mpo.TensorTable(V, R, G, M, W), hp, norm_ws=ws, exact=True)
+    S_gpu = float(ws[0].item())
+    S_orc = sum(orc.sumsq(fmt, g) for g in gs)
+    assert abs(S_gpu - S_orc) <= 1e-10 * S_orc
+    coef = orc.clip_coef(S_gpu, 1.0)     # hybrid: the oracle steps with the GPU's S
+    assert (coef < 1.0) == (target_norm > 1.0)
+    for i in range(len(sizes)):
+        orc.adam_step(fmt, fmt, hs[i], rs[i], gs[i], ms[i], vs[i], **_adam_hp_kw(hp), clip_coef=coef)
+        assert np.array_equal(host16(V[i]), hs[i]) and np.array_equal(R[i].cpu().numpy(), rs[i])
+        assert same_bits_nan_equal(M[i].cpu().numpy(), ms[i])
+
+
+def test_clip_exact_sum_construction(mpo, orc):
+    """All |g| equal to one power of two: S is exact on both sides, so coef is identical."""
+    fmt = "bf16"
+    n = 3 * 4096 + 40
+    sign = np.where(synth.rng(1, 2).random(n) < 0.5, -1.0, 1.0).astype(np.float32)
+    g = synth.to16_bits(sign * np.float32(2.0 ** -6), fmt)
+    h, r = orc.split(fmt, synth.weights(n))
+    m = np.zeros(n, np.float32); v = np.zeros(n, np.float32)
+    ws = torch.zeros(mpo.norm_ws_doubles(), dtype=torch.float64, device="cuda")
+    hp = mpo.AdamParams(lr=1e-3, max_grad_norm=0.25, step=1)
+    hg, rg, mg, vg = _gpu_adam(mpo, fmt, fmt, h, r, g, m, v, hp, exact=True, norm_ws=ws)
+    S = float(ws[0].item())
+    assert S == n * 2.0 ** -12 == orc.sumsq(fmt, g)
+    orc.adam_step(fmt, fmt, h, r, g, m, v, **_adam_hp_kw(hp), clip_coef=orc.clip_coef(orc.sumsq(fmt, g), 0.25))
+    assert np.array_equal(hg, h) and np.array_equal(rg, r) and same_bits_nan_equal(mg, m)
+
+
+# ------------------------------------------------------------------------------------------
+# Full-size workloads in the bench's launch configuration (sampled / whole where cheap)
+# ------------------------------------------------------------------------------------------
+def _workload_table(mpo, name, fmt, kind, seed, gfmt=None):
+    gfmt = gfmt or fmt
+    sizes = workloads.sizes(name)
+    tot = sum(sizes)
+    w = synth.weights(tot, 0.02, seed)
+    orc = _orc()
+    h, r = orc.split(fmt, w)
+    g = synth.grads(tot, 1e-3, gfmt, seed, 1)
+    m = synth.normal_f32(tot, 1e-4, seed, 3)
+    v = np.abs(synth.normal_f32(tot, 1e-7, seed, 4))
+    return sizes, h, r, g, m, v
+
+
+def _views(flat, sizes):
+    out, o = [], 0
+    for n in sizes:
+        out.append(flat[o:o + n])
+        o += n
+    return out
+
+
+def _aligned_copy(dev_flat_fn, arr, sizes):
+    """Per-tensor device tensors (each its own allocation, so 16-B aligned)."""
+    return [dev_flat_fn(a) for a in _views(arr, sizes)]
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_resnet50_sgd_full(mpo, orc, exact):
+    """configs[1]: ResNet-50 parameter set, fp16 + residual, SGD-momentum, one multi-tensor launch;
+    compared on ALL 25.6M elements."""
+    fmt = "fp16"
+    sizes, h, r, g, m, v = _workload_table(mpo, "resnet50", fmt, "sgd", 0xB0B)
+    V = _aligned_copy(lambda a: dev16(a, fmt), h, sizes)
+    R = _aligned_copy(devi16, r, sizes)
+    G = _aligned_copy(lambda a: dev16(a, fmt), g, sizes)
+    M = _aligned_copy(devf, m, sizes)
+    tab = mpo.TensorTable(V, R, G, M, [None] * len(sizes))
+    hp = mpo.SgdParams(lr=0.3, momentum=0.9, weight_decay=2e-4)
+    h0, r0 = h.copy(), r.copy()
+    mpo.mpo_sgd_step(tab, hp, exact=exact)
+    orc.sgd_step(fmt, fmt, h, r, g, m, lr=0.3, momentum=0.9, weight_decay=2e-4)
+    hg = np.concatenate([host16(x) for x in V]); rg = np.concatenate([x.cpu().numpy() for x in R])
+    mg = np.concatenate([x.cpu().numpy() for x in M])
+    if exact:
+        assert np.array_equal(hg, h) and np.array_equal(rg, r) and same_bits_nan_equal(mg, m)
+    else:
+        _check_fma_tolerance(fmt, h0, r0, hg, rg, h, r, mg, m)
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_gpt2_adamw_full(mpo, orc, exact):
+    """configs[2] parameter set (124M), bf16 + residual, AdamW, multi-tensor launch, all elements."""
+    fmt = "bf16"
+    sizes, h, r, g, m, v = _workload_table(mpo, "gpt2_small", fmt, "adam", 2023)
+    V = _aligned_copy(lambda a: dev16(a, fmt), h, sizes)
+    R = _aligned_copy(devi16, r, sizes)
+    G = _aligned_copy(lambda a: dev16(a, fmt), g, sizes)
+    M = _aligned_copy(devf, m, sizes)
+    W = _aligned_copy(devf, v, sizes)
+    hp = mpo.AdamParams(lr=6e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, adamw=True, step=5)
+    h0, r0 = h.copy(), r.copy()
+    mpo.mpo_adam_step(mpo.TensorTable(V, R, G, M, W), hp, exact=exact)
+    orc.adam_step(fmt, fmt, h, r, g, m, v, **_adam_hp_kw(hp))
+    hg = np.concatenate([host16(x) for x in V]); rg = np.concatenate([x.cpu().numpy() for x in R])
+    mg = np.concatenate([x.cpu().numpy() for x in M]); vg = np.concatenate([x.cpu().numpy() for x in W])
+    if exact:
+        assert np.array_equal(hg, h) and np.array_equal(rg, r)
+        assert same_bits_nan_equal(mg, m) and same_bits_nan_equal(vg, v)
+    else:
+        _check_fma_tolerance(fmt, h0, r0, hg, rg, h, r, mg, m, vg, v)
