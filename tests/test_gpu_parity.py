@@ -142,20 +142,39 @@ def test_adam_c1_bit_exact_100_steps(mpo, orc, fmt, wd, adamw):
             assert same_bits_nan_equal(Vv.cpu().numpy(), v), t
 
 
-def _check_fma_tolerance(fmt, h_prev, r_prev, hg, rg, ho, ro, mg=None, mo=None, vg=None, vo=None):
+def _check_fma_tolerance(fmt, pre, gpu, orc_, g32):
+    """FMA-build bar (BASELINE north_star; reading R12 in DESIGN.md).
+
+    pre/gpu/orc_ = (h, r, m, v) before the step, from the GPU and from the oracle; g32 = the fp32
+    gradient the step consumed.  The fp32 weight must agree within 1e-6 of the magnitude of the
+    update's operands, |dw| <= 1e-6 (|w_old| + |w_new|): a plain relative bound on w_new is
+    meaningless where w_old - u cancels (w_new -> 0 while u carries an FMA-rounding difference of
+    ~1 ulp(u)).  Where that cancellation is absent (|dw| <= 1e-6 |w_new|), the 16-bit value must be
+    within 1 ulp16.  fp16 below 2^-16 is lossy by construction (R5): bar 2^-24.  m within
+    1e-6 (|m_old| + |g|), v within 1e-6 |v|."""
     orc = _orc()
-    assert ulp16_dist(hg, ho, fmt).max(initial=0) <= 1
+    h0, r0, m0, v0 = pre
+    hg, rg, mg, vg = gpu
+    ho, ro, mo, vo = orc_
     wg = orc.reconstruct(fmt, hg, rg).astype(np.float64)
     wo = orc.reconstruct(fmt, ho, ro).astype(np.float64)
-    w0 = orc.reconstruct(fmt, h_prev, r_prev).astype(np.float64)
-    fin = np.isfinite(wo)
-    err = np.abs(wg - wo)[fin]
-    ok = (err <= 1e-6 * np.abs(wo[fin])) | (err <= 2 * np.spacing(np.abs(w0[fin]).astype(np.float32)))
-    assert ok.all(), (int((~ok).sum()), float(err.max()))
-    for a, b in ((mg, mo), (vg, vo)):
-        if a is not None:
-            fa = np.isfinite(b)
-            assert (np.abs(a[fa].astype(np.float64) - b[fa]) <= 1e-6 * np.abs(b[fa]) + 1e-30).all()
+    w0 = orc.reconstruct(fmt, h0, r0).astype(np.float64)
+    fin = np.isfinite(wo) & np.isfinite(w0)
+    err = np.abs(wg - wo)
+    bound = 1e-6 * (np.abs(w0) + np.abs(wo))
+    if fmt == "fp16":
+        bound = np.where(np.abs(wo) < 2.0 ** -16, np.maximum(bound, 2.0 ** -24), bound)
+    ok = ~fin | (err <= bound)
+    assert ok.all(), (int((~ok).sum()), np.abs(wo[~ok])[:8], err[~ok][:8], bound[~ok][:8])
+    well = fin & (err <= 1e-6 * np.abs(wo))
+    assert ulp16_dist(hg[well], ho[well], fmt).max(initial=0) <= 1
+    g = np.abs(np.asarray(g32, dtype=np.float64))
+    if mg is not None:
+        f = np.isfinite(mo)
+        assert (np.abs(mg[f].astype(np.float64) - mo[f]) <= 1e-6 * (np.abs(m0[f]) + g[f] + np.abs(mo[f])) + 1e-30).all()
+    if vg is not None:
+        f = np.isfinite(vo)
+        assert (np.abs(vg[f].astype(np.float64) - vo[f]) <= 1e-6 * np.abs(vo[f]) + 1e-30).all()
 
 
 @pytest.mark.parametrize("fmt", ["fp16", "bf16"])
@@ -167,9 +186,9 @@ def test_adam_fma_build_within_tolerance(mpo, orc, fmt):
         g = synth.grads(n, 1e-3, fmt, 2023, t)
         hp = mpo.AdamParams(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, adamw=True, step=t)
         hg, rg, mg, vg = _gpu_adam(mpo, fmt, fmt, h, r, g, m, v, hp, exact=False)
-        hp_, rp_ = h.copy(), r.copy()
+        pre = (h.copy(), r.copy(), m.copy(), v.copy())
         orc.adam_step(fmt, fmt, h, r, g, m, v, **_adam_hp_kw(hp))
-        _check_fma_tolerance(fmt, hp_, rp_, hg, rg, h, r, mg, m, vg, v)
+        _check_fma_tolerance(fmt, pre, (hg, rg, mg, vg), (h, r, m, v), orc.widen(fmt, g))
 
 
 # ------------------------------------------------------------------------------------------
@@ -337,7 +356,7 @@ def test_resnet50_sgd_full(mpo, orc, exact):
     M = _aligned_copy(devf, m, sizes)
     tab = mpo.TensorTable(V, R, G, M, [None] * len(sizes))
     hp = mpo.SgdParams(lr=0.3, momentum=0.9, weight_decay=2e-4)
-    h0, r0 = h.copy(), r.copy()
+    pre = (h.copy(), r.copy(), m.copy(), None)
     mpo.mpo_sgd_step(tab, hp, exact=exact)
     orc.sgd_step(fmt, fmt, h, r, g, m, lr=0.3, momentum=0.9, weight_decay=2e-4)
     hg = np.concatenate([host16(x) for x in V]); rg = np.concatenate([x.cpu().numpy() for x in R])
@@ -345,7 +364,9 @@ def test_resnet50_sgd_full(mpo, orc, exact):
     if exact:
         assert np.array_equal(hg, h) and np.array_equal(rg, r) and same_bits_nan_equal(mg, m)
     else:
-        _check_fma_tolerance(fmt, h0, r0, hg, rg, h, r, mg, m)
+        # the momentum operand also carries wd*w (SGD folds decay into the gradient)
+        g32 = np.abs(orc.widen(fmt, g)) + 2e-4 * np.abs(orc.reconstruct(fmt, pre[0], pre[1]))
+        _check_fma_tolerance(fmt, pre, (hg, rg, mg, None), (h, r, m, None), g32)
 
 
 @pytest.mark.parametrize("exact", [True, False])
@@ -359,7 +380,7 @@ def test_gpt2_adamw_full(mpo, orc, exact):
     M = _aligned_copy(devf, m, sizes)
     W = _aligned_copy(devf, v, sizes)
     hp = mpo.AdamParams(lr=6e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, adamw=True, step=5)
-    h0, r0 = h.copy(), r.copy()
+    pre = (h.copy(), r.copy(), m.copy(), v.copy())
     mpo.mpo_adam_step(mpo.TensorTable(V, R, G, M, W), hp, exact=exact)
     orc.adam_step(fmt, fmt, h, r, g, m, v, **_adam_hp_kw(hp))
     hg = np.concatenate([host16(x) for x in V]); rg = np.concatenate([x.cpu().numpy() for x in R])
@@ -368,4 +389,4 @@ def test_gpt2_adamw_full(mpo, orc, exact):
         assert np.array_equal(hg, h) and np.array_equal(rg, r)
         assert same_bits_nan_equal(mg, m) and same_bits_nan_equal(vg, v)
     else:
-        _check_fma_tolerance(fmt, h0, r0, hg, rg, h, r, mg, m, vg, v)
+        _check_fma_tolerance(fmt, pre, (hg, rg, mg, vg), (h, r, m, v), orc.widen(fmt, g))
