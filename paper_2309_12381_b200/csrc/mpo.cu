@@ -21,6 +21,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -256,6 +257,76 @@ struct SgdOp {
     }
 };
 
+// One unit (8 consecutive elements): reconstruct -> update -> re-split, registers in and out.
+template <int F, int G, class Op, bool CLIP>
+__device__ __forceinline__ void process_unit(const uint4& hv, const uint4& rv, const GradUnit<G>& gu, float (&mm)[8],
+                                             float (&vv)[8], const typename Op::K& c, float coef, uint4& ho,
+                                             uint4& ro) {
+    const uint32_t* h = &hv.x;
+    const uint32_t* r = &rv.x;
+    float w[8];
+    const uint32_t special = nonfinite_pair<F>(h[0]) | nonfinite_pair<F>(h[1]) | nonfinite_pair<F>(h[2]) |
+                             nonfinite_pair<F>(h[3]);
+    if (__builtin_expect(special == 0u, 1)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) reconstruct_pair_finite<F>(h[q], r[q], w[2 * q], w[2 * q + 1]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            w[2 * q] = reconstruct1<F>(lo16(h[q]), slo16(r[q]));
+            w[2 * q + 1] = reconstruct1<F>(hi16(h[q]), shi16(r[q]));
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        float g = grad_at<G>(gu, k) * c.gs;
+        if constexpr (CLIP) g = g * coef;
+        w[k] = Op::apply(w[k], g, mm[k], vv[k], c);
+    }
+    uint32_t* hop = &ho.x;
+    uint32_t* rop = &ro.x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) split2_fast<F>(w[2 * q], w[2 * q + 1], hop[q], rop[q]);
+}
+
+// Ragged tail of one tensor (n % 8 elements): element by element from global memory.
+template <int F, int G, class Op, bool CLIP>
+__device__ __noinline__ void process_tail(const KT T, int64_t lo, int64_t hi, const typename Op::K c, float coef) {
+    uint16_t* val = static_cast<uint16_t*>(T.value);
+    const bool need_m = Op::reads_m(c), has_m = Op::writes_m(c);
+    for (int64_t i = lo; i < hi; ++i) {
+        float g = grad_scalar<G>(T.grad, i) * c.gs;
+        if constexpr (CLIP) g = g * coef;
+        float w = reconstruct1<F>(val[i], T.resid[i]);
+        float mi = need_m ? T.m[i] : 0.0f;
+        float vi = 0.0f;
+        if constexpr (Op::kHasV) vi = T.v[i];
+        w = Op::apply(w, g, mi, vi, c);
+        uint32_t ho, ro;
+        split2<F>(w, 0.0f, ho, ro);
+        val[i] = static_cast<uint16_t>(ho & 0xFFFFu);
+        T.resid[i] = static_cast<int16_t>(ro & 0xFFFFu);
+        if (has_m) T.m[i] = mi;
+        if constexpr (Op::kHasV) T.v[i] = vi;
+    }
+}
+
+template <class Op>
+__device__ __forceinline__ void store_unit(const KT& T, int64_t e, const uint4& ho, const uint4& ro, const float (&mm)[8],
+                                           const float (&vv)[8], bool has_m) {
+    stv(static_cast<uint16_t*>(T.value) + e, ho);
+    stv(T.resid + e, ro);
+    if (has_m) {
+        stf(T.m + e, make_float4(mm[0], mm[1], mm[2], mm[3]));
+        stf(T.m + e + 4, make_float4(mm[4], mm[5], mm[6], mm[7]));
+    }
+    if constexpr (Op::kHasV) {
+        stf(T.v + e, make_float4(vv[0], vv[1], vv[2], vv[3]));
+        stf(T.v + e + 4, make_float4(vv[4], vv[5], vv[6], vv[7]));
+    }
+}
+
+// ---- variant A ("lsu"): every thread loads its own units with 128-bit LDG, computes, stores ----
 template <int MAXT, int F, int G, class Op, bool CLIP>
 __global__ void __launch_bounds__(kThreads) step_kernel(const __grid_constant__ Table<MAXT> tab,
                                                         const __grid_constant__ HP<typename Op::K> hp,
@@ -305,54 +376,189 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const __grid_constant__ 
             if (e + kUnitEl <= n) {
                 float mm[8] = {m0[j].x, m0[j].y, m0[j].z, m0[j].w, m1[j].x, m1[j].y, m1[j].z, m1[j].w};
                 float vv[8] = {v0[j].x, v0[j].y, v0[j].z, v0[j].w, v1[j].x, v1[j].y, v1[j].z, v1[j].w};
-                const uint32_t* h = &hv[j].x;
-                const uint32_t* r = &rv[j].x;
                 uint4 ho, ro;
-                uint32_t* hop = &ho.x;
-                uint32_t* rop = &ro.x;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    float g0 = grad_at<G>(gu[j], 2 * q) * c.gs;
-                    float g1 = grad_at<G>(gu[j], 2 * q + 1) * c.gs;
-                    if constexpr (CLIP) {
-                        g0 = g0 * coef;
-                        g1 = g1 * coef;
-                    }
-                    float w0 = reconstruct1<F>(lo16(h[q]), slo16(r[q]));
-                    float w1 = reconstruct1<F>(hi16(h[q]), shi16(r[q]));
-                    w0 = Op::apply(w0, g0, mm[2 * q], vv[2 * q], c);
-                    w1 = Op::apply(w1, g1, mm[2 * q + 1], vv[2 * q + 1], c);
-                    split2<F>(w0, w1, hop[q], rop[q]);
-                }
-                stv(static_cast<uint16_t*>(T.value) + e, ho);
-                stv(T.resid + e, ro);
-                if (has_m) {
-                    stf(T.m + e, make_float4(mm[0], mm[1], mm[2], mm[3]));
-                    stf(T.m + e + 4, make_float4(mm[4], mm[5], mm[6], mm[7]));
-                }
-                if constexpr (Op::kHasV) {
-                    stf(T.v + e, make_float4(vv[0], vv[1], vv[2], vv[3]));
-                    stf(T.v + e + 4, make_float4(vv[4], vv[5], vv[6], vv[7]));
-                }
+                process_unit<F, G, Op, CLIP>(hv[j], rv[j], gu[j], mm, vv, c, coef, ho, ro);
+                store_unit<Op>(T, e, ho, ro, mm, vv, has_m);
             } else if (e < n) {
-                // ragged tail of this tensor: element by element
-                uint16_t* val = static_cast<uint16_t*>(T.value);
-                for (int64_t i = e; i < n; ++i) {
-                    float g = grad_scalar<G>(T.grad, i) * c.gs;
-                    if constexpr (CLIP) g = g * coef;
-                    float w = reconstruct1<F>(val[i], T.resid[i]);
-                    float mi = need_m ? T.m[i] : 0.0f;
-                    float vi = 0.0f;
-                    if constexpr (Op::kHasV) vi = T.v[i];
-                    w = Op::apply(w, g, mi, vi, c);
-                    uint32_t ho, ro;
-                    split2<F>(w, 0.0f, ho, ro);
-                    val[i] = static_cast<uint16_t>(ho & 0xFFFFu);
-                    T.resid[i] = static_cast<int16_t>(ro & 0xFFFFu);
-                    if (has_m) T.m[i] = mi;
-                    if constexpr (Op::kHasV) T.v[i] = vi;
+                process_tail<F, G, Op, CLIP>(T, e, n, c, coef);
+            }
+        }
+    }
+}
+
+// ---- variant B ("tma", default): warp-specialised bulk-copy pipeline ----------------------
+// One producer warp streams each tile's value / residual / grad / m / v from HBM into a ring of
+// shared-memory stages with 1-D TMA bulk copies (cp.async.bulk, mbarrier complete_tx, L2
+// evict-first); kCW consumer warps read the stage from shared memory, compute, and store the
+// results straight to HBM with 128-bit stores, then release the stage.  Loads are therefore
+// issued independently of the arithmetic, several tiles ahead.
+constexpr int kCW = 16;                                  // consumer warps per CTA
+constexpr int kTmaThreads = (kCW + 1) * 32;              // + 1 producer warp
+static_assert(kCW * 32 * kUnitEl == kTileEl, "one unit per consumer thread per tile");
+constexpr int kMaxStages = 8;
+constexpr int kBarBytes = 2 * kMaxStages * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// 1-D bulk copy global -> shared, completing `bytes` of transaction on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+template <int G>
+struct GradBytes {
+    static constexpr int v = G == kFP32 ? 4 : 2;
+};
+
+// bytes of one stage: value 2 + resid 2 + grad gb + m 4 [+ v 4] per element
+template <int G, bool HAS_V>
+__host__ __device__ constexpr int stage_bytes() {
+    return int(kTileEl) * (2 + 2 + GradBytes<G>::v + 4 + (HAS_V ? 4 : 0));
+}
+
+template <int MAXT, int F, int G, class Op, bool CLIP>
+__global__ void __launch_bounds__(kTmaThreads, 1) step_tma_kernel(const __grid_constant__ Table<MAXT> tab,
+                                                                  const __grid_constant__ HP<typename Op::K> hp,
+                                                                  const double* __restrict__ sumsq, double max_norm,
+                                                                  int stages) {
+    using K = typename Op::K;
+    constexpr int GB = GradBytes<G>::v;
+    constexpr int64_t TE = kTileEl;
+    // stage layout: [value TE*2 | resid TE*2 | grad TE*GB | m TE*4 | v TE*4]
+    constexpr int OFF_R = int(TE) * 2, OFF_G = int(TE) * 4, OFF_M = int(TE) * (4 + GB), OFF_V = int(TE) * (8 + GB);
+    constexpr int SB = stage_bytes<G, Op::kHasV>();
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + kMaxStages;
+    unsigned char* ring = smem + kBarBytes;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kCW) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            int cur = 0, it = 0;
+            for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x, ++it) {
+                const int s = it % stages;
+                const uint32_t round = uint32_t(it / stages);
+                mbar_wait(&empty[s], (round & 1u) ^ 1u);
+                while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
+                const KT& T = tab.t[cur];
+                const K c = hp.g[T.hp];
+                const int64_t base = int64_t(tile - T.tile0) * TE;
+                const int64_t nvalid = T.n - base < TE ? T.n - base : TE;
+                const uint32_t nvec = uint32_t(nvalid) & ~uint32_t(kUnitEl - 1);
+                const bool need_m = Op::reads_m(c);
+                uint32_t bytes = nvec * (4u + GB);
+                if (need_m) bytes += nvec * 4u;
+                if constexpr (Op::kHasV) bytes += nvec * 4u;
+                unsigned char* st = ring + size_t(s) * SB;
+                mbar_arrive_expect_tx(&full[s], bytes);
+                if (nvec) {
+                    bulk_g2s(st, static_cast<const uint16_t*>(T.value) + base, nvec * 2u, &full[s], pol);
+                    bulk_g2s(st + OFF_R, T.resid + base, nvec * 2u, &full[s], pol);
+                    bulk_g2s(st + OFF_G, static_cast<const unsigned char*>(T.grad) + base * GB, nvec * GB, &full[s], pol);
+                    if (need_m) bulk_g2s(st + OFF_M, T.m + base, nvec * 4u, &full[s], pol);
+                    if constexpr (Op::kHasV) bulk_g2s(st + OFF_V, T.v + base, nvec * 4u, &full[s], pol);
                 }
             }
+        }
+        return;
+    }
+
+    // ---------------- consumers ----------------
+    float coef = 1.0f;
+    if constexpr (CLIP) coef = clip_coef(sumsq, max_norm);
+    const int ct = threadIdx.x;   // 0 .. kCW*32-1, one unit per tile
+    int cur = 0, it = 0;
+    for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x, ++it) {
+        const int s = it % stages;
+        const uint32_t round = uint32_t(it / stages);
+        while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
+        const KT& T = tab.t[cur];
+        const K c = hp.g[T.hp];
+        const int64_t base = int64_t(tile - T.tile0) * TE;
+        const int64_t nvalid = T.n - base < TE ? T.n - base : TE;
+        const int64_t nvec = nvalid & ~int64_t(kUnitEl - 1);
+        const int64_t el = int64_t(ct) * kUnitEl;
+        mbar_wait(&full[s], round & 1u);
+        const bool full_unit = el + kUnitEl <= nvec;
+        uint4 hv, rv;
+        GradUnit<G> gu;
+        float mm[8], vv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mm[k] = vv[k] = 0.0f;
+        if (full_unit) {
+            const unsigned char* st = ring + size_t(s) * SB;
+            hv = *reinterpret_cast<const uint4*>(st + el * 2);
+            rv = *reinterpret_cast<const uint4*>(st + OFF_R + el * 2);
+            if constexpr (G == kFP32) {
+                gu.a = *reinterpret_cast<const uint4*>(st + OFF_G + el * 4);
+                gu.b = *reinterpret_cast<const uint4*>(st + OFF_G + el * 4 + 16);
+            } else {
+                gu.a = *reinterpret_cast<const uint4*>(st + OFF_G + el * 2);
+            }
+            if (Op::reads_m(c)) {
+                const float4 a = *reinterpret_cast<const float4*>(st + OFF_M + el * 4);
+                const float4 b = *reinterpret_cast<const float4*>(st + OFF_M + el * 4 + 16);
+                mm[0] = a.x; mm[1] = a.y; mm[2] = a.z; mm[3] = a.w; mm[4] = b.x; mm[5] = b.y; mm[6] = b.z; mm[7] = b.w;
+            }
+            if constexpr (Op::kHasV) {
+                const float4 a = *reinterpret_cast<const float4*>(st + OFF_V + el * 4);
+                const float4 b = *reinterpret_cast<const float4*>(st + OFF_V + el * 4 + 16);
+                vv[0] = a.x; vv[1] = a.y; vv[2] = a.z; vv[3] = a.w; vv[4] = b.x; vv[5] = b.y; vv[6] = b.z; vv[7] = b.w;
+            }
+        }
+        // the warp's share of the stage now sits in registers: release the stage to the producer
+        // before the arithmetic, so the next bulk copies overlap this tile's compute
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (full_unit) {
+            uint4 ho, ro;
+            process_unit<F, G, Op, CLIP>(hv, rv, gu, mm, vv, c, coef, ho, ro);
+            store_unit<Op>(T, base + el, ho, ro, mm, vv, Op::writes_m(c));
+        } else if (el == nvec && nvec < nvalid) {
+            process_tail<F, G, Op, CLIP>(T, base + nvec, base + nvalid, c, coef);
         }
     }
 }
@@ -522,6 +728,18 @@ mpo_status launch_sumsq(const mpo_tensor* t, int lo, int hi, const HP<float>& gs
     return check_launch("sumsq_kernel");
 }
 
+// Kernel variant: "tma" (default, bulk-copy pipeline) or "lsu" (per-thread 128-bit loads), chosen
+// once per process from MPO_STEP_KERNEL (A/B evidence for DESIGN.md section 5).
+bool use_tma() {
+    static const bool tma = [] {
+        const char* e = std::getenv("MPO_STEP_KERNEL");
+        return !(e && std::strcmp(e, "lsu") == 0);
+    }();
+    return tma;
+}
+
+constexpr int kSmemBudget = 227 * 1024;
+
 template <int MAXT, int F, int G, class Op, bool CLIP>
 mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typename Op::K>& hp, bool one_hp,
                              const double* sumsq, double max_norm, cudaStream_t s) {
@@ -529,6 +747,19 @@ mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typen
     const int64_t tiles = fill_table(tab, t, lo, hi, one_hp);
     if (tiles == 0) return MPO_OK;
     if (tiles > INT32_MAX) return fail(MPO_EINVAL, "table slice too large");
+    if (use_tma()) {
+        auto kern = step_tma_kernel<MAXT, F, G, Op, CLIP>;
+        constexpr int SB = stage_bytes<G, Op::kHasV>();
+        constexpr int stages = (kSmemBudget - kBarBytes) / SB < kMaxStages ? (kSmemBudget - kBarBytes) / SB : kMaxStages;
+        static_assert(stages >= 2, "need at least two pipeline stages");
+        constexpr int smem = kBarBytes + stages * SB;
+        static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (attr != cudaSuccess) return fail(MPO_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr));
+        const int64_t grid = grid_for(tiles, 1);
+        kern<<<unsigned(grid), kTmaThreads, smem, s>>>(tab, hp, sumsq, max_norm, stages);
+        ++g_launches;
+        return check_launch("step_tma_kernel");
+    }
     auto kern = step_kernel<MAXT, F, G, Op, CLIP>;
     static int per_sm = resident_blocks(kern);
     const int64_t grid = grid_for(tiles, per_sm);
