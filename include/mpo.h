@@ -170,6 +170,17 @@ mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t rank, i
                             int64_t n_total, const void* hp, double* norm_ws,
                             mpo_stream stream);
 
+/* Diagnostic: checks the branch-free fast sqrt / division sequences of the step kernels against
+ * the compiler's IEEE sqrtf() and `/`.  sqrt: ALL 2^32 binary32 patterns;
+ * division: `pairs` operand pairs drawn from a counter-based generator keyed by `seed` (bit
+ * patterns uniform over the accepted exponent window, plus fully random patterns).  Wherever an
+ * input is accepted by the fast range check the two results must be bit-identical.
+ *   counts: DEVICE array of 4 uint64, zeroed by the call, then accumulated in stream order:
+ *           [0] sqrt mismatches, [1] division mismatches, [2] sqrt inputs on the fast path,
+ *           [3] division pairs on the fast path. */
+mpo_status mpo_selfcheck_fastmath(int64_t pairs, uint64_t seed, unsigned long long* counts,
+                                  mpo_stream stream);
+
 /* Thread-local description of the last non-OK status ("" if none). */
 const char* mpo_last_error(void);
 

@@ -22,7 +22,7 @@ MPO_MAX_HP_GROUPS = 16
 # Every entry point include/mpo.h declares (tests/test_boundary.py checks the header agrees).
 SYMBOLS = ("mpo_split", "mpo_reconstruct", "mpo_sgd_step", "mpo_adam_step", "mpo_norm_ws_doubles",
            "mpo_fused_backward_hook_step", "mpo_sharded_step", "mpo_last_error", "mpo_build_exact",
-           "mpo_launch_count")
+           "mpo_launch_count", "mpo_selfcheck_fastmath")
 
 
 class MpoError(RuntimeError):
@@ -70,6 +70,8 @@ def _declare(L):
     L.mpo_build_exact.restype = I32
     L.mpo_launch_count.restype = I64
     L.mpo_norm_ws_doubles.restype = I64
+    L.mpo_selfcheck_fastmath.argtypes = [I64, C.c_uint64, P, P]
+    L.mpo_selfcheck_fastmath.restype = C.c_int
 
 
 def load(exact: bool = False):

@@ -218,6 +218,15 @@ def mpo_sharded_step(kind: int, comm_ptr: int, rank: int, world: int, value_flat
                                      value_flat.numel(), C.byref(chp), _ptr(norm_ws), _stream(stream)))
 
 
+def mpo_selfcheck_fastmath(pairs: int = 1 << 30, seed: int = 0xB0B, exact: bool = False, stream=None):
+    """Fast sqrt/div sequences vs IEEE sqrtf and `/` on the device (diagnostic; see include/mpo.h).
+    Returns (sqrt mismatches, div mismatches, sqrt fast-path count, div fast-path count)."""
+    counts = torch.zeros(4, dtype=torch.int64, device="cuda")
+    L = _lib_of(exact)
+    _lib.check(L, L.mpo_selfcheck_fastmath(pairs, seed, _ptr(counts), _stream(stream)))
+    return tuple(int(x) for x in counts.cpu())
+
+
 def norm_ws_doubles(exact: bool = False) -> int:
     return int(_lib_of(exact).mpo_norm_ws_doubles())
 

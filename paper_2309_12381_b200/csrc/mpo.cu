@@ -243,6 +243,10 @@ struct AdamOp {
     __device__ __forceinline__ static float apply(float w, float g, float& m, float& v, const K& c) {
         return adam_update(w, g, m, v, c);
     }
+    __device__ __forceinline__ static float apply_fast(float w, float g, float& m, float& v, const K& c,
+                                                       uint32_t& bad) {
+        return adam_update_t<true>(w, g, m, v, c, bad);
+    }
 };
 
 template <int F, int G>
@@ -254,6 +258,9 @@ struct SgdOp {
     __device__ __forceinline__ static bool writes_m(const K& c) { return c.has_mom; }
     __device__ __forceinline__ static float apply(float w, float g, float& m, float&, const K& c) {
         return sgd_update(w, g, m, c);
+    }
+    __device__ __forceinline__ static float apply_fast(float w, float g, float& m, float& v, const K& c, uint32_t&) {
+        return apply(w, g, m, v, c);
     }
 };
 
@@ -277,11 +284,30 @@ __device__ __forceinline__ void process_unit(const uint4& hv, const uint4& rv, c
             w[2 * q + 1] = reconstruct1<F>(hi16(h[q]), shi16(r[q]));
         }
     }
+    float g[8], wn[8], mn[8], vn[8];
+    uint32_t bad = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        float g = grad_at<G>(gu, k) * c.gs;
-        if constexpr (CLIP) g = g * coef;
-        w[k] = Op::apply(w[k], g, mm[k], vv[k], c);
+        g[k] = grad_at<G>(gu, k) * c.gs;
+        if constexpr (CLIP) g[k] = g[k] * coef;
+        mn[k] = mm[k];
+        vn[k] = vv[k];
+        wn[k] = Op::apply_fast(w[k], g[k], mn[k], vn[k], c, bad);
+    }
+    if (__builtin_expect(bad != 0u, 0)) {
+        // an operand left the fast sqrt/div range: redo the unit with the full IEEE operators
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            mn[k] = mm[k];
+            vn[k] = vv[k];
+            wn[k] = Op::apply(w[k], g[k], mn[k], vn[k], c);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        w[k] = wn[k];
+        mm[k] = mn[k];
+        vv[k] = vn[k];
     }
     uint32_t* hop = &ho.x;
     uint32_t* rop = &ro.x;
@@ -561,6 +587,55 @@ __global__ void __launch_bounds__(kTmaThreads, 1) step_tma_kernel(const __grid_c
             process_tail<F, G, Op, CLIP>(T, base + nvec, base + nvalid, c, coef);
         }
     }
+}
+
+// ------------------------------------------------------------------------------------------
+// Self-check of the branch-free fast sqrt / division against the IEEE operators.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+__global__ void __launch_bounds__(kThreads) selfcheck_sqrt_kernel(unsigned long long* counts) {
+    unsigned long long bad_cnt = 0, fast_cnt = 0;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < (1ull << 32); u += stride) {
+        const float x = __uint_as_float(uint32_t(u));
+        uint32_t bad = 0;
+        const float f = sqrt_rn_fast(x, bad);
+        if (!bad) {
+            ++fast_cnt;
+            if (__float_as_uint(f) != __float_as_uint(sqrtf(x))) ++bad_cnt;
+        }
+    }
+    atomicAdd(&counts[0], bad_cnt);
+    atomicAdd(&counts[2], fast_cnt);
+}
+
+__global__ void __launch_bounds__(kThreads) selfcheck_div_kernel(int64_t pairs, uint64_t seed, unsigned long long* counts) {
+    unsigned long long bad_cnt = 0, fast_cnt = 0;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < pairs; i += stride) {
+        const uint64_t r = splitmix64(seed ^ splitmix64(uint64_t(i)));
+        uint32_t ab = uint32_t(r), bb = uint32_t(r >> 32);
+        if (i & 1) {   // half the pairs: exponents inside the accepted window [67, 187]
+            ab = (ab & 0x807FFFFFu) | ((67u + (ab >> 23) % 121u) << 23);
+            bb = (bb & 0x807FFFFFu) | ((67u + (bb >> 23) % 121u) << 23);
+        }
+        if ((i & 15) == 2) ab &= 0x80000000u;   // signed zero dividends
+        const float a = __uint_as_float(ab), b = __uint_as_float(bb);
+        uint32_t bad = 0;
+        const float f = div_rn_fast(a, b, bad);
+        if (!bad) {
+            ++fast_cnt;
+            if (__float_as_uint(f) != __float_as_uint(a / b)) ++bad_cnt;
+        }
+    }
+    atomicAdd(&counts[1], bad_cnt);
+    atomicAdd(&counts[3], fast_cnt);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -857,6 +932,23 @@ MPO_API int32_t mpo_build_exact(void) { return 0; }
 MPO_API int64_t mpo_launch_count(void) { return g_launches.load(); }
 
 MPO_API int64_t mpo_norm_ws_doubles(void) { return 1 + kNormBlocksMax; }
+
+MPO_API mpo_status mpo_selfcheck_fastmath(int64_t pairs, uint64_t seed, unsigned long long* counts,
+                                          mpo_stream stream) {
+    g_err.clear();
+    if (pairs < 0) return fail(MPO_EINVAL, "negative pair count");
+    if (!counts) return fail(MPO_EINVAL, "NULL counts");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(counts, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess)
+        return check_launch("cudaMemsetAsync");
+    const unsigned grid = unsigned(num_sms()) * 8u;
+    selfcheck_sqrt_kernel<<<grid, kThreads, 0, s>>>(counts);
+    ++g_launches;
+    if (check_launch("selfcheck_sqrt_kernel") != MPO_OK) return MPO_ECUDA;
+    selfcheck_div_kernel<<<grid, kThreads, 0, s>>>(pairs, seed, counts);
+    ++g_launches;
+    return check_launch("selfcheck_div_kernel");
+}
 
 MPO_API mpo_status mpo_split(mpo_dtype vdt, const float* w, void* value, int16_t* resid, int64_t n,
                              mpo_stream stream) {
