@@ -437,6 +437,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Orders this thread's generic-proxy shared-memory reads of a stage before the async-proxy (bulk
+// copy) writes that will refill it: without it the producer's next cp.async.bulk can land in the
+// stage under a still-pending LDS (seen as wrong value/residual words).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -549,8 +555,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) step_tma_kernel(const __grid_c
         const int64_t el = int64_t(ct) * kUnitEl;
         mbar_wait(&full[s], round & 1u);
         const bool full_unit = el + kUnitEl <= nvec;
-        uint4 hv, rv;
+        uint4 hv = make_uint4(0u, 0u, 0u, 0u), rv = hv;
         GradUnit<G> gu;
+        gu.a = gu.b = hv;
         float mm[8], vv[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) mm[k] = vv[k] = 0.0f;
@@ -576,7 +583,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) step_tma_kernel(const __grid_c
             }
         }
         // the warp's share of the stage now sits in registers: release the stage to the producer
-        // before the arithmetic, so the next bulk copies overlap this tile's compute
+        // before the arithmetic, so the next bulk copies overlap this tile's compute (the proxy
+        // fence orders the reads before the refill).
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         if (full_unit) {

@@ -402,11 +402,24 @@ def test_gpt2_adamw_full(mpo, orc, exact):
     hg = np.concatenate([host16(x) for x in V]); rg = np.concatenate([x.cpu().numpy() for x in R])
     mg = np.concatenate([x.cpu().numpy() for x in M]); vg = np.concatenate([x.cpu().numpy() for x in W])
     if exact:
-        assert np.array_equal(hg, h) and np.array_equal(rg, r)
+        bad = np.nonzero((hg != h) | (rg != r))[0]
+        assert len(bad) == 0, _report(bad, sizes, pre, orc.widen(fmt, g), (hg, rg, mg, vg), (h, r, m, v))
         assert same_bits_nan_equal(mg, m) and same_bits_nan_equal(vg, v)
     else:
         _check_fma_tolerance(fmt, pre, (hg, rg, mg, vg), (h, r, m, v), orc.widen(fmt, g),
                              _adam_uscale(hp, pre[2], orc.widen(fmt, g), v))
+
+
+def _report(bad, sizes, pre, g32, gpu, orc_):
+    """Failure report: count, the tensors hit, and the first elements with their inputs."""
+    offs = np.cumsum([0] + list(sizes))
+    tens = sorted(set(int(np.searchsorted(offs, i, side="right") - 1) for i in bad))
+    lines = [f"{len(bad)} mismatches in tensors {tens[:20]} (offsets {[int(offs[t]) for t in tens[:5]]})"]
+    for i in bad[:6]:
+        lines.append(f"i={i} h0={pre[0][i]:04x} r0={pre[1][i]} m0={pre[2][i]!r} v0={pre[3][i]!r} g={g32[i]!r} | "
+                     f"gpu h={gpu[0][i]:04x} r={gpu[1][i]} m={gpu[2][i]!r} v={gpu[3][i]!r} | "
+                     f"orc h={orc_[0][i]:04x} r={orc_[1][i]} m={orc_[2][i]!r} v={orc_[3][i]!r}")
+    return "\n".join(lines)
 
 
 @pytest.mark.parametrize("exact", [False, True])
