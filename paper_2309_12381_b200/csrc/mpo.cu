@@ -243,9 +243,9 @@ struct AdamOp {
     __device__ __forceinline__ static float apply(float w, float g, float& m, float& v, const K& c) {
         return adam_update(w, g, m, v, c);
     }
-    __device__ __forceinline__ static float apply_fast(float w, float g, float& m, float& v, const K& c,
-                                                       uint32_t& bad) {
-        return adam_update_t<true>(w, g, m, v, c, bad);
+    __device__ __forceinline__ static bool unit_fast(float (&w)[8], const float (&g)[8], float (&m)[8], float (&v)[8],
+                                                     const K& c) {
+        return adam_unit_fast(w, g, m, v, c);
     }
 };
 
@@ -259,8 +259,11 @@ struct SgdOp {
     __device__ __forceinline__ static float apply(float w, float g, float& m, float&, const K& c) {
         return sgd_update(w, g, m, c);
     }
-    __device__ __forceinline__ static float apply_fast(float w, float g, float& m, float& v, const K& c, uint32_t&) {
-        return apply(w, g, m, v, c);
+    __device__ __forceinline__ static bool unit_fast(float (&w)[8], const float (&g)[8], float (&m)[8], float (&v)[8],
+                                                     const K& c) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] = apply(w[k], g[k], m[k], v[k], c);
+        return true;
     }
 };
 
@@ -271,48 +274,35 @@ __device__ __forceinline__ void process_unit(const uint4& hv, const uint4& rv, c
                                              uint4& ro) {
     const uint32_t* h = &hv.x;
     const uint32_t* r = &rv.x;
-    float w[8];
+    float w[8], g[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        g[k] = grad_at<G>(gu, k) * c.gs;
+        if constexpr (CLIP) g[k] = g[k] * coef;
+    }
     const uint32_t special = nonfinite_pair<F>(h[0]) | nonfinite_pair<F>(h[1]) | nonfinite_pair<F>(h[2]) |
                              nonfinite_pair<F>(h[3]);
+    bool done = false;
     if (__builtin_expect(special == 0u, 1)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) reconstruct_pair_finite<F>(h[q], r[q], w[2 * q], w[2 * q + 1]);
-    } else {
+        done = Op::unit_fast(w, g, mm, vv, c);
+    }
+    if (__builtin_expect(!done, 0)) {
+        // non-finite values, or an operand outside the fast sqrt/div windows: the general path
+        // (full IEEE operators; mm/vv are untouched by a failed fast attempt)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             w[2 * q] = reconstruct1<F>(lo16(h[q]), slo16(r[q]));
             w[2 * q + 1] = reconstruct1<F>(hi16(h[q]), shi16(r[q]));
         }
-    }
-    float g[8], wn[8], mn[8], vn[8];
-    uint32_t bad = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        g[k] = grad_at<G>(gu, k) * c.gs;
-        if constexpr (CLIP) g[k] = g[k] * coef;
-        mn[k] = mm[k];
-        vn[k] = vv[k];
-        wn[k] = Op::apply_fast(w[k], g[k], mn[k], vn[k], c, bad);
+        for (int k = 0; k < 8; ++k) w[k] = Op::apply(w[k], g[k], mm[k], vv[k], c);
     }
-    if (__builtin_expect(bad != 0u, 0)) {
-        // an operand left the fast sqrt/div range: redo the unit with the full IEEE operators
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            mn[k] = mm[k];
-            vn[k] = vv[k];
-            wn[k] = Op::apply(w[k], g[k], mn[k], vn[k], c);
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        w[k] = wn[k];
-        mm[k] = mn[k];
-        vv[k] = vn[k];
-    }
-    uint32_t* hop = &ho.x;
-    uint32_t* rop = &ro.x;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) split2_fast<F>(w[2 * q], w[2 * q + 1], hop[q], rop[q]);
+    uint32_t hq[4], rq[4];
+    split8<F>(w, hq, rq);
+    ho = make_uint4(hq[0], hq[1], hq[2], hq[3]);
+    ro = make_uint4(rq[0], rq[1], rq[2], rq[3]);
 }
 
 // Ragged tail of one tensor (n % 8 elements): element by element from global memory.
@@ -709,6 +699,10 @@ AdamK derive_adam(const mpo_adam_hp& h) {
     c.wd = float(h.weight_decay);
     c.mode = h.adamw ? 1 : (h.weight_decay != 0.0 ? 2 : 0);
     c.lerp_hi = (c.b1c < 0.5f) ? 0 : 1;
+    c.dec1 = c.mode == 1 ? c.dec : 1.0f;
+    c.wdl2 = c.mode == 2 ? c.wd : 0.0f;
+    c.fast_ok = !c.lerp_hi && c.bc2s >= 0x1p-60f && c.bc2s < 0x1p61f;
+    c._pad = 0;
     return c;
 }
 
