@@ -48,6 +48,18 @@ def flags(exact: bool):
     return f
 
 
+def build_variant(name: str, defines, exact: bool = False) -> str:
+    """Build an experimental variant (extra -D defines) into lib/variants/ (A/B measurements)."""
+    out = os.path.join(LIBDIR, "variants", f"libmpo_{name}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [NVCC, *flags(exact), *[f"-D{d}" for d in defines], "-o", out, *SOURCES]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"nvcc failed building variant {name}")
+    return out
+
+
 def lib_path(exact: bool = False) -> str:
     return os.path.join(LIBDIR, "libmpo_exact.so" if exact else "libmpo.so")
 

@@ -79,6 +79,9 @@ def load(exact: bool = False):
     key = bool(exact)
     if key not in _libs:
         path = _build.lib_path(exact)
+        override = os.environ.get("MPO_LIB_OVERRIDE")   # A/B experiments only (scripts/ab_variants.py)
+        if override and not exact:
+            path = override
         if not os.path.exists(path):
             raise ImportError(f"{path} is missing: build it with `python -m paper_2309_12381_b200._build` "
                               "(there is no CPU fallback)")

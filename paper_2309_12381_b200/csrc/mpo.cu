@@ -31,10 +31,17 @@
 
 namespace mpo {
 
+#ifndef MPO_CW
+#define MPO_CW 16            // consumer warps per CTA of the TMA kernel (A/B knob)
+#endif
+#ifndef MPO_CTAS_PER_SM
+#define MPO_CTAS_PER_SM 1    // resident TMA CTAs per SM (A/B knob)
+#endif
 constexpr int kThreads = 256;
-constexpr int kUnroll = 2;                          // units per thread per tile
 constexpr int kUnitEl = 8;                          // elements per unit (128-bit of 16-bit data)
-constexpr int64_t kTileEl = int64_t(kThreads) * kUnroll * kUnitEl;   // 4096 elements
+constexpr int64_t kTileEl = int64_t(MPO_CW) * 32 * kUnitEl;   // 4096 elements: one unit per consumer thread
+constexpr int kUnroll = int(kTileEl / (kThreads * kUnitEl));  // LSU kernel: units per thread per tile
+static_assert(kUnroll >= 1, "tile smaller than one LSU pass");
 constexpr int kNormBlocksMax = 2048;                // partial sums of the norm pre-pass
 
 struct KT {                 // one table entry inside the kernel parameter block
@@ -408,7 +415,7 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const __grid_constant__ 
 // evict-first); kCW consumer warps read the stage from shared memory, compute, and store the
 // results straight to HBM with 128-bit stores, then release the stage.  Loads are therefore
 // issued independently of the arithmetic, several tiles ahead.
-constexpr int kCW = 16;                                  // consumer warps per CTA
+constexpr int kCW = MPO_CW;                              // consumer warps per CTA
 constexpr int kTmaThreads = (kCW + 1) * 32;              // + 1 producer warp
 static_assert(kCW * 32 * kUnitEl == kTileEl, "one unit per consumer thread per tile");
 constexpr int kMaxStages = 8;
@@ -431,7 +438,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // copy) writes that will refill it: without it the producer's next cp.async.bulk can land in the
 // stage under a still-pending LDS (seen as wrong value/residual words).
 __device__ __forceinline__ void fence_proxy_async_smem() {
+#ifndef MPO_NO_PROXY_FENCE   // diagnostic A/B knob only: the fence is required for correctness
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -470,7 +479,7 @@ __host__ __device__ constexpr int stage_bytes() {
 }
 
 template <int MAXT, int F, int G, class Op, bool CLIP>
-__global__ void __launch_bounds__(kTmaThreads, 1) step_tma_kernel(const __grid_constant__ Table<MAXT> tab,
+__global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(const __grid_constant__ Table<MAXT> tab,
                                                                   const __grid_constant__ HP<typename Op::K> hp,
                                                                   const double* __restrict__ sumsq, double max_norm,
                                                                   int stages) {
@@ -572,15 +581,34 @@ __global__ void __launch_bounds__(kTmaThreads, 1) step_tma_kernel(const __grid_c
                 vv[0] = a.x; vv[1] = a.y; vv[2] = a.z; vv[3] = a.w; vv[4] = b.x; vv[5] = b.y; vv[6] = b.z; vv[7] = b.w;
             }
         }
+#ifdef MPO_RELEASE_EARLY
         // the warp's share of the stage now sits in registers: release the stage to the producer
         // before the arithmetic, so the next bulk copies overlap this tile's compute (the proxy
         // fence orders the reads before the refill).
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
+#endif
+        uint4 ho, ro;
+#ifdef MPO_TRIVIAL_MATH
+        // roofline experiment only: same bytes moved, trivial arithmetic (not a product path)
         if (full_unit) {
-            uint4 ho, ro;
-            process_unit<F, G, Op, CLIP>(hv, rv, gu, mm, vv, c, coef, ho, ro);
+            ho = make_uint4(hv.x ^ gu.a.x, hv.y ^ gu.a.y, hv.z ^ gu.a.z, hv.w ^ gu.a.w);
+            ro = make_uint4(rv.x + 1u, rv.y + 1u, rv.z + 1u, rv.w + 1u);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { mm[k] = mm[k] * 0.5f; vv[k] = vv[k] * 0.25f; }
+        }
+#else
+        if (full_unit) process_unit<F, G, Op, CLIP>(hv, rv, gu, mm, vv, c, coef, ho, ro);
+#endif
+#ifndef MPO_RELEASE_EARLY
+        // release after the arithmetic has consumed the registers (the proxy fence then waits on
+        // nothing still pending from this stage)
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+#endif
+        if (full_unit) {
             store_unit<Op>(T, base + el, ho, ro, mm, vv, Op::writes_m(c));
         } else if (el == nvec && nvec < nvalid) {
             process_tail<F, G, Op, CLIP>(T, base + nvec, base + nvalid, c, coef);
@@ -816,7 +844,7 @@ bool use_tma() {
     return tma;
 }
 
-constexpr int kSmemBudget = 227 * 1024;
+constexpr int kSmemBudget = (MPO_CTAS_PER_SM == 1 ? 227 * 1024 : (228 * 1024) / MPO_CTAS_PER_SM - 1024);
 
 template <int MAXT, int F, int G, class Op, bool CLIP>
 mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typename Op::K>& hp, bool one_hp,
@@ -833,7 +861,7 @@ mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typen
         constexpr int smem = kBarBytes + stages * SB;
         static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (attr != cudaSuccess) return fail(MPO_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr));
-        const int64_t grid = grid_for(tiles, 1);
+        const int64_t grid = grid_for(tiles, MPO_CTAS_PER_SM);
         kern<<<unsigned(grid), kTmaThreads, smem, s>>>(tab, hp, sumsq, max_norm, stages);
         ++g_launches;
         return check_launch("step_tma_kernel");
