@@ -493,10 +493,12 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
                     for m_, p in zip(master, params):
                         p.copy_(m_)
                 return loss
+        torch.cuda.synchronize()
+        state = torch.cuda.memory_allocated()      # params + residual/master + optimizer state
         for _ in range(warmup):
             step()
         torch.cuda.synchronize()
-        persistent = torch.cuda.memory_allocated()
+        persistent = torch.cuda.memory_allocated()  # what survives between training steps
         torch.cuda.reset_peak_memory_stats()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
@@ -505,7 +507,8 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
         e.record()
         torch.cuda.synchronize()
         peak = torch.cuda.max_memory_allocated()
-        res = {"ms_per_train_step": s.elapsed_time(e) / steps, "persistent_bytes_per_param": persistent / P,
+        res = {"ms_per_train_step": s.elapsed_time(e) / steps, "state_bytes_per_param": state / P,
+               "persistent_bytes_per_param": persistent / P,
                "peak_bytes_per_param": peak / P, "peak_gb": peak / 1e9, "loss": float(loss)}
         del model, opt
         torch.cuda.empty_cache()

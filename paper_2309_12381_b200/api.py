@@ -109,7 +109,6 @@ class TensorTable:
         if not (len(resids) == len(grads) == len(ms) == len(vs) == n):
             raise MpoError(_lib.MPO_EINVAL, "table columns differ in length")
         self.values, self.resids, self.ms, self.vs = list(values), list(resids), list(ms), list(vs)
-        self.grads = list(grads)
         self.hp_index = list(hp_index) if hp_index is not None else [0] * n
         self.arr = (Tensor * max(n, 1))()
         self.nt = n
@@ -143,7 +142,8 @@ class TensorTable:
             elif c != gdt:
                 raise MpoError(_lib.MPO_EDTYPE, f"tensor {i}: mixed gradient dtypes in one table")
             self.arr[i].grad = _ptr(g)
-        self.grads = list(grads)
+        # pointers only: the table must not keep gradients alive (hook / set_to_none training frees them)
+        self.grad_ptrs = [g.data_ptr() for g in grads]
         self.gdt = gdt if gdt is not None else self.vdt
 
 

@@ -82,7 +82,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                                   [0] * len(params))
             tab._group_of = [gi[id(p)] for p in params]
             self._tables[key] = tab
-        elif any(g.data_ptr() != og.data_ptr() for g, og in zip(grads, tab.grads)):
+        elif [g.data_ptr() for g in grads] != tab.grad_ptrs:
             tab.set_grads(grads)
         return tab
 

@@ -1,0 +1,135 @@
+"""The data-parallel sharded path's host logic at world size 2 on CPU (gloo), no GPU.
+
+The GPU path (mpo_sharded_step) is NCCL reduce-scatter -> update of this rank's shard -> NCCL
+all-gather of the 16-bit values.  Here the same decomposition is exercised with the product's
+ShardLayout and gloo collectives, with the CPU oracle doing the shard update:
+* the layout partitions the flat buffer exactly (every element of every parameter in exactly one
+  shard; 16-byte-aligned parameter offsets; total a multiple of 8*world);
+* sharded == unsharded (P8): per-rank gradients built so the cross-rank sum is exact (reading R13),
+  grad_scale = 1/N, then each rank updates only its shard and the all-gathered values equal the
+  unsharded oracle step on the mean gradient, bit for bit, for Adam (with and without global-norm
+  clipping, whose shard sums are all-reduced) and SGD-momentum.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import synth
+from paper_2309_12381_b200.sharded import ShardLayout
+
+SIZES = [33 * 17, 4096, 5, 128 * 64, 1000, 3]
+
+
+def test_layout_partitions_exactly():
+    for world in (1, 2, 3, 4, 8):
+        L = ShardLayout(SIZES, world)
+        assert L.total % (8 * world) == 0 and L.shard * world == L.total
+        assert all(o % 8 == 0 for o in L.offsets)
+        seen = {i: np.zeros(n, np.int32) for i, n in enumerate(SIZES)}
+        for r in range(world):
+            lo, hi = L.shard_range(r)
+            for i, a, b, n in L.owner_slices(r):
+                assert 0 <= b and b + n <= L.shard
+                assert L.offsets[i] + a == lo + b
+                seen[i][a:a + n] += 1
+        assert all((c == 1).all() for c in seen.values())
+        # params never overlap
+        ends = [o + n for o, n in zip(L.offsets, SIZES)]
+        assert all(e <= o2 for e, o2 in zip(ends, L.offsets[1:]))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank_grads(rank, n, fmt):
+    # multiples of 2^-12 with |k| <= 16: the 2-rank sum (<= 32 * 2^3 scale, 8 significant bits) and
+    # the /2 mean are exact in bf16
+    q = synth.rng(77, rank).integers(-16, 17, size=n).astype(np.float32) * np.float32(2.0 ** -12)
+    return q
+
+
+def _worker(rank, world, port, kind, clip, out_dir):
+    import oracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fmt = "bf16"
+        L = ShardLayout(SIZES, world)
+        lo, hi = L.shard_range(rank)
+        # identical initial flat fp32 weights on every rank, split with the oracle
+        w = np.zeros(L.total, np.float32)
+        for i, (o, n) in enumerate(zip(L.offsets, SIZES)):
+            w[o:o + n] = synth.weights(n, 0.02, 0xB0B + i)
+        h, r = oracle.split(fmt, w)
+        # this rank's gradient (fp32 exact values) -> 16-bit as the backward would hand it over
+        g32 = np.zeros(L.total, np.float32)
+        for i, (o, n) in enumerate(zip(L.offsets, SIZES)):
+            g32[o:o + n] = _rank_grads(rank, n, fmt)[:n] * np.float32(2.0 ** (i % 4))
+        # reduce-scatter (gloo has no reduce_scatter: all_reduce + take the shard; exact sums)
+        t = torch.from_numpy(g32.copy())
+        dist.all_reduce(t)
+        gsum = t.numpy()[lo:hi].copy()
+        g16 = synth.to16_bits(gsum, fmt)
+        assert np.array_equal(oracle.widen(fmt, g16), gsum)          # the sum is exact in bf16
+        hs, rs = h[lo:hi].copy(), r[lo:hi].copy()
+        m = np.zeros(L.shard, np.float32)
+        v = np.zeros(L.shard, np.float32)
+        coef = None
+        if kind == "adam" and clip:
+            ss = torch.tensor([oracle.sumsq(fmt, g16, 1.0 / world)], dtype=torch.float64)
+            dist.all_reduce(ss)
+            coef = oracle.clip_coef(float(ss[0]), 0.01)
+        if kind == "adam":
+            oracle.adam_step(fmt, fmt, hs, rs, g16, m, v, lr=1e-3, weight_decay=0.1, grad_scale=1.0 / world,
+                             step=1, clip_coef=coef)
+        else:
+            oracle.sgd_step(fmt, fmt, hs, rs, g16, m, lr=0.1, momentum=0.9, grad_scale=1.0 / world, first_step=True)
+        # all-gather of the 16-bit values only
+        # (gloo has no int16 collectives: the 16-bit patterns travel widened to int32, unchanged)
+        parts = [torch.zeros(L.shard, dtype=torch.int32) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(hs.astype(np.int32)))
+        value = torch.cat(parts).numpy().astype(np.uint16)
+        np.save(os.path.join(out_dir, f"value_{rank}.npy"), value)
+        np.save(os.path.join(out_dir, f"resid_{rank}.npy"), rs)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,clip", [("adam", False), ("adam", True), ("sgd", False)])
+def test_sharded_equals_unsharded_world2(tmp_path, orc, kind, clip):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), kind, clip, str(tmp_path)), nprocs=world, join=True)
+    fmt = "bf16"
+    L = ShardLayout(SIZES, world)
+    w = np.zeros(L.total, np.float32)
+    g = np.zeros(L.total, np.float32)
+    for i, (o, n) in enumerate(zip(L.offsets, SIZES)):
+        w[o:o + n] = synth.weights(n, 0.02, 0xB0B + i)
+        g[o:o + n] = sum(_rank_grads(rk, n, fmt) for rk in range(world)) * np.float32(2.0 ** (i % 4))
+    h, r = orc.split(fmt, w)
+    g16 = synth.to16_bits(g, fmt)
+    m = np.zeros(L.total, np.float32)
+    v = np.zeros(L.total, np.float32)
+    if kind == "adam":
+        coef = orc.clip_coef(orc.sumsq(fmt, g16, 1.0 / world), 0.01) if clip else None
+        if clip:
+            assert coef < 1.0
+        orc.adam_step(fmt, fmt, h, r, g16, m, v, lr=1e-3, weight_decay=0.1, grad_scale=1.0 / world, step=1,
+                      clip_coef=coef)
+    else:
+        orc.sgd_step(fmt, fmt, h, r, g16, m, lr=0.1, momentum=0.9, grad_scale=1.0 / world, first_step=True)
+    for rank in range(world):
+        assert np.array_equal(np.load(tmp_path / f"value_{rank}.npy"), h)
+        lo, hi = L.shard_range(rank)
+        assert np.array_equal(np.load(tmp_path / f"resid_{rank}.npy"), r[lo:hi])
