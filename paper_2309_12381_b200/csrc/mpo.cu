@@ -192,31 +192,41 @@ __global__ void __launch_bounds__(kThreads) sumsq_kernel(const __grid_constant__
                                                          const __grid_constant__ HP<float> gsc,
                                                          double* __restrict__ partial) {
     __shared__ double sh[32];
-    double acc = 0.0;
+    // 8 independent fp64 accumulators per thread (one per unit lane): a single accumulator would
+    // serialise every DFMA of the thread.  Each square of a float is exact in fp64.
+    double acc8[kUnitEl];
+#pragma unroll
+    for (int k = 0; k < kUnitEl; ++k) acc8[k] = 0.0;
     int cur = 0;
     for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
         while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
         const KT& T = tab.t[cur];
         const float gs = gsc.g[T.hp];
         const int64_t base = int64_t(tile - T.tile0) * kTileEl;
+        GradUnit<G> gu[kUnroll];
+#pragma unroll
+        for (int j = 0; j < kUnroll; ++j) {   // all loads of the tile first
+            const int64_t e = base + (int64_t(j) * kThreads + threadIdx.x) * kUnitEl;
+            if (e + kUnitEl <= T.n) gu[j] = ld_grad<G>(T.grad, e);
+        }
 #pragma unroll
         for (int j = 0; j < kUnroll; ++j) {
             const int64_t e = base + (int64_t(j) * kThreads + threadIdx.x) * kUnitEl;
             if (e + kUnitEl <= T.n) {
-                GradUnit<G> gu = ld_grad<G>(T.grad, e);
 #pragma unroll
                 for (int k = 0; k < kUnitEl; ++k) {
-                    const double g = double(grad_at<G>(gu, k) * gs);
-                    acc += g * g;
+                    const double g = double(grad_at<G>(gu[j], k) * gs);
+                    acc8[k] = fma(g, g, acc8[k]);
                 }
             } else if (e < T.n) {
                 for (int64_t i = e; i < T.n; ++i) {
                     const double g = double(grad_scalar<G>(T.grad, i) * gs);
-                    acc += g * g;
+                    acc8[0] = fma(g, g, acc8[0]);
                 }
             }
         }
     }
+    double acc = ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
     acc = block_sum(acc, sh);
     if (threadIdx.x == 0) partial[blockIdx.x] = acc;
 }
@@ -915,7 +925,9 @@ mpo_status table_sumsq(mpo_dtype gdt, const mpo_tensor* t, int nt, const float* 
     for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) gsc.g[i] = i < nhp ? gs_of_group[i] : 1.0f;
     int64_t tiles = 0;
     for (int i = 0; i < nt; ++i) tiles += (t[i].n + kTileEl - 1) / kTileEl;
-    const int nblocks = int(grid_for(tiles, 4) < kNormBlocksMax ? grid_for(tiles, 4) : kNormBlocksMax);
+    static const int per_sm = resident_blocks(sumsq_kernel<kBigT, kBF16>);
+    const int64_t g0 = grid_for(tiles, per_sm);
+    const int nblocks = int(g0 < kNormBlocksMax ? g0 : kNormBlocksMax);
     double* partial = norm_ws + 1;
     int nparts = 0;
     // every slice writes its own run of partials, summed together at the end (fixed order)

@@ -430,3 +430,26 @@ def test_fast_sqrt_div_match_ieee(mpo, exact):
     sq_bad, div_bad, sq_fast, div_fast = api.mpo_selfcheck_fastmath(pairs=1 << 31, seed=0xC0FFEE, exact=exact)
     assert sq_bad == 0 and div_bad == 0
     assert sq_fast > (1 << 30) and div_fast > (1 << 29)
+
+
+def test_table_larger_than_one_launch(mpo, orc):
+    """A table of 1100 tensors spans three launches (<= 512 entries each); every tensor bit-exact,
+    including empty and single-element ones (exact build)."""
+    fmt = "bf16"
+    rs_ = synth.rng(5, 5)
+    sizes = [int(x) for x in rs_.integers(0, 300, size=1100)]
+    sizes[0], sizes[511], sizes[512], sizes[1099] = 0, 1, 4097, 8
+    hs, rs, gs = [], [], []
+    for i, n in enumerate(sizes):
+        h, r = orc.split(fmt, synth.weights(n, 0.02, 100 + i))
+        hs.append(h); rs.append(r); gs.append(synth.grads(n, 1e-3, fmt, 7, i))
+    V = [dev16(h, fmt) for h in hs]; R = [devi16(r) for r in rs]; G = [dev16(g, fmt) for g in gs]
+    M = [torch.zeros(n, device="cuda") for n in sizes]; W = [torch.zeros(n, device="cuda") for n in sizes]
+    hp = mpo.AdamParams(lr=1e-3, weight_decay=0.1, step=1)
+    n0 = mpo.api.launch_count(exact=True)
+    mpo.mpo_adam_step(mpo.TensorTable(V, R, G, M, W), hp, exact=True)
+    assert mpo.api.launch_count(exact=True) - n0 == 3
+    for i, n in enumerate(sizes):
+        m = np.zeros(n, np.float32); v = np.zeros(n, np.float32)
+        orc.adam_step(fmt, fmt, hs[i], rs[i], gs[i], m, v, **_adam_hp_kw(hp))
+        assert np.array_equal(host16(V[i]), hs[i]) and np.array_equal(R[i].cpu().numpy(), rs[i]), i
