@@ -554,7 +554,11 @@ def main():
     wl = Workload(args.workload, world, rank)
     sampler = ClockSampler(local) if rank == 0 else None
     ms, launches = timed(wl.step, args.steps, args.warmup, dist, sampler)
-    per_launch = ms * args.steps / max(1, launches)   # one step-kernel launch per step at N=1
+    # one step-kernel launch per step at N=1 without clipping: the region time per launch IS the
+    # kernel's mean launch duration; with clipping the step also holds the norm pre-pass (2 small
+    # launches), and at N>1 the NCCL collectives, so the whole step is reported (its bytes include
+    # the grad re-read: 28 B/param)
+    per_launch = ms
     clocks = sampler.stop() if sampler else None
     value = wl.P / (ms * 1e-3)
     n_upd = wl.layout.shard if world > 1 else wl.P

@@ -626,6 +626,100 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
     }
 }
 
+// ---- G5 on the bulk-copy pipeline: the clip pre-pass reads only the 16-bit grads (2 B/param),
+// so it needs many bytes in flight per SM; a producer warp streams tiles of grads into 8 stages
+// while 16 consumer warps square and accumulate (8 independent fp64 accumulators per thread).
+template <int MAXT, int G>
+__global__ void __launch_bounds__(kTmaThreads, 1) sumsq_tma_kernel(const __grid_constant__ Table<MAXT> tab,
+                                                                   const __grid_constant__ HP<float> gsc,
+                                                                   double* __restrict__ partial, int stages) {
+    constexpr int GB = GradBytes<G>::v;
+    constexpr int64_t TE = kTileEl;
+    constexpr int SB = int(TE) * GB;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double red[kCW];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + kMaxStages;
+    unsigned char* ring = smem + kBarBytes;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kCW) {
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            int cur = 0, it = 0;
+            for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x, ++it) {
+                const int s = it % stages;
+                mbar_wait(&empty[s], (uint32_t(it / stages) & 1u) ^ 1u);
+                while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
+                const KT& T = tab.t[cur];
+                const int64_t base = int64_t(tile - T.tile0) * TE;
+                const int64_t nvalid = T.n - base < TE ? T.n - base : TE;
+                const uint32_t nvec = uint32_t(nvalid) & ~uint32_t(kUnitEl - 1);
+                mbar_arrive_expect_tx(&full[s], nvec * GB);
+                if (nvec)
+                    bulk_g2s(ring + size_t(s) * SB, static_cast<const unsigned char*>(T.grad) + base * GB, nvec * GB,
+                             &full[s], pol);
+            }
+        }
+        return;
+    }
+    double acc8[kUnitEl];
+#pragma unroll
+    for (int k = 0; k < kUnitEl; ++k) acc8[k] = 0.0;
+    const int64_t el = int64_t(threadIdx.x) * kUnitEl;
+    int cur = 0, it = 0;
+    for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x, ++it) {
+        const int s = it % stages;
+        while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
+        const KT& T = tab.t[cur];
+        const float gs = gsc.g[T.hp];
+        const int64_t base = int64_t(tile - T.tile0) * TE;
+        const int64_t nvalid = T.n - base < TE ? T.n - base : TE;
+        const int64_t nvec = nvalid & ~int64_t(kUnitEl - 1);
+        mbar_wait(&full[s], uint32_t(it / stages) & 1u);
+        const bool full_unit = el + kUnitEl <= nvec;
+        GradUnit<G> gu;
+        gu.a = gu.b = make_uint4(0u, 0u, 0u, 0u);
+        if (full_unit) {
+            const unsigned char* st = ring + size_t(s) * SB;
+            gu.a = *reinterpret_cast<const uint4*>(st + el * GB);
+            if constexpr (G == kFP32) gu.b = *reinterpret_cast<const uint4*>(st + el * GB + 16);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (full_unit) {
+#pragma unroll
+            for (int k = 0; k < kUnitEl; ++k) {
+                const double g = double(grad_at<G>(gu, k) * gs);
+                acc8[k] = fma(g, g, acc8[k]);
+            }
+        } else if (el == nvec && nvec < nvalid) {
+            for (int64_t i = base + nvec; i < base + nvalid; ++i) {
+                const double g = double(grad_scalar<G>(T.grad, i) * gs);
+                acc8[0] = fma(g, g, acc8[0]);
+            }
+        }
+    }
+    double acc = ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xFFFFFFFFu, acc, o);
+    if (lane == 0) red[warp] = acc;
+    asm volatile("bar.sync 1, %0;" ::"r"(kCW * 32) : "memory");   // consumer warps only
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kCW; ++w) t += red[w];   // fixed order
+        partial[blockIdx.x] = t;
+    }
+}
+
 // ------------------------------------------------------------------------------------------
 // Self-check of the branch-free fast sqrt / division against the IEEE operators.
 // ------------------------------------------------------------------------------------------
@@ -834,11 +928,23 @@ int64_t fill_table(Table<MAXT>& tab, const mpo_tensor* t, int lo, int hi, bool o
     return tiles;
 }
 
+bool use_tma();
+constexpr int kSumsqStages = 8;
+
 template <int MAXT, int F, int G>
 mpo_status launch_sumsq(const mpo_tensor* t, int lo, int hi, const HP<float>& gsc, double* partial, int nblocks,
                         cudaStream_t s) {
     Table<MAXT> tab;
     fill_table(tab, t, lo, hi, false);
+    if (use_tma()) {
+        auto kern = sumsq_tma_kernel<MAXT, G>;
+        constexpr int smem = kBarBytes + kSumsqStages * int(kTileEl) * GradBytes<G>::v;
+        static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (attr != cudaSuccess) return fail(MPO_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr));
+        kern<<<nblocks, kTmaThreads, smem, s>>>(tab, gsc, partial, kSumsqStages);
+        ++g_launches;
+        return check_launch("sumsq_tma_kernel");
+    }
     sumsq_kernel<MAXT, G><<<nblocks, kThreads, 0, s>>>(tab, gsc, partial);
     ++g_launches;
     return check_launch("sumsq_kernel");
@@ -925,7 +1031,7 @@ mpo_status table_sumsq(mpo_dtype gdt, const mpo_tensor* t, int nt, const float* 
     for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) gsc.g[i] = i < nhp ? gs_of_group[i] : 1.0f;
     int64_t tiles = 0;
     for (int i = 0; i < nt; ++i) tiles += (t[i].n + kTileEl - 1) / kTileEl;
-    static const int per_sm = resident_blocks(sumsq_kernel<kBigT, kBF16>);
+    static const int per_sm = use_tma() ? 1 : resident_blocks(sumsq_kernel<kBigT, kBF16>);
     const int64_t g0 = grid_for(tiles, per_sm);
     const int nblocks = int(g0 < kNormBlocksMax ? g0 : kNormBlocksMax);
     double* partial = norm_ws + 1;
