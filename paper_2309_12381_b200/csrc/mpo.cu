@@ -187,13 +187,19 @@ __device__ __forceinline__ double block_sum(double s, double* sh) {
     return s;   // valid in thread 0
 }
 
+// The clip pre-pass reads 2 B/param and is issue-bound (widen, scale, F2F.F64, DFMA per element),
+// so it uses its own, larger tiles (kSumsqTileEl = 16 units per thread) to amortise the per-tile
+// bookkeeping, issues all 16 loads of a tile before any arithmetic, skips the scale multiply when
+// it is exactly 1, and keeps 8 independent fp64 accumulators per thread (a single accumulator
+// would serialise every DFMA).  Every square of a float is exact in fp64.
+constexpr int kSumsqUPT = 16;
+constexpr int64_t kSumsqTileEl = int64_t(kThreads) * kSumsqUPT * kUnitEl;   // 32768 elements
+
 template <int MAXT, int G>
 __global__ void __launch_bounds__(kThreads) sumsq_kernel(const __grid_constant__ Table<MAXT> tab,
                                                          const __grid_constant__ HP<float> gsc,
                                                          double* __restrict__ partial) {
     __shared__ double sh[32];
-    // 8 independent fp64 accumulators per thread (one per unit lane): a single accumulator would
-    // serialise every DFMA of the thread.  Each square of a float is exact in fp64.
     double acc8[kUnitEl];
 #pragma unroll
     for (int k = 0; k < kUnitEl; ++k) acc8[k] = 0.0;
@@ -202,26 +208,47 @@ __global__ void __launch_bounds__(kThreads) sumsq_kernel(const __grid_constant__
         while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
         const KT& T = tab.t[cur];
         const float gs = gsc.g[T.hp];
-        const int64_t base = int64_t(tile - T.tile0) * kTileEl;
-        GradUnit<G> gu[kUnroll];
+        const int64_t n = T.n;
+        const int64_t base = int64_t(tile - T.tile0) * kSumsqTileEl;
+        const char* gp = static_cast<const char*>(T.grad);
+        if (base + kSumsqTileEl <= n) {
+            GradUnit<G> gu[kSumsqUPT];
 #pragma unroll
-        for (int j = 0; j < kUnroll; ++j) {   // all loads of the tile first
-            const int64_t e = base + (int64_t(j) * kThreads + threadIdx.x) * kUnitEl;
-            if (e + kUnitEl <= T.n) gu[j] = ld_grad<G>(T.grad, e);
-        }
+            for (int j = 0; j < kSumsqUPT; ++j)
+                gu[j] = ld_grad<G>(T.grad, base + (int64_t(j) * kThreads + threadIdx.x) * kUnitEl);
+            if (gs == 1.0f) {
 #pragma unroll
-        for (int j = 0; j < kUnroll; ++j) {
-            const int64_t e = base + (int64_t(j) * kThreads + threadIdx.x) * kUnitEl;
-            if (e + kUnitEl <= T.n) {
+                for (int j = 0; j < kSumsqUPT; ++j)
 #pragma unroll
-                for (int k = 0; k < kUnitEl; ++k) {
-                    const double g = double(grad_at<G>(gu[j], k) * gs);
-                    acc8[k] = fma(g, g, acc8[k]);
-                }
-            } else if (e < T.n) {
-                for (int64_t i = e; i < T.n; ++i) {
-                    const double g = double(grad_scalar<G>(T.grad, i) * gs);
-                    acc8[0] = fma(g, g, acc8[0]);
+                    for (int k = 0; k < kUnitEl; ++k) {
+                        const double g = double(grad_at<G>(gu[j], k));
+                        acc8[k] = fma(g, g, acc8[k]);
+                    }
+            } else {
+#pragma unroll
+                for (int j = 0; j < kSumsqUPT; ++j)
+#pragma unroll
+                    for (int k = 0; k < kUnitEl; ++k) {
+                        const double g = double(grad_at<G>(gu[j], k) * gs);
+                        acc8[k] = fma(g, g, acc8[k]);
+                    }
+            }
+        } else {   // partial tile: unit by unit, ragged tail element by element
+            (void)gp;
+            for (int j = 0; j < kSumsqUPT; ++j) {
+                const int64_t e = base + (int64_t(j) * kThreads + threadIdx.x) * kUnitEl;
+                if (e + kUnitEl <= n) {
+                    const GradUnit<G> u = ld_grad<G>(T.grad, e);
+#pragma unroll
+                    for (int k = 0; k < kUnitEl; ++k) {
+                        const double g = double(grad_at<G>(u, k) * gs);
+                        acc8[k] = fma(g, g, acc8[k]);
+                    }
+                } else if (e < n) {
+                    for (int64_t i = e; i < n; ++i) {
+                        const double g = double(grad_scalar<G>(T.grad, i) * gs);
+                        acc8[0] = fma(g, g, acc8[0]);
+                    }
                 }
             }
         }
@@ -909,7 +936,7 @@ mpo_status check_table(const mpo_tensor* t, int32_t nt, int32_t nhp, bool adam, 
 
 // Fill a kernel table from t[lo, hi); returns the tile count.
 template <int MAXT>
-int64_t fill_table(Table<MAXT>& tab, const mpo_tensor* t, int lo, int hi, bool one_hp) {
+int64_t fill_table(Table<MAXT>& tab, const mpo_tensor* t, int lo, int hi, bool one_hp, int64_t tile_el = kTileEl) {
     int64_t tiles = 0;
     tab.nt = hi - lo;
     for (int i = lo; i < hi; ++i) {
@@ -922,21 +949,28 @@ int64_t fill_table(Table<MAXT>& tab, const mpo_tensor* t, int lo, int hi, bool o
         k.n = t[i].n;
         k.hp = one_hp ? 0 : t[i].hp;
         k.tile0 = int32_t(tiles);
-        tiles += (t[i].n + kTileEl - 1) / kTileEl;
+        tiles += (t[i].n + tile_el - 1) / tile_el;
     }
     tab.ntiles = int32_t(tiles);
     return tiles;
 }
 
-bool use_tma();
 constexpr int kSumsqStages = 8;
+// The clip pre-pass uses the LSU kernel unless MPO_SUMSQ_KERNEL=tma (A/B knob; see sumsq_kernel).
+bool use_tma_sumsq() {
+    static const bool tma = [] {
+        const char* e = std::getenv("MPO_SUMSQ_KERNEL");
+        return e && std::strcmp(e, "tma") == 0;
+    }();
+    return tma;
+}
 
 template <int MAXT, int F, int G>
 mpo_status launch_sumsq(const mpo_tensor* t, int lo, int hi, const HP<float>& gsc, double* partial, int nblocks,
                         cudaStream_t s) {
     Table<MAXT> tab;
-    fill_table(tab, t, lo, hi, false);
-    if (use_tma()) {
+    fill_table(tab, t, lo, hi, false, use_tma_sumsq() ? kTileEl : kSumsqTileEl);
+    if (use_tma_sumsq()) {
         auto kern = sumsq_tma_kernel<MAXT, G>;
         constexpr int smem = kBarBytes + kSumsqStages * int(kTileEl) * GradBytes<G>::v;
         static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1030,8 +1064,9 @@ mpo_status table_sumsq(mpo_dtype gdt, const mpo_tensor* t, int nt, const float* 
     HP<float> gsc;
     for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) gsc.g[i] = i < nhp ? gs_of_group[i] : 1.0f;
     int64_t tiles = 0;
-    for (int i = 0; i < nt; ++i) tiles += (t[i].n + kTileEl - 1) / kTileEl;
-    static const int per_sm = use_tma() ? 1 : resident_blocks(sumsq_kernel<kBigT, kBF16>);
+    const int64_t te = use_tma_sumsq() ? kTileEl : kSumsqTileEl;
+    for (int i = 0; i < nt; ++i) tiles += (t[i].n + te - 1) / te;
+    static const int per_sm = use_tma_sumsq() ? 1 : resident_blocks(sumsq_kernel<kBigT, kBF16>);
     const int64_t g0 = grid_for(tiles, per_sm);
     const int nblocks = int(g0 < kNormBlocksMax ? g0 : kNormBlocksMax);
     double* partial = norm_ws + 1;
@@ -1242,14 +1277,16 @@ MPO_API mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t
         if ((st = check_table(&x, 1, 1, false, h)) != MPO_OK) return st;
     }
     // 1. reduce-scatter of the 16-bit gradients (sum), in place: shard `rank` of grad_flat
-    MPO_NCCL(ncclReduceScatter(grad_flat, const_cast<void*>(x.grad), size_t(shard), nccl_dtype(vdt), ncclSum, comm, s));
+    //    (world 1: the reduction of one rank is the identity and the in-place shard is the buffer)
+    if (world > 1)
+        MPO_NCCL(ncclReduceScatter(grad_flat, const_cast<void*>(x.grad), size_t(shard), nccl_dtype(vdt), ncclSum, comm, s));
     // 2. residual-compensated update of this rank's shard
     if (kind == MPO_ADAM) {
         const mpo_adam_hp* h = static_cast<const mpo_adam_hp*>(hp);
         if (h->max_grad_norm > 0.0) {
             float gs = float(h->grad_scale);
             if ((st = table_sumsq(vdt, &x, 1, &gs, 1, norm_ws, s)) != MPO_OK) return st;
-            MPO_NCCL(ncclAllReduce(norm_ws, norm_ws, 1, ncclFloat64, ncclSum, comm, s));
+            if (world > 1) MPO_NCCL(ncclAllReduce(norm_ws, norm_ws, 1, ncclFloat64, ncclSum, comm, s));
         }
         if ((st = adam_common(vdt, vdt, &x, 1, h, 1, norm_ws, true, s, true)) != MPO_OK) return st;
     } else {
@@ -1259,6 +1296,6 @@ MPO_API mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t
         if ((st = dispatch_step<SgdOp, false>(vdt, vdt, &x, 1, k, true, nullptr, 0.0, s)) != MPO_OK) return st;
     }
     // 3. all-gather of the 16-bit values only (residual and state never move)
-    MPO_NCCL(ncclAllGather(x.value, value_flat, size_t(shard), nccl_dtype(vdt), comm, s));
+    if (world > 1) MPO_NCCL(ncclAllGather(x.value, value_flat, size_t(shard), nccl_dtype(vdt), comm, s));
     return MPO_OK;
 }
