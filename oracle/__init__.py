@@ -74,6 +74,18 @@ def lib():
         L.or_sumsq.argtypes = [C.c_int, P, C.c_int64, C.c_double]
         L.or_clip_coef.restype = C.c_float
         L.or_clip_coef.argtypes = [C.c_double, C.c_double]
+        L.or_rtz16.restype = C.c_uint16
+        L.or_rtz16.argtypes = [C.c_int, C.c_uint32]
+        L.or_sr16.restype = C.c_uint16
+        L.or_sr16.argtypes = [C.c_uint32, C.c_uint32]
+        L.or_mix64.restype = C.c_uint64
+        L.or_mix64.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+        L.or_split_s.argtypes = [C.c_int, C.c_int, P, P, P, C.c_int64, C.c_uint64, C.c_uint64]
+        L.or_reconstruct_s.argtypes = [C.c_int, C.c_int, P, P, P, C.c_int64]
+        L.or_sgd_step_s.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, P, C.c_int64, C.POINTER(SgdHP),
+                                    C.c_uint64, C.c_uint64]
+        L.or_adam_step_s.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, P, P, C.c_int64, C.POINTER(AdamHP),
+                                     C.c_float, C.c_uint64, C.c_uint64]
         L.or_bytes_per_param.restype = C.c_int
         L.or_bytes_per_param.argtypes = [C.c_int, C.c_int]
         L.or_fpenv_clear()
@@ -190,3 +202,55 @@ def bytes_per_param(scheme: str, optim: str) -> int:
     s = {"amp": 0, "ours_fused_backward": 1, "ours_multi_tensor": 2}[scheme]
     o = {"sgd_momentum": 0, "adam": 1}[optim]
     return lib().or_bytes_per_param(s, o)
+
+
+# ---- paper variants of the storage scheme (oracle.c "Paper variants") ----
+SCHEME = {"rne": 0, "rtz": 1, "sr": 2, "x8": 3}
+RESID_DTYPE = {"rne": np.int16, "rtz": np.uint16, "sr": np.int16, "x8": np.int8}
+
+
+def rtz16(fmt: str, u: int) -> int:
+    return lib().or_rtz16(FMT[fmt], u)
+
+
+def sr16(u: int, rnd: int) -> int:
+    return lib().or_sr16(u, rnd)
+
+
+def mix64(seed: int, stream: int, index: int) -> int:
+    return lib().or_mix64(seed, stream, index)
+
+
+def split_s(scheme: str, fmt: str, w: np.ndarray, seed: int = 0, stream: int = 0):
+    """fp32 -> (value uint16 bits, residual in the scheme's dtype)."""
+    w = _chk(np.ascontiguousarray(w, dtype=np.float32), np.float32)
+    h = np.empty(w.shape, np.uint16)
+    r = np.empty(w.shape, RESID_DTYPE[scheme])
+    lib().or_split_s(SCHEME[scheme], FMT[fmt], _ptr(w), _ptr(h), _ptr(r), w.size, seed, stream)
+    return h, r
+
+
+def reconstruct_s(scheme: str, fmt: str, h: np.ndarray, r: np.ndarray) -> np.ndarray:
+    h = _chk(np.ascontiguousarray(h, dtype=np.uint16), np.uint16)
+    r = _chk(np.ascontiguousarray(r), RESID_DTYPE[scheme])
+    w = np.empty(h.shape, np.float32)
+    lib().or_reconstruct_s(SCHEME[scheme], FMT[fmt], _ptr(h), _ptr(r), _ptr(w), h.size)
+    return w
+
+
+def sgd_step_s(scheme, vfmt, gfmt, value, resid, grad, buf, *, lr, momentum=0.0, dampening=0.0,
+               weight_decay=0.0, grad_scale=1.0, nesterov=False, first_step=False, seed=0, stream=0):
+    _chk(value, np.uint16); _chk(resid, RESID_DTYPE[scheme]); _grad_fmt(grad, gfmt)
+    hp = SgdHP(lr, momentum, dampening, weight_decay, grad_scale, int(nesterov), int(first_step))
+    lib().or_sgd_step_s(SCHEME[scheme], FMT[vfmt], FMT[gfmt], _ptr(value), _ptr(resid), _ptr(grad), _ptr(buf),
+                        value.size, C.byref(hp), seed, stream)
+
+
+def adam_step_s(scheme, vfmt, gfmt, value, resid, grad, m, v, *, lr, beta1=0.9, beta2=0.999, eps=1e-8,
+                weight_decay=0.0, adamw=True, grad_scale=1.0, step=1, clip_coef=None, seed=0, stream=0):
+    _chk(value, np.uint16); _chk(resid, RESID_DTYPE[scheme]); _grad_fmt(grad, gfmt)
+    _chk(m, np.float32); _chk(v, np.float32)
+    hp = AdamHP(lr, beta1, beta2, eps, weight_decay, grad_scale, int(adamw), int(step))
+    cc = -1.0 if clip_coef is None else float(clip_coef)
+    lib().or_adam_step_s(SCHEME[scheme], FMT[vfmt], FMT[gfmt], _ptr(value), _ptr(resid), _ptr(grad), _ptr(m),
+                         _ptr(v), value.size, C.byref(hp), cc, seed, stream)

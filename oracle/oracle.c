@@ -323,6 +323,181 @@ void or_adam_step_master(int gfmt, float* w, const void* grad, float* m, float* 
 }
 
 /* ------------------------------------------------------------------------------------- */
+/* Paper variants of the storage scheme                               */
+/*   OR_S_RNE  round-to-nearest-even value + int16 signed difference (R1-R5, the default)  */
+/*   OR_S_RTZ  round-to-zero value + uint16 extra bits: "saving only the first part   */
+/*             of the 32bit significand is equivalent to applying a round-to-zero          */
+/*             operation on the full precision value"                                      */
+/*   OR_S_SR   stochastic rounding + the signed difference, whose sign is the paper's one  */
+/*             extra "un-round" bit ("we store one additional extra-bit to keep in     */
+/*             memory whether or not the value was changed when rounded-up"); fp16 only,    */
+/*             as in the paper's "fp16 + 13 stochastic" run -- 13 + 1 bits fit 16   */
+/*   OR_S_X8   RNE value + only 8 extra bits (int8): "We also explore the performance  */
+/*             when keeping only part of those bits"; "fp16 + 8"; reading R14         */
+/* ------------------------------------------------------------------------------------- */
+#define OR_S_RNE 0
+#define OR_S_RTZ 1
+#define OR_S_SR 2
+#define OR_S_X8 3
+
+/* IEEE round-toward-zero of a binary32 pattern to fp16 / bf16 by integer truncation of the
+ * dropped significand bits (no rounding increment).  Finite values never overflow to Inf: they
+ * saturate at the largest finite 16-bit value (IEEE RTZ).  NaN -> 0x7FFF (R4). */
+uint16_t or_rtz16(int fmt, uint32_t u) {
+    uint32_t sign = u & 0x80000000u;
+    uint32_t a = u & 0x7FFFFFFFu;
+    if (a > 0x7F800000u) return 0x7FFF;
+    if (fmt == OR_BF16) return (uint16_t)((sign >> 16) | (a >> 16));
+    if (a == 0x7F800000u) return (uint16_t)((sign >> 16) | 0x7C00u);
+    {
+        uint32_t e = a >> 23, mant = a & 0x7FFFFFu, sig;
+        int ee, s;
+        if (e == 0) { sig = mant; ee = -126; } else { sig = mant | 0x800000u; ee = (int)e - 127; }
+        if (ee > 15) return (uint16_t)((sign >> 16) | 0x7BFFu);                 /* >= 2^16 */
+        if (ee >= -14) return (uint16_t)((sign >> 16) | (((uint32_t)(ee + 15) << 10) + ((sig >> 13) - 0x400u)));
+        s = -1 - ee;                                                           /* subnormal */
+        if (s >= 24) return (uint16_t)(sign >> 16);
+        return (uint16_t)((sign >> 16) | (sig >> s));
+    }
+}
+
+/* The counter-based generator both sides implement (the draws of stochastic rounding are an
+ * input of the method, not its arithmetic): splitmix64's finaliser over a key mixed from
+ * (seed, stream, index) with two odd 64-bit constants. */
+uint64_t or_mix64(uint64_t seed, uint64_t stream, uint64_t index) {
+    uint64_t x = seed ^ (stream * 0x9E3779B97F4A7C15ull) ^ (index * 0xD1B54A32D192ED03ull);
+    x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27; x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return x;
+}
+
+/* Stochastic rounding to fp16 with a 32-bit draw `rnd`: t = RTZ(x); with D = bits(x) -
+ * bits(widen(t)) and U = bits(widen(t + 1 ulp)) - bits(widen(t)) (binary32 patterns), round
+ * up in magnitude iff rnd < floor(D * 2^32 / U), i.e. with probability D/U.  |x| >= 2^16
+ * -> Inf (as RNE overflow).  NaN -> 0x7FFF, Inf -> Inf. */
+uint16_t or_sr16(uint32_t u, uint32_t rnd) {
+    uint32_t a = u & 0x7FFFFFFFu;
+    uint16_t t, up;
+    uint64_t d, uu;
+    if (a > 0x7F800000u) return 0x7FFF;
+    if (a >= 0x47800000u) return (uint16_t)(((u & 0x80000000u) >> 16) | 0x7C00u);   /* >= 2^16 or Inf */
+    t = or_rtz16(OR_FP16, u);
+    up = (uint16_t)(t + 1u);                           /* next magnitude (may become Inf) */
+    d = (uint64_t)(a - (or_widen16(OR_FP16, t) & 0x7FFFFFFFu));
+    uu = (uint64_t)((or_widen16(OR_FP16, up) & 0x7FFFFFFFu) - (or_widen16(OR_FP16, t) & 0x7FFFFFFFu));
+    if ((uint64_t)rnd < ((d << 32) / uu)) return up;
+    return t;
+}
+
+static int64_t floordiv_pow2(int64_t x, int sh) {
+    int64_t q = (int64_t)1 << sh;
+    return x >= 0 ? x / q : -((-x + q - 1) / q);
+}
+
+/* Split under a scheme.  resid receives the stored residual as an integer: int16 range (RNE,
+ * SR), 0..65535 (RTZ, stored as the uint16 bit pattern), int8 range (X8). */
+static void split_s(int scheme, int fmt, uint32_t u, uint32_t rnd, uint16_t* h_out, int32_t* r_out) {
+    uint16_t h;
+    uint32_t wu;
+    int64_t d;
+    if ((u & 0x7FFFFFFFu) > 0x7F800000u) { *h_out = 0x7FFF; *r_out = 0; return; }   /* R4 */
+    if (scheme == OR_S_RTZ) h = or_rtz16(fmt, u);
+    else if (scheme == OR_S_SR) h = or_sr16(u, rnd);
+    else h = or_rne16(fmt, u);
+    wu = or_widen16(fmt, h);
+    *h_out = h;
+    if ((wu & 0x7FFFFFFFu) >= 0x7F800000u) { *r_out = 0; return; }                    /* Inf */
+    d = (int64_t)u - (int64_t)wu;          /* same sign: none of the roundings changes it */
+    if (scheme == OR_S_RTZ) {              /* |x| >= |t|: d >= 0 */
+        *r_out = (int32_t)(d > 65535 ? 65535 : d);
+    } else if (scheme == OR_S_X8) {        /* keep the top 8 of the extra bits, nearest (R14) */
+        int sh = fmt == OR_BF16 ? 8 : 5;
+        int64_t q = floordiv_pow2(d + ((int64_t)1 << (sh - 1)), sh);
+        *r_out = (int32_t)(q > 127 ? 127 : (q < -128 ? -128 : q));
+    } else {
+        *r_out = (int32_t)(d > 32767 ? 32767 : (d < -32768 ? -32768 : d));
+    }
+}
+
+static uint32_t reconstruct_s(int scheme, int fmt, uint16_t h, int32_t r) {
+    uint32_t wu = or_widen16(fmt, h);
+    int64_t add;
+    if ((wu & 0x7FFFFFFFu) > 0x7F800000u) return 0x7FFFFFFFu;
+    if ((wu & 0x7FFFFFFFu) == 0x7F800000u) return wu;
+    if (scheme == OR_S_X8) add = (int64_t)r * (fmt == OR_BF16 ? 256 : 32);
+    else add = r;
+    return (uint32_t)((int64_t)wu + add);
+}
+
+static int32_t load_resid(int scheme, const void* resid, int64_t i) {
+    if (scheme == OR_S_X8) return ((const int8_t*)resid)[i];
+    if (scheme == OR_S_RTZ) return ((const uint16_t*)resid)[i];
+    return ((const int16_t*)resid)[i];
+}
+
+static void store_resid(int scheme, void* resid, int64_t i, int32_t r) {
+    if (scheme == OR_S_X8) ((int8_t*)resid)[i] = (int8_t)r;
+    else if (scheme == OR_S_RTZ) ((uint16_t*)resid)[i] = (uint16_t)r;
+    else ((int16_t*)resid)[i] = (int16_t)r;
+}
+
+static uint32_t draw(int scheme, uint64_t seed, uint64_t stream, int64_t i) {
+    return scheme == OR_S_SR ? (uint32_t)(or_mix64(seed, stream, (uint64_t)i) >> 32) : 0u;
+}
+
+void or_split_s(int scheme, int fmt, const float* w, uint16_t* value, void* resid, int64_t n, uint64_t seed,
+                uint64_t stream) {
+    int64_t i;
+    for (i = 0; i < n; i++) {
+        uint16_t h; int32_t r;
+        split_s(scheme, fmt, f2u(w[i]), draw(scheme, seed, stream, i), &h, &r);
+        value[i] = h;
+        store_resid(scheme, resid, i, r);
+    }
+}
+
+void or_reconstruct_s(int scheme, int fmt, const uint16_t* value, const void* resid, float* w, int64_t n) {
+    int64_t i;
+    for (i = 0; i < n; i++) w[i] = u2f(reconstruct_s(scheme, fmt, value[i], load_resid(scheme, resid, i)));
+}
+
+/* The steps under a scheme: reconstruct -> the same fp32 update -> split (SR draws keyed by
+ * (seed, stream, element index)). */
+void or_sgd_step_s(int scheme, int vfmt, int gfmt, uint16_t* value, void* resid, const void* grad, float* buf,
+                   int64_t n, const or_sgd_hp* hp, uint64_t seed, uint64_t stream) {
+    int64_t i;
+    float gs = (float)hp->grad_scale;
+    for (i = 0; i < n; i++) {
+        float g = load_grad(gfmt, grad, i) * gs;
+        float w = u2f(reconstruct_s(scheme, vfmt, value[i], load_resid(scheme, resid, i)));
+        uint16_t h; int32_t r;
+        w = sgd_update(w, g, buf ? &buf[i] : 0, hp);
+        split_s(scheme, vfmt, f2u(w), draw(scheme, seed, stream, i), &h, &r);
+        value[i] = h;
+        store_resid(scheme, resid, i, r);
+    }
+}
+
+void or_adam_step_s(int scheme, int vfmt, int gfmt, uint16_t* value, void* resid, const void* grad, float* m,
+                    float* v, int64_t n, const or_adam_hp* hp, float clip_coef, uint64_t seed, uint64_t stream) {
+    int64_t i;
+    float gs = (float)hp->grad_scale;
+    adam_scalars c = adam_derive(hp);
+    for (i = 0; i < n; i++) {
+        float g = load_grad(gfmt, grad, i) * gs;
+        float w;
+        uint16_t h; int32_t r;
+        if (clip_coef >= 0.0f || clip_coef != clip_coef) g = g * clip_coef;
+        w = u2f(reconstruct_s(scheme, vfmt, value[i], load_resid(scheme, resid, i)));
+        w = adam_update(w, g, &m[i], &v[i], &c);
+        split_s(scheme, vfmt, f2u(w), draw(scheme, seed, stream, i), &h, &r);
+        value[i] = h;
+        store_resid(scheme, resid, i, r);
+    }
+}
+
+/* ------------------------------------------------------------------------------------- */
 /* Global-norm clipping ("Gradient Clipping"; reading R9: torch clip_grad_norm_     */
 /* formula, fp64 accumulation; only in multi-tensor / sharded modes)                */
 /* ------------------------------------------------------------------------------------- */
