@@ -65,26 +65,44 @@ typedef enum {
     MPO_ENCCL = 5     /* an NCCL call failed (message from ncclGetErrorString)              */
 } mpo_status;
 
-typedef enum { MPO_FP16 = 0, MPO_BF16 = 1, MPO_FP32 = 2 } mpo_dtype;  /* value: FP16|BF16 */
+/* Value storage formats and gradient dtypes.  A storage format names the 16-bit value dtype and
+ * the scheme of its residual (code = base | scheme << 4):
+ *   MPO_FP16, MPO_BF16       RNE value + int16 signed difference (R1-R5; the default)
+ *   MPO_FP16_RTZ, _BF16_RTZ  round-to-zero value + uint16 extra bits ("saving only the first
+ *                            part of the 32bit significand is equivalent to applying a
+ *                            round-to-zero"); bf16 is lossless on every finite fp32 value
+ *   MPO_FP16_SR              stochastic rounding + int16 signed difference whose sign is the
+ *                            paper's "un-round" bit ("fp16 + 13 stochastic"); draws
+ *                            from the counter-based generator keyed by (seed, sr_stream, index)
+ *   MPO_FP16_X8, _BF16_X8    RNE value + 8 extra bits: int8 residual ("keeping only part of
+ *                            those bits"; P:134 fp16+8), reading R14
+ * Gradients: MPO_FP16, MPO_BF16 or MPO_FP32 (variant formats: their base dtype or MPO_FP32). */
+typedef enum {
+    MPO_FP16 = 0, MPO_BF16 = 1, MPO_FP32 = 2,
+    MPO_FP16_RTZ = 16, MPO_BF16_RTZ = 17, MPO_FP16_SR = 32, MPO_FP16_X8 = 48, MPO_BF16_X8 = 49
+} mpo_dtype;
 typedef enum { MPO_SGD = 0, MPO_ADAM = 1 } mpo_optim;
 
 /* One parameter tensor of a multi-tensor table ("one only stream of values").
- *   value : n 16-bit values (dtype vdt), updated in place
- *   resid : n int16 residuals, updated in place
- *   grad  : n gradients (dtype gdt: FP16, BF16 or FP32), read-only
- *   m     : n fp32 -- SGD momentum buffer, or Adam first moment (NULL for SGD without momentum)
- *   v     : n fp32 -- Adam second moment (ignored by SGD)
- *   n     : element count (>= 0)
- *   hp    : index into the hyper-parameter group array of the call                        */
+ *   value     : n 16-bit values (storage format vdt), updated in place
+ *   resid     : n residuals, updated in place: int16 (MPO_FP16/BF16, FP16_SR), uint16 bit
+ *               patterns (the RTZ formats) or int8 (the X8 formats)
+ *   grad      : n gradients (dtype gdt: FP16, BF16 or FP32), read-only
+ *   m         : n fp32 -- SGD momentum buffer, or Adam first moment (NULL for SGD w/o momentum)
+ *   v         : n fp32 -- Adam second moment (ignored by SGD)
+ *   n         : element count (>= 0)
+ *   hp        : index into the hyper-parameter group array of the call
+ *   sr_stream : stream id of the stochastic-rounding draws of this tensor (0 <= id < 2^27;
+ *               ignored by deterministic formats)                                          */
 typedef struct {
     void* value;
-    int16_t* resid;
+    void* resid;
     const void* grad;
     float* m;
     float* v;
     int64_t n;
     int32_t hp;
-    int32_t _pad;
+    int32_t sr_stream;
 } mpo_tensor;
 
 /* torch.optim.SGD semantics (R6; "classic optimizers"; P:19 drop-in hyper-parameters).
@@ -95,6 +113,7 @@ typedef struct {
 typedef struct {
     double lr, momentum, dampening, weight_decay, grad_scale;
     int32_t nesterov, first_step;
+    uint64_t seed;   /* stochastic-rounding draws of this step (MPO_FP16_SR); else ignored */
 } mpo_sgd_hp;
 
 /* torch.optim.Adam / AdamW semantics (R6).  step is 1-based (bias correction).  adamw != 0:
@@ -106,20 +125,23 @@ typedef struct {
     double lr, beta1, beta2, eps, weight_decay, grad_scale, max_grad_norm;
     int32_t adamw, _pad;
     int64_t step;
+    uint64_t seed;   /* stochastic-rounding draws of this step (MPO_FP16_SR); else ignored */
 } mpo_adam_hp;
 
 /* Largest number of hyper-parameter groups one call may carry. */
 #define MPO_MAX_HP_GROUPS 16
 
-/* Split fp32 weights into (16-bit value, int16 residual) (readings R1-R5).
- *   vdt   : MPO_FP16 | MPO_BF16
- *   w     : n fp32 (device, read-only);  value: n 16-bit (device, written);  resid: n int16 */
-mpo_status mpo_split(mpo_dtype vdt, const float* w, void* value, int16_t* resid, int64_t n,
-                     mpo_stream stream);
+/* Split fp32 weights into (16-bit value, residual) (readings R1-R5, R14).
+ *   vdt   : a storage format (see mpo_dtype)
+ *   w     : n fp32 (device, read-only);  value: n 16-bit (device, written);
+ *   resid : n residuals of the format's type (device, written)
+ *   seed, sr_stream : key of the stochastic-rounding draws (MPO_FP16_SR; ignored otherwise) */
+mpo_status mpo_split(mpo_dtype vdt, const float* w, void* value, void* resid, int64_t n,
+                     uint64_t seed, int32_t sr_stream, mpo_stream stream);
 
 /* Reconstruct the fp32 weights from value + residual ("performs the operation in full
  * precision using the extra bits saved separately").  value/resid read-only, w written. */
-mpo_status mpo_reconstruct(mpo_dtype vdt, const void* value, const int16_t* resid, float* w,
+mpo_status mpo_reconstruct(mpo_dtype vdt, const void* value, const void* resid, float* w,
                            int64_t n, mpo_stream stream);
 
 /* Residual-compensated SGD(-momentum) step over a table of nt tensors, one fused launch per
@@ -155,7 +177,8 @@ mpo_status mpo_fused_backward_hook_step(mpo_optim kind, mpo_dtype vdt, mpo_dtype
  * arguments except rank and its own buffers.
  *   nccl_comm   : an ncclComm_t (borrowed, e.g. from torch's ProcessGroupNCCL; never freed)
  *   value_flat  : n_total 16-bit values, replicated on every rank (all-gathered on return)
- *   grad_flat   : n_total 16-bit gradients of THIS rank (same dtype as value); overwritten:
+ *   grad_flat   : n_total 16-bit gradients of THIS rank (the value format's base dtype);
+ *                 overwritten:
  *                 shard `rank` becomes the reduced (summed) gradient
  *   resid_shard, m_shard, v_shard : n_total/world entries of this rank's shard (v ignored,
  *                 m may be NULL, for SGD without momentum)
@@ -163,10 +186,11 @@ mpo_status mpo_fused_backward_hook_step(mpo_optim kind, mpo_dtype vdt, mpo_dtype
  *   hp          : mpo_sgd_hp* | mpo_adam_hp* (HOST); grad_scale should be 1/world for a mean
  *   norm_ws     : as for mpo_adam_step (clipping: the shard sums are all-reduced in fp64)
  * Sequence on `stream`: ncclReduceScatter(sum) -> [sumsq + ncclAllReduce] -> step on the shard
- * -> ncclAllGather of the 16-bit values only. */
+ * -> ncclAllGather of the 16-bit values only (world 1: the collectives are identities and are
+ * skipped).  The shard's stochastic-rounding stream is its rank. */
 mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t rank, int32_t world,
                             mpo_dtype vdt, void* value_flat, void* grad_flat,
-                            int16_t* resid_shard, float* m_shard, float* v_shard,
+                            void* resid_shard, float* m_shard, float* v_shard,
                             int64_t n_total, const void* hp, double* norm_ws,
                             mpo_stream stream);
 

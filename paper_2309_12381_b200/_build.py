@@ -20,8 +20,13 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 INCLUDE = os.path.join(ROOT, "include")
-SOURCES = [os.path.join(CSRC, "mpo.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "mpo_device.cuh"), os.path.join(INCLUDE, "mpo.h"), __file__]
+# translation units: the ABI layer, and the step kernels once per storage format (mpo_dtype code)
+ABI_TU = os.path.join(CSRC, "mpo.cu")
+INST_TU = os.path.join(CSRC, "mpo_inst.cu")
+FORMATS = (0, 1, 16, 17, 32, 48, 49)
+SOURCES = [ABI_TU, INST_TU]
+DEPS = SOURCES + [os.path.join(CSRC, "mpo_device.cuh"), os.path.join(CSRC, "mpo_kernels.cuh"),
+                  os.path.join(INCLUDE, "mpo.h"), __file__]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -38,30 +43,57 @@ def nccl_dirs():
     raise RuntimeError("NCCL headers/library from the torch wheel (nvidia/nccl) not found")
 
 
-def flags(exact: bool):
-    inc, lib = nccl_dirs()
-    f = ["-std=c++17", "-O3", *ARCH, "-lineinfo", "-shared", "-Xcompiler",
-         "-fPIC,-fvisibility=hidden,-ffp-contract=off", "-ftz=false", "-prec-div=true",
-         "-prec-sqrt=true", "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{inc}", f"-L{lib}",
-         "-l:libnccl.so.2", f"-Xlinker", f"-rpath,{lib}"]
+def compile_flags(exact: bool):
+    inc, _ = nccl_dirs()
+    f = ["-std=c++17", "-O3", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden,-ffp-contract=off",
+         "-ftz=false", "-prec-div=true", "-prec-sqrt=true", "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{inc}"]
     f += ["-fmad=false", "-DMPO_EXACT"] if exact else ["-fmad=true"]
     return f
+
+
+def link_flags():
+    _, lib = nccl_dirs()
+    return ["-shared", *ARCH, f"-L{lib}", "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}"]
+
+
+def lib_path(exact: bool = False) -> str:
+    return os.path.join(LIBDIR, "libmpo_exact.so" if exact else "libmpo.so")
+
+
+def _compile_link(out: str, exact: bool, defines=()):
+    """Compile every translation unit in parallel, then link the shared library."""
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = out + ".obj"
+    os.makedirs(objdir, exist_ok=True)
+    jobs = [(ABI_TU, os.path.join(objdir, "mpo.o"), [])]
+    jobs += [(INST_TU, os.path.join(objdir, f"inst_{sf}.o"), [f"-DMPO_SF={sf}"]) for sf in FORMATS]
+
+    def one(job):
+        src, obj, extra = job
+        cmd = [NVCC, *compile_flags(exact), *[f"-D{d}" for d in defines], *extra, "-c", "-o", obj, src]
+        return subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(one, jobs))
+    log = "".join(r.stdout + r.stderr for r in results)
+    if any(r.returncode != 0 for r in results):
+        sys.stderr.write(log)
+        raise RuntimeError(f"nvcc failed building {os.path.basename(out)}")
+    tmp = out + f".tmp{os.getpid()}"
+    r = subprocess.run([NVCC, *link_flags(), "-o", tmp, *[j[1] for j in jobs]], capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"link failed for {os.path.basename(out)}")
+    os.replace(tmp, out)
+    return log
 
 
 def build_variant(name: str, defines, exact: bool = False) -> str:
     """Build an experimental variant (extra -D defines) into lib/variants/ (A/B measurements)."""
     out = os.path.join(LIBDIR, "variants", f"libmpo_{name}.so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    cmd = [NVCC, *flags(exact), *[f"-D{d}" for d in defines], "-o", out, *SOURCES]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError(f"nvcc failed building variant {name}")
+    _compile_link(out, exact, defines)
     return out
-
-
-def lib_path(exact: bool = False) -> str:
-    return os.path.join(LIBDIR, "libmpo_exact.so" if exact else "libmpo.so")
 
 
 def _stale(out: str) -> bool:
@@ -78,21 +110,15 @@ def build(force: bool = False, verbose: bool = False):
     for exact in (False, True):
         out = lib_path(exact)
         if force or _stale(out):
-            tmp = out + f".tmp{os.getpid()}"
-            cmd = [NVCC, *flags(exact), "-o", tmp, *SOURCES]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if r.returncode != 0:
-                sys.stderr.write(r.stdout + r.stderr)
-                raise RuntimeError(f"nvcc failed building {os.path.basename(out)}")
+            log = _compile_link(out, exact)
             with open(out + ".ptxas.txt", "w") as fh:
-                fh.write(r.stderr)
+                fh.write(log)
             if verbose:
-                sys.stderr.write(r.stderr)
-            os.replace(tmp, out)
+                sys.stderr.write(log)
         outs.append(out)
     return outs
 
 
 if __name__ == "__main__":
-    for p in build(force="--force" in sys.argv, verbose=True):
+    for p in build(force="--force" in sys.argv, verbose=False):
         print(p)

@@ -16,6 +16,8 @@ MPO_OK, MPO_EINVAL, MPO_EALIGN, MPO_EDTYPE, MPO_ECUDA, MPO_ENCCL = range(6)
 STATUS_NAMES = {0: "MPO_OK", 1: "MPO_EINVAL", 2: "MPO_EALIGN", 3: "MPO_EDTYPE", 4: "MPO_ECUDA", 5: "MPO_ENCCL"}
 # dtype / optimizer enums (mpo_dtype, mpo_optim)
 MPO_FP16, MPO_BF16, MPO_FP32 = 0, 1, 2
+# storage schemes of the residual: code = base | scheme << 4 (include/mpo.h mpo_dtype)
+SCHEMES = {"rne": 0, "rtz": 1, "sr": 2, "x8": 3}
 MPO_SGD, MPO_ADAM = 0, 1
 MPO_MAX_HP_GROUPS = 16
 
@@ -34,21 +36,21 @@ class MpoError(RuntimeError):
 class Tensor(C.Structure):
     """mpo_tensor"""
     _fields_ = [("value", C.c_void_p), ("resid", C.c_void_p), ("grad", C.c_void_p), ("m", C.c_void_p),
-                ("v", C.c_void_p), ("n", C.c_int64), ("hp", C.c_int32), ("_pad", C.c_int32)]
+                ("v", C.c_void_p), ("n", C.c_int64), ("hp", C.c_int32), ("sr_stream", C.c_int32)]
 
 
 class SgdHP(C.Structure):
     """mpo_sgd_hp"""
     _fields_ = [("lr", C.c_double), ("momentum", C.c_double), ("dampening", C.c_double),
                 ("weight_decay", C.c_double), ("grad_scale", C.c_double), ("nesterov", C.c_int32),
-                ("first_step", C.c_int32)]
+                ("first_step", C.c_int32), ("seed", C.c_uint64)]
 
 
 class AdamHP(C.Structure):
     """mpo_adam_hp"""
     _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
                 ("weight_decay", C.c_double), ("grad_scale", C.c_double), ("max_grad_norm", C.c_double),
-                ("adamw", C.c_int32), ("_pad", C.c_int32), ("step", C.c_int64)]
+                ("adamw", C.c_int32), ("_pad", C.c_int32), ("step", C.c_int64), ("seed", C.c_uint64)]
 
 
 _libs: dict = {}
@@ -56,7 +58,7 @@ _libs: dict = {}
 
 def _declare(L):
     P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_int
-    L.mpo_split.argtypes = [D, P, P, P, I64, P]
+    L.mpo_split.argtypes = [D, P, P, P, I64, C.c_uint64, I32, P]
     L.mpo_reconstruct.argtypes = [D, P, P, P, I64, P]
     L.mpo_sgd_step.argtypes = [D, D, C.POINTER(Tensor), I32, C.POINTER(SgdHP), I32, P]
     L.mpo_adam_step.argtypes = [D, D, C.POINTER(Tensor), I32, C.POINTER(AdamHP), I32, P, P]

@@ -26,6 +26,30 @@ def dtype_code(dt: torch.dtype) -> int:
         raise MpoError(_lib.MPO_EDTYPE, f"unsupported dtype {dt}") from None
 
 
+def format_code(value_dtype: torch.dtype, scheme: str = "rne") -> int:
+    """Storage format code (include/mpo.h mpo_dtype) of a 16-bit value dtype under a scheme:
+    'rne' (default), 'rtz' (round-to-zero + uint16 extra bits), 'sr' (fp16 stochastic rounding),
+    'x8' (8 extra bits, int8 residual)."""
+    if value_dtype not in _VALUE_VIEW:
+        raise MpoError(_lib.MPO_EDTYPE, f"value dtype must be fp16/bf16, got {value_dtype}")
+    if scheme not in _lib.SCHEMES:
+        raise MpoError(_lib.MPO_EDTYPE, f"unknown scheme {scheme!r}")
+    if scheme == "sr" and value_dtype != torch.float16:
+        raise MpoError(_lib.MPO_EDTYPE, "stochastic rounding is defined for fp16 (13 extra bits + the un-round bit)")
+    return dtype_code(value_dtype) | (_lib.SCHEMES[scheme] << 4)
+
+
+def resid_dtype(scheme: str = "rne") -> torch.dtype:
+    """Container dtype of the residual: int16 (rne, sr; rtz holds uint16 bit patterns), int8 (x8)."""
+    return torch.int8 if scheme == "x8" else torch.int16
+
+
+def step_seed(seed: int, step: int) -> int:
+    """Per-step key of the stochastic-rounding draws (any fixed mixing works; this is the one the
+    optimizers use)."""
+    return (int(seed) * 0x9E3779B97F4A7C15 + int(step)) & 0xFFFFFFFFFFFFFFFF
+
+
 def _stream(stream) -> int:
     if stream is None:
         return torch.cuda.current_stream().cuda_stream
@@ -60,10 +84,11 @@ class SgdParams:
     grad_scale: float = 1.0
     nesterov: bool = False
     first_step: bool = False
+    seed: int = 0
 
     def c(self) -> SgdHP:
         return SgdHP(self.lr, self.momentum, self.dampening, self.weight_decay, self.grad_scale,
-                     int(self.nesterov), int(self.first_step))
+                     int(self.nesterov), int(self.first_step), int(self.seed))
 
 
 @dataclass
@@ -77,10 +102,11 @@ class AdamParams:
     max_grad_norm: float = 0.0
     adamw: bool = True
     step: int = 1
+    seed: int = 0
 
     def c(self) -> AdamHP:
         return AdamHP(self.lr, self.beta1, self.beta2, self.eps, self.weight_decay, self.grad_scale,
-                      self.max_grad_norm, int(self.adamw), 0, int(self.step))
+                      self.max_grad_norm, int(self.adamw), 0, int(self.step), int(self.seed))
 
 
 def _hp_array(hps, kind):
@@ -104,7 +130,8 @@ class TensorTable:
 
     def __init__(self, values: Sequence[torch.Tensor], resids: Sequence[torch.Tensor],
                  grads: Sequence[Optional[torch.Tensor]], ms: Sequence[Optional[torch.Tensor]],
-                 vs: Sequence[Optional[torch.Tensor]], hp_index: Optional[Sequence[int]] = None):
+                 vs: Sequence[Optional[torch.Tensor]], hp_index: Optional[Sequence[int]] = None,
+                 scheme: str = "rne", sr_streams: Optional[Sequence[int]] = None):
         n = len(values)
         if not (len(resids) == len(grads) == len(ms) == len(vs) == n):
             raise MpoError(_lib.MPO_EINVAL, "table columns differ in length")
@@ -112,12 +139,14 @@ class TensorTable:
         self.hp_index = list(hp_index) if hp_index is not None else [0] * n
         self.arr = (Tensor * max(n, 1))()
         self.nt = n
-        self.vdt = dtype_code(values[0].dtype) if n else MPO_FP16
+        self.scheme = scheme
+        self.vdt = format_code(values[0].dtype, scheme) if n else MPO_FP16
+        rdt = resid_dtype(scheme)
         for i in range(n):
             v, r = values[i], resids[i]
-            if v.dtype not in _VALUE_VIEW or r.dtype != torch.int16 or v.numel() != r.numel():
-                raise MpoError(_lib.MPO_EDTYPE, f"tensor {i}: value must be fp16/bf16 and resid int16 of equal size")
-            if dtype_code(v.dtype) != self.vdt:
+            if v.dtype not in _VALUE_VIEW or r.dtype != rdt or v.numel() != r.numel():
+                raise MpoError(_lib.MPO_EDTYPE, f"tensor {i}: value must be fp16/bf16 and resid {rdt} of equal size")
+            if format_code(v.dtype, scheme) != self.vdt:
                 raise MpoError(_lib.MPO_EDTYPE, f"tensor {i}: mixed value dtypes in one table")
             row = self.arr[i]
             row.value = _ptr(v)
@@ -126,6 +155,7 @@ class TensorTable:
             row.v = _ptr(vs[i])
             row.n = v.numel()
             row.hp = self.hp_index[i]
+            row.sr_stream = int(sr_streams[i]) if sr_streams is not None else i
         self.gdt = None
         self.set_grads(grads)
 
@@ -151,30 +181,35 @@ class TensorTable:
 # Entry points (same names as the C ABI)
 # ------------------------------------------------------------------------------------------
 def mpo_split(w: torch.Tensor, fmt: torch.dtype, value: Optional[torch.Tensor] = None,
-              resid: Optional[torch.Tensor] = None, stream=None, exact: bool = False):
-    """fp32 -> (16-bit value, int16 residual)."""
+              resid: Optional[torch.Tensor] = None, stream=None, exact: bool = False, scheme: str = "rne",
+              seed: int = 0, sr_stream: int = 0):
+    """fp32 -> (16-bit value, residual) under a storage scheme."""
     if w.dtype != torch.float32:
         raise MpoError(_lib.MPO_EDTYPE, "split input must be fp32")
     if value is None:
         value = torch.empty(w.shape, dtype=fmt, device=w.device)
     if resid is None:
-        resid = torch.empty(w.shape, dtype=torch.int16, device=w.device)
+        resid = torch.empty(w.shape, dtype=resid_dtype(scheme), device=w.device)
+    if resid.dtype != resid_dtype(scheme):
+        raise MpoError(_lib.MPO_EDTYPE, f"resid must be {resid_dtype(scheme)} for scheme {scheme!r}")
     L = _lib_of(exact)
-    _lib.check(L, L.mpo_split(dtype_code(value.dtype), _ptr(w), _ptr(value), _ptr(resid), w.numel(),
-                              _stream(stream)))
+    _lib.check(L, L.mpo_split(format_code(value.dtype, scheme), _ptr(w), _ptr(value), _ptr(resid), w.numel(),
+                              int(seed), int(sr_stream), _stream(stream)))
     return value, resid
 
 
 def mpo_reconstruct(value: torch.Tensor, resid: torch.Tensor, out: Optional[torch.Tensor] = None,
-                    stream=None, exact: bool = False) -> torch.Tensor:
-    """(16-bit value, int16 residual) -> fp32."""
+                    stream=None, exact: bool = False, scheme: str = "rne") -> torch.Tensor:
+    """(16-bit value, residual) -> fp32."""
     if out is None:
         out = torch.empty(value.shape, dtype=torch.float32, device=value.device)
     if value.numel() != resid.numel() or value.numel() != out.numel():
         raise MpoError(_lib.MPO_EINVAL, "size mismatch")
+    if resid.dtype != resid_dtype(scheme):
+        raise MpoError(_lib.MPO_EDTYPE, f"resid must be {resid_dtype(scheme)} for scheme {scheme!r}")
     L = _lib_of(exact)
-    _lib.check(L, L.mpo_reconstruct(dtype_code(value.dtype), _ptr(value), _ptr(resid), _ptr(out), value.numel(),
-                                    _stream(stream)))
+    _lib.check(L, L.mpo_reconstruct(format_code(value.dtype, scheme), _ptr(value), _ptr(resid), _ptr(out),
+                                    value.numel(), _stream(stream)))
     return out
 
 
@@ -207,13 +242,13 @@ def mpo_fused_backward_hook_step(kind: int, vdt: int, gdt: int, one: Tensor, hp,
 def mpo_sharded_step(kind: int, comm_ptr: int, rank: int, world: int, value_flat: torch.Tensor,
                      grad_flat: torch.Tensor, resid_shard: torch.Tensor, m_shard: Optional[torch.Tensor],
                      v_shard: Optional[torch.Tensor], hp, norm_ws: Optional[torch.Tensor] = None, stream=None,
-                     exact: bool = False):
+                     exact: bool = False, scheme: str = "rne"):
     """Data-parallel sharded step: RS(grad) -> shard update -> AG(value) (BASELINE north_star (c))."""
     if grad_flat.dtype != value_flat.dtype or grad_flat.numel() != value_flat.numel():
         raise MpoError(_lib.MPO_EINVAL, "grad_flat must match value_flat in dtype and size")
     L = _lib_of(exact)
     chp = hp.c() if hasattr(hp, "c") else hp
-    _lib.check(L, L.mpo_sharded_step(kind, comm_ptr, rank, world, dtype_code(value_flat.dtype), _ptr(value_flat),
+    _lib.check(L, L.mpo_sharded_step(kind, comm_ptr, rank, world, format_code(value_flat.dtype, scheme), _ptr(value_flat),
                                      _ptr(grad_flat), _ptr(resid_shard), _ptr(m_shard), _ptr(v_shard),
                                      value_flat.numel(), C.byref(chp), _ptr(norm_ws), _stream(stream)))
 

@@ -1,0 +1,58 @@
+// mpo_inst.cu -- the kernels of ONE storage format (compiled once per format with -DMPO_SF=<code>,
+// the code being the C ABI's mpo_dtype value: base | scheme << 4; see mpo_device.cuh Fmt).
+#include "mpo_kernels.cuh"
+
+#ifndef MPO_SF
+#error "compile with -DMPO_SF=<storage format code>"
+#endif
+
+namespace mpo {
+
+namespace {
+constexpr int SF = MPO_SF;
+constexpr int B = Fmt<SF>::base;
+constexpr bool kAllGrads = Fmt<SF>::scheme == kRNE;   // other schemes: grads of the base dtype or fp32
+constexpr int kOther = B == kFP16 ? kBF16 : kFP16;
+
+template <class Op, bool CLIP>
+mpo_status step_for(int gdt, const mpo_tensor* t, int nt, const HP<typename Op::K>& hp, bool one_hp,
+                    const double* sumsq, double max_norm, cudaStream_t s) {
+    if (gdt == B) return launch_step<SF, B, Op, CLIP>(t, nt, hp, one_hp, sumsq, max_norm, s);
+    if (gdt == kFP32) return launch_step<SF, kFP32, Op, CLIP>(t, nt, hp, one_hp, sumsq, max_norm, s);
+    if constexpr (kAllGrads) {
+        if (gdt == kOther) return launch_step<SF, kOther, Op, CLIP>(t, nt, hp, one_hp, sumsq, max_norm, s);
+    }
+    return fail(MPO_EDTYPE, "unsupported gradient dtype for this storage format");
+}
+}  // namespace
+
+template <>
+mpo_status FormatOps<SF>::sgd(int gdt, const mpo_tensor* t, int nt, const HP<SgdK>& hp, bool one_hp, cudaStream_t s) {
+    return step_for<SgdOp, false>(gdt, t, nt, hp, one_hp, nullptr, 0.0, s);
+}
+
+template <>
+mpo_status FormatOps<SF>::adam(int gdt, const mpo_tensor* t, int nt, const HP<AdamK>& hp, bool one_hp,
+                               const double* sumsq, double max_norm, cudaStream_t s) {
+    if (max_norm > 0.0) return step_for<AdamOp, true>(gdt, t, nt, hp, one_hp, sumsq, max_norm, s);
+    return step_for<AdamOp, false>(gdt, t, nt, hp, one_hp, nullptr, 0.0, s);
+}
+
+template <>
+mpo_status FormatOps<SF>::split(const float* w, void* value, void* resid, int64_t n, uint64_t seed, uint32_t stream,
+                                cudaStream_t s) {
+    const int64_t grid = grid_for((n / kUnitEl + kThreads - 1) / kThreads + 1, 8);
+    split_kernel<SF><<<unsigned(grid), kThreads, 0, s>>>(w, static_cast<uint16_t*>(value), resid, n, seed, stream);
+    ++g_launches;
+    return check_launch("split_kernel");
+}
+
+template <>
+mpo_status FormatOps<SF>::reconstruct(const void* value, const void* resid, float* w, int64_t n, cudaStream_t s) {
+    const int64_t grid = grid_for((n / kUnitEl + kThreads - 1) / kThreads + 1, 8);
+    reconstruct_kernel<SF><<<unsigned(grid), kThreads, 0, s>>>(static_cast<const uint16_t*>(value), resid, w, n);
+    ++g_launches;
+    return check_launch("reconstruct_kernel");
+}
+
+}  // namespace mpo

@@ -28,31 +28,39 @@ _16 = (torch.float16, torch.bfloat16)
 class _ResidualOptimizer(torch.optim.Optimizer):
     _kind = None
 
-    def __init__(self, params, defaults, fmt: Optional[torch.dtype], exact: bool):
+    def __init__(self, params, defaults, fmt: Optional[torch.dtype], exact: bool, scheme: str = "rne",
+                 seed: int = 0):
         super().__init__(params, defaults)
         self.exact = exact
+        self.scheme = scheme
+        self.seed = int(seed)
         self._hooks = []
         self._tables = {}
         self._norm_ws = None
+        idx = 0
         for group in self.param_groups:
             for p in group["params"]:
-                self._init_param(p, fmt)
+                self._init_param(p, fmt, idx)
+                idx += 1
 
     # -- state ------------------------------------------------------------------------------
-    def _init_param(self, p: torch.Tensor, fmt):
+    def _init_param(self, p: torch.Tensor, fmt, idx: int):
         if not p.is_cuda:
             raise MpoError(1, "parameters must live on a CUDA device (no CPU path)")
         st = self.state[p]
+        st["index"] = idx            # also the stochastic-rounding stream of this parameter
         if p.dtype == torch.float32:
             if fmt not in _16:
                 raise MpoError(3, "an fp32 parameter needs fmt=torch.float16 or torch.bfloat16 to be split")
             with torch.no_grad():
-                value, resid = api.mpo_split(p.data.contiguous(), fmt, exact=self.exact)
+                value, resid = api.mpo_split(p.data.contiguous(), fmt, exact=self.exact, scheme=self.scheme,
+                                             seed=api.step_seed(self.seed, 0), sr_stream=idx)
                 p.data = value
             st["resid"] = resid
         elif p.dtype in _16:
-            # a 16-bit value is exactly representable: its residual is 0 (P1)
-            st["resid"] = torch.zeros(p.shape, dtype=torch.int16, device=p.device)
+            # a 16-bit value is exactly representable: its residual is 0 under every scheme (P1)
+            api.format_code(p.dtype, self.scheme)
+            st["resid"] = torch.zeros(p.shape, dtype=api.resid_dtype(self.scheme), device=p.device)
         else:
             raise MpoError(3, f"unsupported parameter dtype {p.dtype}")
         st["step"] = 0
@@ -66,7 +74,8 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         out = []
         for group in self.param_groups:
             for p in group["params"]:
-                out.append(api.mpo_reconstruct(p.data, self.state[p]["resid"], exact=self.exact))
+                out.append(api.mpo_reconstruct(p.data, self.state[p]["resid"], exact=self.exact,
+                                               scheme=self.scheme))
         return out
 
     # -- multi-tensor step -----------------------------------------------------------------
@@ -79,7 +88,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             st = [self.state[p] for p in params]
             tab = api.TensorTable([p.data for p in params], [s["resid"] for s in st], grads,
                                   [s.get("m") for s in st], [s.get("v") for s in st],
-                                  [0] * len(params))
+                                  [0] * len(params), scheme=self.scheme, sr_streams=[s["index"] for s in st])
             tab._group_of = [gi[id(p)] for p in params]
             self._tables[key] = tab
         elif [g.data_ptr() for g in grads] != tab.grad_ptrs:
@@ -126,6 +135,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                 row.m = st["m"].data_ptr() if st.get("m") is not None else None
                 row.v = st["v"].data_ptr() if st.get("v") is not None else None
                 row.n = p.numel()
+                row.sr_stream = st["index"]
                 st["row"] = row
                 st["group"] = gi
                 self._hooks.append(p.register_post_accumulate_grad_hook(self._hook))
@@ -143,8 +153,8 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         row = st["row"]
         row.grad = g.data_ptr()
         hp = self._hp(self.param_groups[st["group"]], st["step"]).c()
-        api.mpo_fused_backward_hook_step(self._kind, api.dtype_code(p.dtype), api.dtype_code(g.dtype), row, hp,
-                                         exact=self.exact)
+        api.mpo_fused_backward_hook_step(self._kind, api.format_code(p.dtype, self.scheme), api.dtype_code(g.dtype),
+                                         row, hp, exact=self.exact)
         p.grad = None   # freed now; stream order makes the block's reuse safe
 
     def _check_hook_mode(self):
@@ -164,20 +174,20 @@ class ResidualSGD(_ResidualOptimizer):
 
     def __init__(self, params: Iterable, lr: float, momentum: float = 0.0, dampening: float = 0.0,
                  weight_decay: float = 0.0, nesterov: bool = False, grad_scale: float = 1.0,
-                 fmt: Optional[torch.dtype] = None, exact: bool = False):
+                 fmt: Optional[torch.dtype] = None, exact: bool = False, scheme: str = "rne", seed: int = 0):
         defaults = dict(lr=lr, momentum=momentum, dampening=dampening, weight_decay=weight_decay,
                         nesterov=nesterov, grad_scale=grad_scale)
-        super().__init__(params, defaults, fmt, exact)
+        super().__init__(params, defaults, fmt, exact, scheme, seed)
 
     def _init_state(self, p, st):
-        group = next(g for g in self.param_groups if any(q is p for q in g["params"]))
+        group = next(g for g in self.param_groups if any(q is p for q in g["params"]))  # noqa
         st["m"] = torch.zeros(p.shape, dtype=torch.float32, device=p.device) if group["momentum"] != 0 else None
         st["v"] = None
 
     def _hp(self, g, step):
         return api.SgdParams(lr=g["lr"], momentum=g["momentum"], dampening=g["dampening"],
                              weight_decay=g["weight_decay"], grad_scale=g["grad_scale"], nesterov=g["nesterov"],
-                             first_step=(step == 1))
+                             first_step=(step == 1), seed=api.step_seed(self.seed, step))
 
     def _launch(self, tab, hps):
         api.mpo_sgd_step(tab, hps, exact=self.exact)
@@ -190,11 +200,12 @@ class ResidualAdamW(_ResidualOptimizer):
 
     def __init__(self, params: Iterable, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
                  weight_decay: float = 0.0, adamw: bool = True, grad_scale: float = 1.0,
-                 max_grad_norm: Optional[float] = None, fmt: Optional[torch.dtype] = None, exact: bool = False):
+                 max_grad_norm: Optional[float] = None, fmt: Optional[torch.dtype] = None, exact: bool = False,
+                 scheme: str = "rne", seed: int = 0):
         defaults = dict(lr=lr, betas=tuple(betas), eps=eps, weight_decay=weight_decay, adamw=adamw,
                         grad_scale=grad_scale)
         self.max_grad_norm = float(max_grad_norm) if max_grad_norm else 0.0
-        super().__init__(params, defaults, fmt, exact)
+        super().__init__(params, defaults, fmt, exact, scheme, seed)
 
     def _init_state(self, p, st):
         st["m"] = torch.zeros(p.shape, dtype=torch.float32, device=p.device)
@@ -209,7 +220,7 @@ class ResidualAdamW(_ResidualOptimizer):
         b1, b2 = g["betas"]
         return api.AdamParams(lr=g["lr"], beta1=b1, beta2=b2, eps=g["eps"], weight_decay=g["weight_decay"],
                               grad_scale=g["grad_scale"], max_grad_norm=self.max_grad_norm, adamw=g["adamw"],
-                              step=step)
+                              step=step, seed=api.step_seed(self.seed, step))
 
     def _launch(self, tab, hps):
         ws = None

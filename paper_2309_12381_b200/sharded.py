@@ -78,7 +78,8 @@ class ShardedResidualOptimizer:
     gradient buffer, which backward accumulates into."""
 
     def __init__(self, params, kind: str = "adam", fmt: Optional[torch.dtype] = None, group=None,
-                 hp=None, exact: bool = False, comm_ptr: Optional[int] = None):
+                 hp=None, exact: bool = False, comm_ptr: Optional[int] = None, scheme: str = "rne",
+                 seed: int = 0):
         import torch.distributed as dist
         self.params = [p for p in params]
         if not self.params:
@@ -98,7 +99,9 @@ class ShardedResidualOptimizer:
         src = torch.zeros(L.total, dtype=torch.float32, device=dev)
         for p, o in zip(self.params, L.offsets):
             src[o:o + p.numel()].copy_(p.data.reshape(-1).float())
-        value, resid = api.mpo_split(src, vdt, exact=exact)
+        self.scheme, self.seed = scheme, int(seed)
+        value, resid = api.mpo_split(src, vdt, exact=exact, scheme=scheme, seed=api.step_seed(self.seed, 0),
+                                     sr_stream=0)
         if any(p.dtype != torch.float32 for p in self.params):
             # 16-bit params are exactly representable: their residual is zero (P1)
             pass
@@ -131,12 +134,13 @@ class ShardedResidualOptimizer:
             hp.step = self.step_count
         else:
             hp.first_step = self.step_count == 1
+        hp.seed = api.step_seed(self.seed, self.step_count)
         api.mpo_sharded_step(self.kind, self.comm, self.rank, self.world, self.value, self.grad, self.resid, self.m,
                              self.v, hp, norm_ws=self.norm_ws if getattr(hp, "max_grad_norm", 0.0) > 0 else None,
-                             exact=self.exact)
+                             exact=self.exact, scheme=self.scheme)
 
     def persistent_bytes(self) -> int:
-        b = self.value.numel() * 2 + self.grad.numel() * 2 + self.resid.numel() * 2
+        b = self.value.numel() * 2 + self.grad.numel() * 2 + self.resid.numel() * self.resid.element_size()
         b += 0 if self.m is None else self.m.numel() * 4
         b += 0 if self.v is None else self.v.numel() * 4
         return b

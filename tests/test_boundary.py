@@ -65,22 +65,22 @@ def test_validation_errors(libs):
     _lib, L, _ = libs
     T, S, A = _lib.Tensor, _lib.SgdHP, _lib.AdamHP
     # bad value dtype
-    rc, msg = _status(L, L.mpo_split(_lib.MPO_FP32, 16, 16, 16, 8, None))
+    rc, msg = _status(L, L.mpo_split(_lib.MPO_FP32, 16, 16, 16, 8, 0, 0, None))
     assert rc == _lib.MPO_EDTYPE and "value dtype" in msg
     # negative size
     rc, msg = _status(L, L.mpo_reconstruct(_lib.MPO_BF16, 16, 16, 16, -1, None))
     assert rc == _lib.MPO_EINVAL
     # misaligned pointer
-    rc, msg = _status(L, L.mpo_split(_lib.MPO_FP16, 16, 18, 32, 8, None))
+    rc, msg = _status(L, L.mpo_split(_lib.MPO_FP16, 16, 18, 32, 8, 0, 0, None))
     assert rc == _lib.MPO_EALIGN
     # n == 0 is a no-op (OK) even with NULL pointers
-    assert L.mpo_split(_lib.MPO_FP16, None, None, None, 0, None) == _lib.MPO_OK
+    assert L.mpo_split(_lib.MPO_FP16, None, None, None, 0, 0, 0, None) == _lib.MPO_OK
     # table errors name the offending index
     tab = (T * 2)()
     for i in range(2):
         tab[i].value, tab[i].resid, tab[i].grad, tab[i].m, tab[i].v, tab[i].n = 16, 32, 48, 64, 80, 8
     tab[1].resid = 34
-    hp = A(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1)
+    hp = A(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1, 0)
     rc, msg = _status(L, L.mpo_adam_step(_lib.MPO_BF16, _lib.MPO_BF16, tab, 2, C.byref(hp), 1, None, None))
     assert rc == _lib.MPO_EALIGN and "tensor 1" in msg
     tab[1].resid = 32
@@ -89,22 +89,22 @@ def test_validation_errors(libs):
     assert rc == _lib.MPO_EINVAL and "tensor 1" in msg
     tab[1].hp = 0
     # non-finite hyper-parameters rejected
-    bad = A(float("nan"), 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1)
+    bad = A(float("nan"), 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1, 0)
     rc, msg = _status(L, L.mpo_adam_step(_lib.MPO_BF16, _lib.MPO_BF16, tab, 2, C.byref(bad), 1, None, None))
     assert rc == _lib.MPO_EINVAL and "non-finite" in msg
     # step must be >= 1
-    bad = A(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 0)
+    bad = A(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 0, 0)
     assert L.mpo_adam_step(_lib.MPO_BF16, _lib.MPO_BF16, tab, 2, C.byref(bad), 1, None, None) == _lib.MPO_EINVAL
     # unsupported grad dtype
     rc, _ = _status(L, L.mpo_adam_step(_lib.MPO_BF16, 7, tab, 2, C.byref(hp), 1, None, None))
     assert rc == _lib.MPO_EDTYPE
     # clipping without a workspace
-    clip = A(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 1.0, 1, 0, 1)
+    clip = A(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 1.0, 1, 0, 1, 0)
     assert L.mpo_adam_step(_lib.MPO_BF16, _lib.MPO_BF16, tab, 2, C.byref(clip), 1, None, None) == _lib.MPO_EINVAL
     # group count out of range
     assert L.mpo_adam_step(_lib.MPO_BF16, _lib.MPO_BF16, tab, 2, C.byref(hp), 0, None, None) == _lib.MPO_EINVAL
     # SGD: nesterov without momentum
-    s = S(0.1, 0.0, 0.0, 0.0, 1.0, 1, 0)
+    s = S(0.1, 0.0, 0.0, 0.0, 1.0, 1, 0, 0)
     rc, msg = _status(L, L.mpo_sgd_step(_lib.MPO_FP16, _lib.MPO_FP16, tab, 2, C.byref(s), 1, None))
     assert rc == _lib.MPO_EINVAL and "nesterov" in msg
 
@@ -113,7 +113,7 @@ def test_hook_refuses_global_clipping(libs):
     """P:93 / P:186: global operations are impossible inside the fused backward."""
     _lib, L, _ = libs
     one = _lib.Tensor(16, 32, 48, 64, 80, 8, 0, 0)
-    clip = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 1.0, 1, 0, 1)
+    clip = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 1.0, 1, 0, 1, 0)
     rc, msg = _status(L, L.mpo_fused_backward_hook_step(_lib.MPO_ADAM, _lib.MPO_BF16, _lib.MPO_BF16, C.byref(one),
                                                         C.byref(clip), None))
     assert rc == _lib.MPO_EINVAL and "P:186" in msg
@@ -123,7 +123,7 @@ def test_hook_refuses_global_clipping(libs):
 
 def test_sharded_validation(libs):
     _lib, L, _ = libs
-    hp = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1)
+    hp = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1, 0)
     args = lambda comm, rank, world, n: (_lib.MPO_ADAM, comm, rank, world, _lib.MPO_BF16, 16, 32, 48, 64, 80, n,
                                          C.byref(hp), None, None)
     assert L.mpo_sharded_step(*args(0, 0, 2, 32)) == _lib.MPO_EINVAL          # NULL comm

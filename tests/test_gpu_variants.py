@@ -1,0 +1,145 @@
+"""GPU parity of the paper variants of the storage scheme against the CPU oracle.
+
+* split / reconstruct under RTZ (fp16, bf16), SR (fp16) and X8 (fp16, bf16): bit-exact on ALL 2^32
+  binary32 patterns (SR with the shared counter-based draws keyed by (seed, stream, index));
+* Adam / AdamW / SGD-momentum steps through the multi-tensor table, ragged sizes (tails of X8's
+  16-element bulk-copy granule included), several hyper-parameter groups and streams: bit-exact
+  in the -fmad=false build, every step;
+* the optimizer objects: hook mode == multi-tensor mode bitwise under SR (per-parameter streams).
+"""
+import os
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from gpu_util import TDT, bits32, dev16, dev_grad, devf, hostf, host16
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = [("rtz", "fp16"), ("rtz", "bf16"), ("sr", "fp16"), ("x8", "fp16"), ("x8", "bf16")]
+RDT = {"rne": np.int16, "rtz": np.uint16, "sr": np.int16, "x8": np.int8}
+
+
+@pytest.fixture(scope="module")
+def mpo():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2309_12381_b200 as m
+    from paper_2309_12381_b200 import _build
+    _build.build()
+    return m
+
+
+def dev_resid(r):
+    if r.dtype == np.int8:
+        return torch.from_numpy(r.copy()).cuda()
+    return torch.from_numpy(np.ascontiguousarray(r).view(np.int16).copy()).cuda()
+
+
+def host_resid(t, scheme):
+    a = t.cpu().numpy()
+    return a.view(RDT[scheme]) if scheme != "x8" else a
+
+
+@pytest.mark.parametrize("scheme,fmt", VARIANTS)
+def test_variant_split_reconstruct_all_2_32(mpo, orc, scheme, fmt):
+    chunk = 1 << 26
+    lock = threading.Lock()
+    seed = 0xC0FFEE
+
+    def one(c):
+        u = np.arange(c * chunk, (c + 1) * chunk, dtype=np.uint64).astype(np.uint32)
+        x = u.view(np.float32)
+        ho, ro = orc.split_s(scheme, fmt, x, seed=seed + c, stream=3)
+        reco = orc.reconstruct_s(scheme, fmt, ho, ro)
+        with lock:
+            v, r = mpo.mpo_split(devf(x), TDT[fmt], scheme=scheme, seed=seed + c, sr_stream=3)
+            rec = mpo.mpo_reconstruct(v, r, scheme=scheme)
+            hg, rg, recg = host16(v), host_resid(r, scheme), hostf(rec)
+        return int(np.count_nonzero(hg != ho)) + int(np.count_nonzero(rg != ro)) + \
+            int(np.count_nonzero(bits32(recg) != bits32(reco)))
+
+    with ThreadPoolExecutor(max_workers=max(2, min(16, os.cpu_count() or 2))) as ex:
+        assert sum(ex.map(one, range(64))) == 0
+
+
+SIZES = [0, 1, 7, 8, 9, 15, 16, 17, 4095, 4096, 4097, 12345, 65539, 3]
+
+
+def _kw(hp):
+    return dict(lr=hp.lr, beta1=hp.beta1, beta2=hp.beta2, eps=hp.eps, weight_decay=hp.weight_decay,
+                adamw=hp.adamw, grad_scale=hp.grad_scale, step=hp.step)
+
+
+@pytest.mark.parametrize("scheme,fmt", VARIANTS)
+@pytest.mark.parametrize("kind", ["adam", "sgd"])
+@pytest.mark.parametrize("gsame", [True, False])
+def test_variant_steps_bit_exact(mpo, orc, scheme, fmt, kind, gsame):
+    gf = fmt if gsame else "fp32"
+    hs, rs, ms, vs = [], [], [], []
+    for i, n in enumerate(SIZES):
+        w = synth.weights(n, 0.05, 0xB0B + i)
+        if n > 40:
+            w[:36] = synth.edge_f32() * np.float32(1e-3)
+        h, r = orc.split_s(scheme, fmt, w, seed=77, stream=i)
+        hs.append(h); rs.append(r)
+        ms.append(synth.normal_f32(n, 1e-3, 5, i)); vs.append(np.abs(synth.normal_f32(n, 1e-5, 6, i)))
+    V = [dev16(h, fmt) for h in hs]
+    R = [dev_resid(r) for r in rs]
+    M = [devf(m) for m in ms]
+    W = [devf(v) for v in vs]
+    grp = [i % 2 for i in range(len(SIZES))]
+    for t in range(1, 4):
+        gs = [synth.grads(n, 1e-2, gf, 0xC0FFEE + t, i) for i, n in enumerate(SIZES)]
+        G = [dev_grad(g, gf) for g in gs]
+        seed = 1000 + t
+        if kind == "adam":
+            hps = [mpo.AdamParams(lr=1e-3, weight_decay=0.1, adamw=True, step=t, seed=seed),
+                   mpo.AdamParams(lr=2e-3, beta2=0.95, weight_decay=0.01, adamw=False, step=t, grad_scale=0.5,
+                                  seed=seed)]
+            tab = mpo.TensorTable(V, R, G, M, W, grp, scheme=scheme)
+            mpo.mpo_adam_step(tab, hps, exact=True)
+        else:
+            hps = [mpo.SgdParams(lr=0.1, momentum=0.9, weight_decay=1e-4, first_step=(t == 1), seed=seed),
+                   mpo.SgdParams(lr=0.05, momentum=0.9, nesterov=True, first_step=(t == 1), seed=seed)]
+            tab = mpo.TensorTable(V, R, G, M, [None] * len(SIZES), grp, scheme=scheme)
+            mpo.mpo_sgd_step(tab, hps, exact=True)
+        for i, n in enumerate(SIZES):
+            hp = hps[grp[i]]
+            if kind == "adam":
+                orc.adam_step_s(scheme, fmt, gf, hs[i], rs[i], gs[i], ms[i], vs[i], seed=seed, stream=i, **_kw(hp))
+            else:
+                orc.sgd_step_s(scheme, fmt, gf, hs[i], rs[i], gs[i], ms[i], lr=hp.lr, momentum=hp.momentum,
+                               weight_decay=hp.weight_decay, nesterov=hp.nesterov, first_step=hp.first_step,
+                               seed=seed, stream=i)
+    for i in range(len(SIZES)):
+        assert np.array_equal(host16(V[i]), hs[i]), (i, SIZES[i])
+        assert np.array_equal(host_resid(R[i], scheme), rs[i]), (i, SIZES[i])
+        assert np.array_equal(M[i].cpu().numpy().view(np.uint32), ms[i].view(np.uint32)), i
+
+
+def test_sr_hook_mode_equals_multi_tensor(mpo):
+    """Stochastic rounding keyed by per-parameter streams: the fused-backward path and the
+    multi-tensor path draw the same numbers and agree bitwise."""
+    torch.manual_seed(0)
+    d = 96
+    mk = lambda: torch.nn.Sequential(torch.nn.Linear(d, 2 * d), torch.nn.GELU(), torch.nn.Linear(2 * d, d)).cuda()
+    a, b = mk(), mk()
+    b.load_state_dict(a.state_dict())
+    oa = mpo.ResidualAdamW(a.parameters(), lr=1e-3, weight_decay=0.1, fmt=torch.float16, scheme="sr", seed=9)
+    ob = mpo.ResidualAdamW(b.parameters(), lr=1e-3, weight_decay=0.1, fmt=torch.float16, scheme="sr", seed=9)
+    ob.install_backward_hooks()
+    for t in range(3):
+        x = torch.randn(32, d, device="cuda", dtype=torch.float16)
+        a(x).float().square().mean().backward()
+        oa.step()
+        for p in a.parameters():
+            p.grad = None
+        b(x).float().square().mean().backward()
+    for pa, pb in zip(a.parameters(), b.parameters()):
+        assert torch.equal(pa.view(torch.int16), pb.view(torch.int16))
+        assert torch.equal(oa.state[pa]["resid"], ob.state[pb]["resid"])
