@@ -121,11 +121,12 @@ class Workload:
     """Flat value / residual / grad / state buffers with one 16-B aligned view per parameter
     (ShardLayout), and the cached multi-tensor table."""
 
-    def __init__(self, name, world=1, rank=0, seed=0xB0B):
+    def __init__(self, name, world=1, rank=0, seed=0xB0B, scheme="rne"):
         import torch
         import paper_2309_12381_b200 as mpo
         from synth import torch_normal_, workloads
         self.name = name
+        self.scheme = scheme
         wl, fmt, kind, hp, cfg = WORKLOADS[name]
         self.kind, self.fmt, self.hpkw, self.cfg = kind, fmt, hp, cfg
         self.sizes = workloads.sizes(wl)
@@ -140,15 +141,17 @@ class Workload:
         base = torch.cuda.memory_allocated()
         self.value = torch.empty(L.total, dtype=self.tdt, device=dev)
         # fp32 init, split on the device chunk by chunk (N(0,0.02), seeded)
-        resid_full = torch.empty(L.shard if world > 1 else L.total, dtype=torch.int16, device=dev)
+        rdt = mpo.api.resid_dtype(scheme)
+        resid_full = torch.empty(L.shard if world > 1 else L.total, dtype=rdt, device=dev)
         chunk = 1 << 28
         lo, hi = L.shard_range(rank) if world > 1 else (0, L.total)
-        tmp_r = torch.empty(min(chunk, L.total), dtype=torch.int16, device=dev)
+        tmp_r = torch.empty(min(chunk, L.total), dtype=rdt, device=dev)
         for s in range(0, L.total, chunk):
             e = min(L.total, s + chunk)
             w32 = torch.empty(e - s, dtype=torch.float32, device=dev)
             torch_normal_(w32, 0.02, seed, s // chunk)
-            mpo.mpo_split(w32, self.tdt, value=self.value[s:e], resid=tmp_r[:e - s])
+            mpo.mpo_split(w32, self.tdt, value=self.value[s:e], resid=tmp_r[:e - s], scheme=scheme, seed=seed,
+                          sr_stream=s // chunk)
             a, b = max(s, lo), min(e, hi)
             if a < b:
                 resid_full[a - lo:b - lo].copy_(tmp_r[a - s:b - s])
@@ -175,7 +178,7 @@ class Workload:
             G = L.views(self.grad, shapes)
             M = L.views(self.m, shapes)
             W = L.views(self.v, shapes) if self.v is not None else [None] * len(shapes)
-            self.table = mpo.TensorTable(V, R, G, M, W)
+            self.table = mpo.TensorTable(V, R, G, M, W, scheme=scheme)
         self.comm = None
 
     @property
@@ -184,13 +187,15 @@ class Workload:
 
     @property
     def bytes_per_param(self):
-        return BYTES_PER_PARAM["adam_clip" if self.clip else self.kind]
+        b = BYTES_PER_PARAM["adam_clip" if self.clip else self.kind]
+        return b - 2 if self.scheme == "x8" else b      # int8 residual: 1 B read + 1 B written
 
     def hp(self):
         mpo = self.mpo
+        seed = mpo.api.step_seed(0xB0B, self.t)
         if self.kind == "sgd":
-            return mpo.SgdParams(first_step=(self.t == 1), **self.hpkw)
-        return mpo.AdamParams(step=self.t, **self.hpkw)
+            return mpo.SgdParams(first_step=(self.t == 1), seed=seed, **self.hpkw)
+        return mpo.AdamParams(step=self.t, seed=seed, **self.hpkw)
 
     def step(self, sharded=False):
         """One pass of the hot path (one C-ABI call)."""
@@ -215,7 +220,7 @@ class Workload:
                 self.comm = nccl_comm_ptr()
             mpo.mpo_sharded_step(MPO_ADAM if self.kind == "adam" else MPO_SGD, self.comm, self.rank, self.world,
                                  self.value, self.grad, self.resid, self.m, self.v, hp,
-                                 norm_ws=self.norm_ws if self.clip else None)
+                                 norm_ws=self.norm_ws if self.clip else None, scheme=self.scheme)
         elif self.kind == "sgd":
             mpo.mpo_sgd_step(self.table, hp)
         else:
@@ -416,16 +421,16 @@ def secondary(names, steps, warmup, hbm_peak):
     return out
 
 
-def _secondary_one(name, steps, warmup, hbm_peak):
+def _secondary_one(name, steps, warmup, hbm_peak, scheme="rne"):
     import torch
     if True:
-        wl = Workload(name)
+        wl = Workload(name, scheme=scheme)
         use_sharded = name == "llama7b_adam"
         st = max(3, min(steps, int(2.0 / max(1e-6, wl.P * wl.bytes_per_param / (hbm_peak * 1e9)))))
         ms, launches = timed(lambda: wl.step(sharded=use_sharded), st, warmup)
         res = {"params_per_s": wl.P / (ms * 1e-3), "ms_per_step": ms, "steps": st,
                      "config": f"BASELINE configs[{wl.cfg}] parameter set {WORKLOADS[name][0]} "
-                               f"({wl.P} params, {wl.ntensors} tensors), {wl.fmt}+int16 residual, "
+                               f"({wl.P} params, {wl.ntensors} tensors), {wl.fmt} + {scheme} residual, "
                                + ("mpo_sharded_step world 1 (RS/AG degenerate)" if use_sharded else
                                   "one multi-tensor launch" + (" + norm pre-pass" if wl.clip else "")),
                      "bytes_per_param": wl.bytes_per_param,
@@ -596,6 +601,18 @@ def main():
         del wl
         torch.cuda.empty_cache()
         line["secondary"] = secondary(["gpt2_adamw", "vit_l16_adam_clip", "llama7b_adam"], 200, 5, hbm_peak)
+        for sch in ("rtz", "sr", "x8"):    # paper variants of the storage scheme, GPT-2 AdamW set
+            name = "gpt2_adamw"
+            fmt_ok = sch != "sr" or WORKLOADS[name][1] == "fp16"
+            key = f"{name}_{sch}" + ("" if fmt_ok else "_fp16")
+            try:
+                if not fmt_ok:   # SR is defined for fp16: same parameter set in fp16
+                    WORKLOADS["gpt2_adamw_fp16"] = ("gpt2_small", "fp16") + WORKLOADS[name][2:]
+                    name = "gpt2_adamw_fp16"
+                line["secondary"][key] = _secondary_one(name, 200, 5, hbm_peak, scheme=sch)
+            except Exception as ex:
+                line["secondary"][key] = {"error": f"{type(ex).__name__}: {ex}"}
+            torch.cuda.empty_cache()
         try:
             line["secondary"]["gpt2_hook_mode"] = hook_mode_secondary()
         except Exception as ex:
