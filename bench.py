@@ -515,7 +515,9 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
         res = {"ms_per_train_step": s.elapsed_time(e) / steps, "state_bytes_per_param": state / P,
                "persistent_bytes_per_param": persistent / P,
                "peak_bytes_per_param": peak / P, "peak_gb": peak / 1e9, "loss": float(loss)}
-        del model, opt
+        del model, opt, step
+        import gc
+        gc.collect()          # hooks <-> params <-> optimizer form reference cycles
         torch.cuda.empty_cache()
         return res
     for mode in ("hook", "two_phase", "amp_fp32_master"):
