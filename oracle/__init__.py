@@ -36,13 +36,13 @@ def build(force: bool = False) -> str:
 class SgdHP(C.Structure):
     _fields_ = [("lr", C.c_double), ("momentum", C.c_double), ("dampening", C.c_double),
                 ("weight_decay", C.c_double), ("grad_scale", C.c_double),
-                ("nesterov", C.c_int32), ("first_step", C.c_int32)]
+                ("nesterov", C.c_int32), ("first_step", C.c_int32), ("clip_value", C.c_double)]
 
 
 class AdamHP(C.Structure):
     _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
                 ("eps", C.c_double), ("weight_decay", C.c_double), ("grad_scale", C.c_double),
-                ("adamw", C.c_int32), ("step", C.c_int64)]
+                ("adamw", C.c_int32), ("step", C.c_int64), ("clip_value", C.c_double)]
 
 
 _lib = None
@@ -152,38 +152,38 @@ def _grad_fmt(grad: np.ndarray, gfmt: str):
 
 
 def sgd_step(vfmt, gfmt, value, resid, grad, buf, *, lr, momentum=0.0, dampening=0.0,
-             weight_decay=0.0, grad_scale=1.0, nesterov=False, first_step=False):
+             weight_decay=0.0, grad_scale=1.0, nesterov=False, first_step=False, clip_value=0.0):
     """In-place residual-compensated SGD step on one tensor (buf may be None if momentum=0)."""
     _chk(value, np.uint16); _chk(resid, np.int16); _grad_fmt(grad, gfmt)
     if buf is not None:
         _chk(buf, np.float32)
-    hp = SgdHP(lr, momentum, dampening, weight_decay, grad_scale, int(nesterov), int(first_step))
+    hp = SgdHP(lr, momentum, dampening, weight_decay, grad_scale, int(nesterov), int(first_step), clip_value)
     lib().or_sgd_step(FMT[vfmt], FMT[gfmt], _ptr(value), _ptr(resid), _ptr(grad), _ptr(buf),
                       value.size, C.byref(hp))
 
 
 def adam_step(vfmt, gfmt, value, resid, grad, m, v, *, lr, beta1=0.9, beta2=0.999, eps=1e-8,
-              weight_decay=0.0, adamw=True, grad_scale=1.0, step=1, clip_coef=None):
+              weight_decay=0.0, adamw=True, grad_scale=1.0, step=1, clip_coef=None, clip_value=0.0):
     """In-place residual-compensated Adam/AdamW step on one tensor."""
     _chk(value, np.uint16); _chk(resid, np.int16); _grad_fmt(grad, gfmt)
     _chk(m, np.float32); _chk(v, np.float32)
-    hp = AdamHP(lr, beta1, beta2, eps, weight_decay, grad_scale, int(adamw), int(step))
+    hp = AdamHP(lr, beta1, beta2, eps, weight_decay, grad_scale, int(adamw), int(step), clip_value)
     cc = -1.0 if clip_coef is None else float(clip_coef)
     lib().or_adam_step(FMT[vfmt], FMT[gfmt], _ptr(value), _ptr(resid), _ptr(grad), _ptr(m),
                        _ptr(v), value.size, C.byref(hp), cc)
 
 
 def sgd_step_master(gfmt, w, grad, buf, *, lr, momentum=0.0, dampening=0.0, weight_decay=0.0,
-                    grad_scale=1.0, nesterov=False, first_step=False):
+                    grad_scale=1.0, nesterov=False, first_step=False, clip_value=0.0):
     _chk(w, np.float32); _grad_fmt(grad, gfmt)
-    hp = SgdHP(lr, momentum, dampening, weight_decay, grad_scale, int(nesterov), int(first_step))
+    hp = SgdHP(lr, momentum, dampening, weight_decay, grad_scale, int(nesterov), int(first_step), clip_value)
     lib().or_sgd_step_master(FMT[gfmt], _ptr(w), _ptr(grad), _ptr(buf), w.size, C.byref(hp))
 
 
 def adam_step_master(gfmt, w, grad, m, v, *, lr, beta1=0.9, beta2=0.999, eps=1e-8,
-                     weight_decay=0.0, adamw=True, grad_scale=1.0, step=1, clip_coef=None):
+                     weight_decay=0.0, adamw=True, grad_scale=1.0, step=1, clip_coef=None, clip_value=0.0):
     _chk(w, np.float32); _grad_fmt(grad, gfmt)
-    hp = AdamHP(lr, beta1, beta2, eps, weight_decay, grad_scale, int(adamw), int(step))
+    hp = AdamHP(lr, beta1, beta2, eps, weight_decay, grad_scale, int(adamw), int(step), clip_value)
     cc = -1.0 if clip_coef is None else float(clip_coef)
     lib().or_adam_step_master(FMT[gfmt], _ptr(w), _ptr(grad), _ptr(m), _ptr(v), w.size,
                               C.byref(hp), cc)
@@ -239,18 +239,20 @@ def reconstruct_s(scheme: str, fmt: str, h: np.ndarray, r: np.ndarray) -> np.nda
 
 
 def sgd_step_s(scheme, vfmt, gfmt, value, resid, grad, buf, *, lr, momentum=0.0, dampening=0.0,
-               weight_decay=0.0, grad_scale=1.0, nesterov=False, first_step=False, seed=0, stream=0):
+               weight_decay=0.0, grad_scale=1.0, nesterov=False, first_step=False, seed=0, stream=0,
+               clip_value=0.0):
     _chk(value, np.uint16); _chk(resid, RESID_DTYPE[scheme]); _grad_fmt(grad, gfmt)
-    hp = SgdHP(lr, momentum, dampening, weight_decay, grad_scale, int(nesterov), int(first_step))
+    hp = SgdHP(lr, momentum, dampening, weight_decay, grad_scale, int(nesterov), int(first_step), clip_value)
     lib().or_sgd_step_s(SCHEME[scheme], FMT[vfmt], FMT[gfmt], _ptr(value), _ptr(resid), _ptr(grad), _ptr(buf),
                         value.size, C.byref(hp), seed, stream)
 
 
 def adam_step_s(scheme, vfmt, gfmt, value, resid, grad, m, v, *, lr, beta1=0.9, beta2=0.999, eps=1e-8,
-                weight_decay=0.0, adamw=True, grad_scale=1.0, step=1, clip_coef=None, seed=0, stream=0):
+                weight_decay=0.0, adamw=True, grad_scale=1.0, step=1, clip_coef=None, seed=0, stream=0,
+                clip_value=0.0):
     _chk(value, np.uint16); _chk(resid, RESID_DTYPE[scheme]); _grad_fmt(grad, gfmt)
     _chk(m, np.float32); _chk(v, np.float32)
-    hp = AdamHP(lr, beta1, beta2, eps, weight_decay, grad_scale, int(adamw), int(step))
+    hp = AdamHP(lr, beta1, beta2, eps, weight_decay, grad_scale, int(adamw), int(step), clip_value)
     cc = -1.0 if clip_coef is None else float(clip_coef)
     lib().or_adam_step_s(SCHEME[scheme], FMT[vfmt], FMT[gfmt], _ptr(value), _ptr(resid), _ptr(grad), _ptr(m),
                          _ptr(v), value.size, C.byref(hp), cc, seed, stream)

@@ -201,13 +201,27 @@ static float load_grad(int gfmt, const void* grad, int64_t i) {
 typedef struct {
     double lr, momentum, dampening, weight_decay, grad_scale;
     int32_t nesterov, first_step;
+    double clip_value;     /* > 0: clamp the scaled gradient to [-c, c]; 0: off */
 } or_sgd_hp;
 
 typedef struct {
     double lr, beta1, beta2, eps, weight_decay, grad_scale;
     int32_t adamw;
     int64_t step;          /* 1-based */
+    double clip_value;     /* > 0: clamp the scaled gradient to [-c, c]; 0: off */
 } or_adam_hp;
+
+/* Clip-by-value of the (scaled) gradient: the paper's hook "torch.clamp(grad, -clip_value,
+ * clip_value)", applied as the optimizer's gradient ingest.  NaN stays NaN
+ * (torch.clamp semantics), +-Inf clamps to +-c. */
+static float clamp_grad(float g, double clip_value) {
+    float c;
+    if (!(clip_value > 0.0)) return g;
+    c = (float)clip_value;
+    if (g > c) return c;
+    if (g < -c) return -c;
+    return g;
+}
 
 /* SGD(-momentum) element update on the fp32 value w (torch.optim.SGD). */
 static float sgd_update(float w, float g, float* buf, const or_sgd_hp* hp) {
@@ -273,7 +287,7 @@ void or_sgd_step(int vfmt, int gfmt, uint16_t* value, int16_t* resid, const void
     int64_t i;
     float gs = (float)hp->grad_scale;
     for (i = 0; i < n; i++) {
-        float g = load_grad(gfmt, grad, i) * gs;
+        float g = clamp_grad(load_grad(gfmt, grad, i) * gs, hp->clip_value);
         float w = u2f(reconstruct1(vfmt, value[i], resid[i]));
         w = sgd_update(w, g, buf ? &buf[i] : 0, hp);
         split1(vfmt, f2u(w), &value[i], &resid[i]);
@@ -289,7 +303,7 @@ void or_adam_step(int vfmt, int gfmt, uint16_t* value, int16_t* resid, const voi
     float gs = (float)hp->grad_scale;
     adam_scalars c = adam_derive(hp);
     for (i = 0; i < n; i++) {
-        float g = load_grad(gfmt, grad, i) * gs;
+        float g = clamp_grad(load_grad(gfmt, grad, i) * gs, hp->clip_value);
         float w;
         if (clip_coef >= 0.0f || clip_coef != clip_coef) g = g * clip_coef;
         w = u2f(reconstruct1(vfmt, value[i], resid[i]));
@@ -305,7 +319,7 @@ void or_sgd_step_master(int gfmt, float* w, const void* grad, float* buf, int64_
     int64_t i;
     float gs = (float)hp->grad_scale;
     for (i = 0; i < n; i++) {
-        float g = load_grad(gfmt, grad, i) * gs;
+        float g = clamp_grad(load_grad(gfmt, grad, i) * gs, hp->clip_value);
         w[i] = sgd_update(w[i], g, buf ? &buf[i] : 0, hp);
     }
 }
@@ -316,7 +330,7 @@ void or_adam_step_master(int gfmt, float* w, const void* grad, float* m, float* 
     float gs = (float)hp->grad_scale;
     adam_scalars c = adam_derive(hp);
     for (i = 0; i < n; i++) {
-        float g = load_grad(gfmt, grad, i) * gs;
+        float g = clamp_grad(load_grad(gfmt, grad, i) * gs, hp->clip_value);
         if (clip_coef >= 0.0f || clip_coef != clip_coef) g = g * clip_coef;
         w[i] = adam_update(w[i], g, &m[i], &v[i], &c);
     }
@@ -469,7 +483,7 @@ void or_sgd_step_s(int scheme, int vfmt, int gfmt, uint16_t* value, void* resid,
     int64_t i;
     float gs = (float)hp->grad_scale;
     for (i = 0; i < n; i++) {
-        float g = load_grad(gfmt, grad, i) * gs;
+        float g = clamp_grad(load_grad(gfmt, grad, i) * gs, hp->clip_value);
         float w = u2f(reconstruct_s(scheme, vfmt, value[i], load_resid(scheme, resid, i)));
         uint16_t h; int32_t r;
         w = sgd_update(w, g, buf ? &buf[i] : 0, hp);
@@ -485,7 +499,7 @@ void or_adam_step_s(int scheme, int vfmt, int gfmt, uint16_t* value, void* resid
     float gs = (float)hp->grad_scale;
     adam_scalars c = adam_derive(hp);
     for (i = 0; i < n; i++) {
-        float g = load_grad(gfmt, grad, i) * gs;
+        float g = clamp_grad(load_grad(gfmt, grad, i) * gs, hp->clip_value);
         float w;
         uint16_t h; int32_t r;
         if (clip_coef >= 0.0f || clip_coef != clip_coef) g = g * clip_coef;

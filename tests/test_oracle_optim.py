@@ -266,3 +266,51 @@ def test_p9_byte_model(orc):
     assert orc.bytes_per_param("ours_fused_backward", "adam") == 12
     assert orc.bytes_per_param("ours_fused_backward", "sgd_momentum") == 8
     assert orc.bytes_per_param("ours_multi_tensor", "adam") == 14
+
+
+# ------------------------------------------------------------- clip-by-value ingest --
+def test_clip_value_closed_form_and_torch_clamp(orc):
+    """SPEC S:322 example: clip c=0.5, grad [1, -2, 0.1] -> effective grad [0.5, -0.5, 0.1]; and on
+    random grads (with +-Inf, NaN) the oracle's ingest equals torch.clamp (library routine), seen
+    through an SGD step with lr=1 from w=0 (w_new = -g_effective exactly)."""
+    import torch
+    g = np.array([1.0, -2.0, 0.1], np.float32)
+    w = np.zeros(3, np.float32)
+    orc.sgd_step_master("fp32", w, g, None, lr=1.0, clip_value=0.5)
+    assert np.array_equal(-w, np.array([0.5, -0.5, np.float32(0.1)], np.float32))
+    g = np.concatenate([synth.normal_f32(5000, 2.0, 3, 3), np.array([np.inf, -np.inf, np.nan, 0.0, -0.0], np.float32)])
+    for c, gs in ((0.7, 1.0), (1.5, 0.25), (3.0, 2.0)):
+        w = np.zeros(g.size, np.float32)
+        orc.sgd_step_master("fp32", w, g, None, lr=1.0, grad_scale=gs, clip_value=c)
+        want = torch.clamp(torch.from_numpy(g) * np.float32(gs), -np.float32(c), np.float32(c)).numpy()
+        got = -w
+        nan = np.isnan(want)
+        assert np.array_equal(np.isnan(got), nan) and np.array_equal(got[~nan], want[~nan])
+    # clip_value 0 = off: identical to the unclipped step
+    w1 = np.zeros(g.size, np.float32); w2 = np.zeros(g.size, np.float32)
+    orc.sgd_step_master("fp32", w1, g, None, lr=1.0, clip_value=0.0)
+    orc.sgd_step_master("fp32", w2, g, None, lr=1.0)
+    assert np.array_equal(w1.view(np.uint32), w2.view(np.uint32))
+
+
+def test_clip_value_in_residual_steps_matches_master(orc):
+    """The residual-compensated Adam / SGD steps apply the same ingest (bf16: value+residual equal
+    the clipped fp32-master trajectory on every element without a lossy split)."""
+    n = 4096
+    w = synth.weights(n, 0.02, 11)
+    g = synth.grads(n, 5e-2, "bf16", 11, 1)
+    for kind in ("adam", "sgd"):
+        h, r = orc.split("bf16", w)
+        wm = w.copy()
+        m = np.zeros(n, np.float32); v = np.zeros(n, np.float32)
+        mm = np.zeros(n, np.float32); vm = np.zeros(n, np.float32)
+        if kind == "adam":
+            orc.adam_step("bf16", "bf16", h, r, g, m, v, lr=1e-3, clip_value=0.03)
+            orc.adam_step_master("bf16", wm, g, mm, vm, lr=1e-3, clip_value=0.03)
+        else:
+            orc.sgd_step("bf16", "bf16", h, r, g, m, lr=0.1, momentum=0.9, first_step=True, clip_value=0.03)
+            orc.sgd_step_master("bf16", wm, g, mm, lr=0.1, momentum=0.9, first_step=True, clip_value=0.03)
+        rec = orc.reconstruct("bf16", h, r)
+        lossy = (r == 32767)
+        assert np.array_equal(rec.view(np.uint32)[~lossy], wm.view(np.uint32)[~lossy])
+        assert np.array_equal(m, mm)
