@@ -114,6 +114,9 @@ typedef struct {
     double lr, momentum, dampening, weight_decay, grad_scale;
     int32_t nesterov, first_step;
     uint64_t seed;   /* stochastic-rounding draws of this step (MPO_FP16_SR); else ignored */
+    double clip_value;       /* > 0: clamp the scaled gradient to [-c, c] (see below); 0: off */
+    int32_t skip_nonfinite;  /* != 0: skip the update when a scaled gradient is Inf/NaN (below) */
+    int32_t _pad2;
 } mpo_sgd_hp;
 
 /* torch.optim.Adam / AdamW semantics (R6).  step is 1-based (bias correction).  adamw != 0:
@@ -126,7 +129,25 @@ typedef struct {
     int32_t adamw, _pad;
     int64_t step;
     uint64_t seed;   /* stochastic-rounding draws of this step (MPO_FP16_SR); else ignored */
+    double clip_value;       /* > 0: clamp the scaled gradient to [-c, c] (see below); 0: off */
+    int32_t skip_nonfinite;  /* != 0: skip the update when a scaled gradient is Inf/NaN (below) */
+    int32_t _pad2;
 } mpo_adam_hp;
+
+/* Gradient surgery inside the optimizer ("every operations on the gradient (eg. clipping or
+ * scaling) has to be done through the optimizer"; "perform the clipping through a
+ * parameter hook ... The same applies to loss scaling"):
+ *   grad_scale      multiplies first (loss-scale unscale; 1/N data-parallel mean);
+ *   clip_value      then clamps to [-c, c] like torch.clamp (NaN stays NaN), in every mode;
+ *                   exclusive with max_grad_norm;
+ *   skip_nonfinite  loss-scaling "found inf": the fp64 sum of squares S of the scaled grads is
+ *                   computed first (needs norm_ws) and the update is skipped -- nothing written --
+ *                   when S is not finite.  Multi-tensor and sharded modes skip the whole call
+ *                   (sharded: S all-reduced, all ranks agree); the hook mode can only skip the
+ *                   one parameter (earlier parameters of the same backward were already stepped,
+ *                   P:93) and accumulates S into norm_ws[mpo_norm_ws_doubles() - 1] so the
+ *                   caller learns at the end of backward whether any gradient was non-finite.
+ * Must be the same for every group of a call. */
 
 /* Largest number of hyper-parameter groups one call may carry. */
 #define MPO_MAX_HP_GROUPS 16
@@ -148,28 +169,31 @@ mpo_status mpo_reconstruct(mpo_dtype vdt, const void* value, const void* resid, 
  * table slice.  hp: nhp groups (1 <= nhp <= MPO_MAX_HP_GROUPS) in HOST memory;
  * t: nt entries in HOST memory (copied into the launch; not retained). */
 mpo_status mpo_sgd_step(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t, int32_t nt,
-                        const mpo_sgd_hp* hp, int32_t nhp, mpo_stream stream);
+                        const mpo_sgd_hp* hp, int32_t nhp, double* norm_ws, mpo_stream stream);
 
 /* Residual-compensated Adam/AdamW step over a table of nt tensors.
  * norm_ws: DEVICE scratch of at least mpo_norm_ws_doubles() doubles, required iff
  * max_grad_norm > 0 (global-norm clipping: fp64 sum of squares of the scaled gradients over
- * the whole table, coef = min(1, max_norm / (sqrt(S) + 1e-6)), R9).  On return (stream
- * order) norm_ws[0] holds S. */
+ * the whole table, coef = min(1, max_norm / (sqrt(S) + 1e-6)), R9) or skip_nonfinite.  On
+ * return (stream order) norm_ws[0] holds S.  mpo_sgd_step takes the same workspace (needed iff
+ * skip_nonfinite). */
 mpo_status mpo_adam_step(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t, int32_t nt,
                          const mpo_adam_hp* hp, int32_t nhp, double* norm_ws,
                          mpo_stream stream);
 
-/* Doubles of device scratch mpo_adam_step / mpo_sharded_step need for clipping. */
+/* Doubles of device scratch the norm pre-pass needs (clipping, skip_nonfinite): [0] = S of the
+ * call, then per-block partials, last = S accumulated by hook-mode calls (zeroed by the caller). */
 int64_t mpo_norm_ws_doubles(void);
 
 /* Fused backward + optimizer step for ONE parameter, called from its post-accumulate-grad hook
  * ("operate the optimization step as soon as the gradient is computed").
  *   kind : MPO_SGD (hp -> mpo_sgd_hp) | MPO_ADAM (hp -> mpo_adam_hp), hp in HOST memory
  *   one  : the parameter's table entry (its hp field is ignored)
+ *   norm_ws : device workspace, required iff skip_nonfinite (see "Gradient surgery")
  * Global operations are impossible here: MPO_EINVAL if max_grad_norm > 0.
  * The caller frees the gradient right after the call; stream order makes that safe. */
 mpo_status mpo_fused_backward_hook_step(mpo_optim kind, mpo_dtype vdt, mpo_dtype gdt,
-                                        const mpo_tensor* one, const void* hp,
+                                        const mpo_tensor* one, const void* hp, double* norm_ws,
                                         mpo_stream stream);
 
 /* Data-parallel sharded step (not in the paper, which lists distribution as future work,

@@ -43,14 +43,16 @@ class SgdHP(C.Structure):
     """mpo_sgd_hp"""
     _fields_ = [("lr", C.c_double), ("momentum", C.c_double), ("dampening", C.c_double),
                 ("weight_decay", C.c_double), ("grad_scale", C.c_double), ("nesterov", C.c_int32),
-                ("first_step", C.c_int32), ("seed", C.c_uint64)]
+                ("first_step", C.c_int32), ("seed", C.c_uint64), ("clip_value", C.c_double),
+                ("skip_nonfinite", C.c_int32), ("_pad2", C.c_int32)]
 
 
 class AdamHP(C.Structure):
     """mpo_adam_hp"""
     _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
                 ("weight_decay", C.c_double), ("grad_scale", C.c_double), ("max_grad_norm", C.c_double),
-                ("adamw", C.c_int32), ("_pad", C.c_int32), ("step", C.c_int64), ("seed", C.c_uint64)]
+                ("adamw", C.c_int32), ("_pad", C.c_int32), ("step", C.c_int64), ("seed", C.c_uint64),
+                ("clip_value", C.c_double), ("skip_nonfinite", C.c_int32), ("_pad2", C.c_int32)]
 
 
 _libs: dict = {}
@@ -60,9 +62,9 @@ def _declare(L):
     P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_int
     L.mpo_split.argtypes = [D, P, P, P, I64, C.c_uint64, I32, P]
     L.mpo_reconstruct.argtypes = [D, P, P, P, I64, P]
-    L.mpo_sgd_step.argtypes = [D, D, C.POINTER(Tensor), I32, C.POINTER(SgdHP), I32, P]
+    L.mpo_sgd_step.argtypes = [D, D, C.POINTER(Tensor), I32, C.POINTER(SgdHP), I32, P, P]
     L.mpo_adam_step.argtypes = [D, D, C.POINTER(Tensor), I32, C.POINTER(AdamHP), I32, P, P]
-    L.mpo_fused_backward_hook_step.argtypes = [D, D, D, C.POINTER(Tensor), P, P]
+    L.mpo_fused_backward_hook_step.argtypes = [D, D, D, C.POINTER(Tensor), P, P, P]
     L.mpo_sharded_step.argtypes = [D, C.c_size_t, I32, I32, D, P, P, P, P, P, I64, P, P, P]
     for f in ("mpo_split", "mpo_reconstruct", "mpo_sgd_step", "mpo_adam_step", "mpo_fused_backward_hook_step",
               "mpo_sharded_step"):

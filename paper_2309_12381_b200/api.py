@@ -85,10 +85,13 @@ class SgdParams:
     nesterov: bool = False
     first_step: bool = False
     seed: int = 0
+    clip_value: float = 0.0
+    skip_nonfinite: bool = False
 
     def c(self) -> SgdHP:
         return SgdHP(self.lr, self.momentum, self.dampening, self.weight_decay, self.grad_scale,
-                     int(self.nesterov), int(self.first_step), int(self.seed))
+                     int(self.nesterov), int(self.first_step), int(self.seed), float(self.clip_value),
+                     int(self.skip_nonfinite), 0)
 
 
 @dataclass
@@ -103,10 +106,13 @@ class AdamParams:
     adamw: bool = True
     step: int = 1
     seed: int = 0
+    clip_value: float = 0.0
+    skip_nonfinite: bool = False
 
     def c(self) -> AdamHP:
         return AdamHP(self.lr, self.beta1, self.beta2, self.eps, self.weight_decay, self.grad_scale,
-                      self.max_grad_norm, int(self.adamw), 0, int(self.step), int(self.seed))
+                      self.max_grad_norm, int(self.adamw), 0, int(self.step), int(self.seed),
+                      float(self.clip_value), int(self.skip_nonfinite), 0)
 
 
 def _hp_array(hps, kind):
@@ -213,11 +219,17 @@ def mpo_reconstruct(value: torch.Tensor, resid: torch.Tensor, out: Optional[torc
     return out
 
 
-def mpo_sgd_step(table: TensorTable, hps, stream=None, exact: bool = False):
-    """Residual-compensated SGD(-momentum) step over a table."""
+def _check_ws(norm_ws, exact):
+    if norm_ws is not None and (norm_ws.dtype != torch.float64 or norm_ws.numel() < norm_ws_doubles(exact)):
+        raise MpoError(_lib.MPO_EINVAL, "norm_ws must be a float64 tensor of norm_ws_doubles() entries")
+
+
+def mpo_sgd_step(table: TensorTable, hps, norm_ws: Optional[torch.Tensor] = None, stream=None, exact: bool = False):
+    """Residual-compensated SGD(-momentum) step over a table; skip_nonfinite needs norm_ws."""
     arr, nhp = _hp_array(hps, SgdHP)
     L = _lib_of(exact)
-    _lib.check(L, L.mpo_sgd_step(table.vdt, table.gdt, table.arr, table.nt, arr, nhp, _stream(stream)))
+    _check_ws(norm_ws, exact)
+    _lib.check(L, L.mpo_sgd_step(table.vdt, table.gdt, table.arr, table.nt, arr, nhp, _ptr(norm_ws), _stream(stream)))
 
 
 def mpo_adam_step(table: TensorTable, hps, norm_ws: Optional[torch.Tensor] = None, stream=None,
@@ -225,18 +237,19 @@ def mpo_adam_step(table: TensorTable, hps, norm_ws: Optional[torch.Tensor] = Non
     """Residual-compensated Adam/AdamW step over a table; clipping needs norm_ws."""
     arr, nhp = _hp_array(hps, AdamHP)
     L = _lib_of(exact)
-    if norm_ws is not None and (norm_ws.dtype != torch.float64 or norm_ws.numel() < norm_ws_doubles()):
-        raise MpoError(_lib.MPO_EINVAL, "norm_ws must be a float64 tensor of norm_ws_doubles() entries")
+    _check_ws(norm_ws, exact)
     _lib.check(L, L.mpo_adam_step(table.vdt, table.gdt, table.arr, table.nt, arr, nhp, _ptr(norm_ws),
                                   _stream(stream)))
 
 
 def mpo_fused_backward_hook_step(kind: int, vdt: int, gdt: int, one: Tensor, hp, stream=None,
-                                 exact: bool = False):
+                                 exact: bool = False, norm_ws: Optional[torch.Tensor] = None):
     """One parameter's step from its post-accumulate-grad hook.  ``one`` is an
-    mpo_tensor row, ``hp`` an SgdHP / AdamHP struct (kept by the caller)."""
+    mpo_tensor row, ``hp`` an SgdHP / AdamHP struct (kept by the caller); norm_ws is needed for
+    skip_nonfinite (its last entry accumulates the sums of squares over the backward)."""
     L = _lib_of(exact)
-    _lib.check(L, L.mpo_fused_backward_hook_step(kind, vdt, gdt, C.byref(one), C.byref(hp), _stream(stream)))
+    _lib.check(L, L.mpo_fused_backward_hook_step(kind, vdt, gdt, C.byref(one), C.byref(hp), _ptr(norm_ws),
+                                                 _stream(stream)))
 
 
 def mpo_sharded_step(kind: int, comm_ptr: int, rank: int, world: int, value_flat: torch.Tensor,

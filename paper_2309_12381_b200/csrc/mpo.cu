@@ -129,6 +129,8 @@ AdamK derive_adam(const mpo_adam_hp& h) {
     c.fast_ok = !c.lerp_hi && c.bc2s >= 0x1p-60f && c.bc2s < 0x1p61f;
     c._pad = 0;
     c.seed = h.seed;
+    c.clip_on = h.clip_value > 0.0;
+    c.clipv = float(h.clip_value);
     return c;
 }
 
@@ -145,6 +147,8 @@ SgdK derive_sgd(const mpo_sgd_hp& h) {
     c.nesterov = h.nesterov != 0;
     c._pad = 0;
     c.seed = h.seed;
+    c.clip_on = h.clip_value > 0.0;
+    c.clipv = float(h.clip_value);
     return c;
 }
 
@@ -160,6 +164,12 @@ mpo_status check_adam_hp(const mpo_adam_hp* hp, int32_t nhp) {
             return fail(MPO_EINVAL, "adam group " + std::to_string(i) + ": betas must lie in [0, 1)");
         if (h.max_grad_norm != hp[0].max_grad_norm)
             return fail(MPO_EINVAL, "adam group " + std::to_string(i) + ": max_grad_norm differs from group 0");
+        if (!finite(h.clip_value) || h.clip_value < 0.0)
+            return fail(MPO_EINVAL, "adam group " + std::to_string(i) + ": clip_value must be finite and >= 0");
+        if (h.clip_value > 0.0 && h.max_grad_norm > 0.0)
+            return fail(MPO_EINVAL, "adam group " + std::to_string(i) + ": clip_value and max_grad_norm are exclusive");
+        if ((h.skip_nonfinite != 0) != (hp[0].skip_nonfinite != 0))
+            return fail(MPO_EINVAL, "adam group " + std::to_string(i) + ": skip_nonfinite differs from group 0");
     }
     return MPO_OK;
 }
@@ -173,6 +183,10 @@ mpo_status check_sgd_hp(const mpo_sgd_hp* hp, int32_t nhp) {
             return fail(MPO_EINVAL, "sgd group " + std::to_string(i) + ": non-finite hyper-parameter");
         if (h.nesterov && (h.momentum == 0.0 || h.dampening != 0.0))
             return fail(MPO_EINVAL, "sgd group " + std::to_string(i) + ": nesterov needs momentum > 0, dampening 0");
+        if (!finite(h.clip_value) || h.clip_value < 0.0)
+            return fail(MPO_EINVAL, "sgd group " + std::to_string(i) + ": clip_value must be finite and >= 0");
+        if ((h.skip_nonfinite != 0) != (hp[0].skip_nonfinite != 0))
+            return fail(MPO_EINVAL, "sgd group " + std::to_string(i) + ": skip_nonfinite differs from group 0");
     }
     return MPO_OK;
 }
@@ -237,7 +251,7 @@ mpo_status launch_sumsq(const mpo_tensor* t, int lo, int hi, const HP<float>& gs
 
 // Sum of squares of the scaled grads of the whole table into norm_ws[0] (partials in norm_ws[1..]).
 mpo_status table_sumsq(mpo_dtype gdt, const mpo_tensor* t, int nt, const float* gs_of_group, int nhp,
-                       double* norm_ws, cudaStream_t s) {
+                       double* norm_ws, cudaStream_t s, double* accum = nullptr) {
     HP<float> gsc;
     for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) gsc.g[i] = i < nhp ? gs_of_group[i] : 1.0f;
     int64_t tiles = 0;
@@ -261,7 +275,7 @@ mpo_status table_sumsq(mpo_dtype gdt, const mpo_tensor* t, int nt, const float* 
         nparts += nb;
         if (nt == 0) break;
     }
-    sumsq_final_kernel<<<1, kThreads, 0, s>>>(partial, nparts, norm_ws);
+    sumsq_final_kernel<<<1, kThreads, 0, s>>>(partial, nparts, norm_ws, accum);
     ++g_launches;
     return check_launch("sumsq_final_kernel");
 }
@@ -269,16 +283,17 @@ mpo_status table_sumsq(mpo_dtype gdt, const mpo_tensor* t, int nt, const float* 
 // ---- dispatch to the per-format translation units ----
 #define MPO_FORMATS(X) X(MPO_FP16) X(MPO_BF16) X(MPO_FP16_RTZ) X(MPO_BF16_RTZ) X(MPO_FP16_SR) X(MPO_FP16_X8) X(MPO_BF16_X8)
 
-mpo_status dispatch_sgd(int vdt, int gdt, const mpo_tensor* t, int nt, const HP<SgdK>& k, bool one_hp, cudaStream_t s) {
-#define X(F) if (vdt == F) return FormatOps<F>::sgd(gdt, t, nt, k, one_hp, s);
+mpo_status dispatch_sgd(int vdt, int gdt, const mpo_tensor* t, int nt, const HP<SgdK>& k, bool one_hp,
+                        const double* sumsq, int skip, cudaStream_t s) {
+#define X(F) if (vdt == F) return FormatOps<F>::sgd(gdt, t, nt, k, one_hp, sumsq, skip, s);
     MPO_FORMATS(X)
 #undef X
     return fail(MPO_EDTYPE, "unsupported storage format");
 }
 
 mpo_status dispatch_adam(int vdt, int gdt, const mpo_tensor* t, int nt, const HP<AdamK>& k, bool one_hp,
-                         const double* sumsq, double max_norm, cudaStream_t s) {
-#define X(F) if (vdt == F) return FormatOps<F>::adam(gdt, t, nt, k, one_hp, sumsq, max_norm, s);
+                         const double* sumsq, double max_norm, int skip, cudaStream_t s) {
+#define X(F) if (vdt == F) return FormatOps<F>::adam(gdt, t, nt, k, one_hp, sumsq, max_norm, skip, s);
     MPO_FORMATS(X)
 #undef X
     return fail(MPO_EDTYPE, "unsupported storage format");
@@ -325,7 +340,7 @@ MPO_API int32_t mpo_build_exact(void) { return 0; }
 
 MPO_API int64_t mpo_launch_count(void) { return g_launches.load(); }
 
-MPO_API int64_t mpo_norm_ws_doubles(void) { return 1 + kNormBlocksMax; }
+MPO_API int64_t mpo_norm_ws_doubles(void) { return 2 + kNormBlocksMax; }
 
 MPO_API mpo_status mpo_selfcheck_fastmath(int64_t pairs, uint64_t seed, unsigned long long* counts,
                                           mpo_stream stream) {
@@ -367,34 +382,53 @@ MPO_API mpo_status mpo_reconstruct(mpo_dtype vdt, const void* value, const void*
     return dispatch_reconstruct(vdt, value, resid, w, n, static_cast<cudaStream_t>(stream));
 }
 
+// The norm pre-pass of a call when clipping or the found-inf skip needs it.
+static mpo_status prepass(mpo_dtype gdt, const mpo_tensor* t, int32_t nt, const float* gs, int32_t nhp,
+                          double* norm_ws, cudaStream_t s, double* accum = nullptr) {
+    if (!norm_ws) return fail(MPO_EINVAL, "clipping / skip_nonfinite need a norm workspace");
+    return table_sumsq(gdt, t, nt, gs, nhp, norm_ws, s, accum);
+}
+
+static mpo_status sgd_common(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t, int32_t nt, const mpo_sgd_hp* hp,
+                             int32_t nhp, double* norm_ws, bool one_hp, cudaStream_t s, bool sumsq_ready,
+                             double* accum = nullptr) {
+    HP<SgdK> k;
+    for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) k.g[i] = derive_sgd(hp[i < nhp ? i : 0]);
+    const int skip = hp[0].skip_nonfinite != 0;
+    if (skip && !sumsq_ready) {
+        float gs[MPO_MAX_HP_GROUPS];
+        for (int i = 0; i < nhp; ++i) gs[i] = k.g[i].gs;
+        mpo_status st = prepass(gdt, t, nt, gs, nhp, norm_ws, s, accum);
+        if (st != MPO_OK) return st;
+    }
+    return dispatch_sgd(vdt, gdt, t, nt, k, one_hp, skip ? norm_ws : nullptr, skip, s);
+}
+
 MPO_API mpo_status mpo_sgd_step(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t, int32_t nt, const mpo_sgd_hp* hp,
-                                int32_t nhp, mpo_stream stream) {
+                                int32_t nhp, double* norm_ws, mpo_stream stream) {
     g_err.clear();
     mpo_status st;
     if ((st = check_dtypes(vdt, gdt)) != MPO_OK) return st;
     if ((st = check_sgd_hp(hp, nhp)) != MPO_OK) return st;
     if ((st = check_table(t, nt, nhp, false, hp)) != MPO_OK) return st;
-    HP<SgdK> k;
-    for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) k.g[i] = derive_sgd(hp[i < nhp ? i : 0]);
-    return dispatch_sgd(vdt, gdt, t, nt, k, false, static_cast<cudaStream_t>(stream));
+    return sgd_common(vdt, gdt, t, nt, hp, nhp, norm_ws, false, static_cast<cudaStream_t>(stream), false);
 }
 
 static mpo_status adam_common(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t, int32_t nt, const mpo_adam_hp* hp,
-                              int32_t nhp, double* norm_ws, bool one_hp, cudaStream_t s, bool sumsq_ready) {
+                              int32_t nhp, double* norm_ws, bool one_hp, cudaStream_t s, bool sumsq_ready,
+                              double* accum = nullptr) {
     HP<AdamK> k;
     for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) k.g[i] = derive_adam(hp[i < nhp ? i : 0]);
     const double max_norm = hp[0].max_grad_norm;
-    if (max_norm > 0.0) {
-        if (!norm_ws) return fail(MPO_EINVAL, "clipping (max_grad_norm > 0) needs a norm workspace");
-        if (!sumsq_ready) {
-            float gs[MPO_MAX_HP_GROUPS];
-            for (int i = 0; i < nhp; ++i) gs[i] = k.g[i].gs;
-            mpo_status st = table_sumsq(gdt, t, nt, gs, nhp, norm_ws, s);
-            if (st != MPO_OK) return st;
-        }
-        return dispatch_adam(vdt, gdt, t, nt, k, one_hp, norm_ws, max_norm, s);
+    const int skip = hp[0].skip_nonfinite != 0;
+    const bool need = max_norm > 0.0 || skip;
+    if (need && !sumsq_ready) {
+        float gs[MPO_MAX_HP_GROUPS];
+        for (int i = 0; i < nhp; ++i) gs[i] = k.g[i].gs;
+        mpo_status st = prepass(gdt, t, nt, gs, nhp, norm_ws, s, accum);
+        if (st != MPO_OK) return st;
     }
-    return dispatch_adam(vdt, gdt, t, nt, k, one_hp, nullptr, 0.0, s);
+    return dispatch_adam(vdt, gdt, t, nt, k, one_hp, need ? norm_ws : nullptr, max_norm > 0.0 ? max_norm : 0.0, skip, s);
 }
 
 MPO_API mpo_status mpo_adam_step(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t, int32_t nt,
@@ -408,7 +442,7 @@ MPO_API mpo_status mpo_adam_step(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor*
 }
 
 MPO_API mpo_status mpo_fused_backward_hook_step(mpo_optim kind, mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* one,
-                                                const void* hp, mpo_stream stream) {
+                                                const void* hp, double* norm_ws, mpo_stream stream) {
     g_err.clear();
     mpo_status st;
     if (!one || !hp) return fail(MPO_EINVAL, "NULL tensor or hyper-parameters");
@@ -416,21 +450,20 @@ MPO_API mpo_status mpo_fused_backward_hook_step(mpo_optim kind, mpo_dtype vdt, m
     mpo_tensor x = *one;
     x.hp = 0;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    double* accum = norm_ws ? norm_ws + (1 + kNormBlocksMax) : nullptr;   // found-inf over the backward
     if (kind == MPO_ADAM) {
         const mpo_adam_hp* h = static_cast<const mpo_adam_hp*>(hp);
         if ((st = check_adam_hp(h, 1)) != MPO_OK) return st;
         if (h->max_grad_norm > 0.0)
             return fail(MPO_EINVAL, "global-norm clipping is impossible in the fused backward hook (P:93, P:186)");
         if ((st = check_table(&x, 1, 1, true, nullptr)) != MPO_OK) return st;
-        return adam_common(vdt, gdt, &x, 1, h, 1, nullptr, true, s, false);
+        return adam_common(vdt, gdt, &x, 1, h, 1, norm_ws, true, s, false, accum);
     }
     if (kind == MPO_SGD) {
         const mpo_sgd_hp* h = static_cast<const mpo_sgd_hp*>(hp);
         if ((st = check_sgd_hp(h, 1)) != MPO_OK) return st;
         if ((st = check_table(&x, 1, 1, false, h)) != MPO_OK) return st;
-        HP<SgdK> k;
-        for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) k.g[i] = derive_sgd(*h);
-        return dispatch_sgd(vdt, gdt, &x, 1, k, true, s);
+        return sgd_common(vdt, gdt, &x, 1, h, 1, norm_ws, true, s, false, accum);
     }
     return fail(MPO_EINVAL, "unknown optimizer kind");
 }
@@ -468,30 +501,35 @@ MPO_API mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t
         const mpo_adam_hp* h = static_cast<const mpo_adam_hp*>(hp);
         if ((st = check_adam_hp(h, 1)) != MPO_OK) return st;
         if ((st = check_table(&x, 1, 1, true, nullptr)) != MPO_OK) return st;
-        if (h->max_grad_norm > 0.0 && !norm_ws) return fail(MPO_EINVAL, "clipping needs a norm workspace");
+        if ((h->max_grad_norm > 0.0 || h->skip_nonfinite) && !norm_ws)
+            return fail(MPO_EINVAL, "clipping / skip_nonfinite need a norm workspace");
     } else {
         const mpo_sgd_hp* h = static_cast<const mpo_sgd_hp*>(hp);
         if ((st = check_sgd_hp(h, 1)) != MPO_OK) return st;
         if ((st = check_table(&x, 1, 1, false, h)) != MPO_OK) return st;
+        if (h->skip_nonfinite && !norm_ws) return fail(MPO_EINVAL, "skip_nonfinite needs a norm workspace");
     }
     // 1. reduce-scatter of the 16-bit gradients (sum), in place: shard `rank` of grad_flat
     //    (world 1: the reduction of one rank is the identity and the in-place shard is the buffer)
     if (world > 1)
         MPO_NCCL(ncclReduceScatter(grad_flat, const_cast<void*>(x.grad), size_t(shard), nccl_dtype(vdt), ncclSum, comm, s));
     // 2. residual-compensated update of this rank's shard
+    //    (clipping / found-inf: the shard's sum of squares, all-reduced so every rank agrees)
+    const bool need = kind == MPO_ADAM ? (static_cast<const mpo_adam_hp*>(hp)->max_grad_norm > 0.0 ||
+                                          static_cast<const mpo_adam_hp*>(hp)->skip_nonfinite != 0)
+                                       : static_cast<const mpo_sgd_hp*>(hp)->skip_nonfinite != 0;
+    if (need) {
+        const float gs = float(kind == MPO_ADAM ? static_cast<const mpo_adam_hp*>(hp)->grad_scale
+                                                : static_cast<const mpo_sgd_hp*>(hp)->grad_scale);
+        if ((st = prepass(gdt, &x, 1, &gs, 1, norm_ws, s)) != MPO_OK) return st;
+        if (world > 1) MPO_NCCL(ncclAllReduce(norm_ws, norm_ws, 1, ncclFloat64, ncclSum, comm, s));
+    }
     if (kind == MPO_ADAM) {
         const mpo_adam_hp* h = static_cast<const mpo_adam_hp*>(hp);
-        if (h->max_grad_norm > 0.0) {
-            float gs = float(h->grad_scale);
-            if ((st = table_sumsq(gdt, &x, 1, &gs, 1, norm_ws, s)) != MPO_OK) return st;
-            if (world > 1) MPO_NCCL(ncclAllReduce(norm_ws, norm_ws, 1, ncclFloat64, ncclSum, comm, s));
-        }
         if ((st = adam_common(vdt, gdt, &x, 1, h, 1, norm_ws, true, s, true)) != MPO_OK) return st;
     } else {
         const mpo_sgd_hp* h = static_cast<const mpo_sgd_hp*>(hp);
-        HP<SgdK> k;
-        for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) k.g[i] = derive_sgd(*h);
-        if ((st = dispatch_sgd(vdt, gdt, &x, 1, k, true, s)) != MPO_OK) return st;
+        if ((st = sgd_common(vdt, gdt, &x, 1, h, 1, norm_ws, true, s, true)) != MPO_OK) return st;
     }
     // 3. all-gather of the 16-bit values only (residual and state never move)
     if (world > 1) MPO_NCCL(ncclAllGather(x.value, value_flat, size_t(shard), nccl_dtype(vdt), comm, s));

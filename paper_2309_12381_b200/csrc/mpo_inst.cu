@@ -16,26 +16,27 @@ constexpr int kOther = B == kFP16 ? kBF16 : kFP16;
 
 template <class Op, bool CLIP>
 mpo_status step_for(int gdt, const mpo_tensor* t, int nt, const HP<typename Op::K>& hp, bool one_hp,
-                    const double* sumsq, double max_norm, cudaStream_t s) {
-    if (gdt == B) return launch_step<SF, B, Op, CLIP>(t, nt, hp, one_hp, sumsq, max_norm, s);
-    if (gdt == kFP32) return launch_step<SF, kFP32, Op, CLIP>(t, nt, hp, one_hp, sumsq, max_norm, s);
+                    const double* sumsq, double max_norm, int skip, cudaStream_t s) {
+    if (gdt == B) return launch_step<SF, B, Op, CLIP>(t, nt, hp, one_hp, sumsq, max_norm, skip, s);
+    if (gdt == kFP32) return launch_step<SF, kFP32, Op, CLIP>(t, nt, hp, one_hp, sumsq, max_norm, skip, s);
     if constexpr (kAllGrads) {
-        if (gdt == kOther) return launch_step<SF, kOther, Op, CLIP>(t, nt, hp, one_hp, sumsq, max_norm, s);
+        if (gdt == kOther) return launch_step<SF, kOther, Op, CLIP>(t, nt, hp, one_hp, sumsq, max_norm, skip, s);
     }
     return fail(MPO_EDTYPE, "unsupported gradient dtype for this storage format");
 }
 }  // namespace
 
 template <>
-mpo_status FormatOps<SF>::sgd(int gdt, const mpo_tensor* t, int nt, const HP<SgdK>& hp, bool one_hp, cudaStream_t s) {
-    return step_for<SgdOp, false>(gdt, t, nt, hp, one_hp, nullptr, 0.0, s);
+mpo_status FormatOps<SF>::sgd(int gdt, const mpo_tensor* t, int nt, const HP<SgdK>& hp, bool one_hp,
+                              const double* sumsq, int skip, cudaStream_t s) {
+    return step_for<SgdOp, false>(gdt, t, nt, hp, one_hp, sumsq, 0.0, skip, s);
 }
 
 template <>
 mpo_status FormatOps<SF>::adam(int gdt, const mpo_tensor* t, int nt, const HP<AdamK>& hp, bool one_hp,
-                               const double* sumsq, double max_norm, cudaStream_t s) {
-    if (max_norm > 0.0) return step_for<AdamOp, true>(gdt, t, nt, hp, one_hp, sumsq, max_norm, s);
-    return step_for<AdamOp, false>(gdt, t, nt, hp, one_hp, nullptr, 0.0, s);
+                               const double* sumsq, double max_norm, int skip, cudaStream_t s) {
+    if (max_norm > 0.0) return step_for<AdamOp, true>(gdt, t, nt, hp, one_hp, sumsq, max_norm, skip, s);
+    return step_for<AdamOp, false>(gdt, t, nt, hp, one_hp, sumsq, 0.0, skip, s);
 }
 
 template <>

@@ -427,12 +427,15 @@ __global__ void __launch_bounds__(kThreads) sumsq_kernel(const __grid_constant__
 
 // Sums nparts partials (fixed order) into out[0].
 __global__ void __launch_bounds__(kThreads) sumsq_final_kernel(const double* __restrict__ partial, int nparts,
-                                                               double* __restrict__ out) {
+                                                               double* __restrict__ out, double* __restrict__ accum) {
     __shared__ double sh[32];
     double acc = 0.0;
     for (int i = threadIdx.x; i < nparts; i += blockDim.x) acc += partial[i];
     acc = block_sum(acc, sh);
-    if (threadIdx.x == 0) out[0] = acc;
+    if (threadIdx.x == 0) {
+        out[0] = acc;
+        if (accum) accum[0] += acc;   // hook mode: found-inf over a whole backward
+    }
 }
 
 
@@ -482,9 +485,14 @@ __device__ __forceinline__ void process_unit(const uint4& hv, const ResidUnit<SF
     const uint32_t* h = &hv.x;
     float w[8], g[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        g[k] = grad_at<G>(gu, k) * c.gs;
-        if constexpr (CLIP) g[k] = g[k] * coef;
+    for (int k = 0; k < 8; ++k) g[k] = grad_at<G>(gu, k) * c.gs;
+    if (c.clip_on) {   // uniform per tensor
+#pragma unroll
+        for (int k = 0; k < 8; ++k) g[k] = clamp_grad(g[k], c.clipv);
+    }
+    if constexpr (CLIP) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) g[k] = g[k] * coef;
     }
     const uint32_t special = nonfinite_pair<FM::base>(h[0]) | nonfinite_pair<FM::base>(h[1]) |
                              nonfinite_pair<FM::base>(h[2]) | nonfinite_pair<FM::base>(h[3]);
@@ -532,6 +540,7 @@ __device__ __noinline__ void process_tail(const KT T, int64_t lo, int64_t hi, co
     const bool need_m = Op::reads_m(c), has_m = Op::writes_m(c);
     for (int64_t i = lo; i < hi; ++i) {
         float g = grad_scalar<G>(T.grad, i) * c.gs;
+        if (c.clip_on) g = clamp_grad(g, c.clipv);
         if constexpr (CLIP) g = g * coef;
         int32_t code;
         if constexpr (FM::rbytes == 1) code = static_cast<const int8_t*>(T.resid)[i];
@@ -571,8 +580,10 @@ __device__ __forceinline__ void store_unit(const KT& T, int64_t e, const uint4& 
 template <int MAXT, int SF, int G, class Op, bool CLIP>
 __global__ void __launch_bounds__(kThreads) step_kernel(const __grid_constant__ Table<MAXT> tab,
                                                         const __grid_constant__ HP<typename Op::K> hp,
-                                                        const double* __restrict__ sumsq, double max_norm) {
+                                                        const double* __restrict__ sumsq, double max_norm,
+                                                        int skip) {
     using K = typename Op::K;
+    if (skip && !isfinite(sumsq[0])) return;   // loss-scaling found-inf: no update at all
     float coef = 1.0f;
     if constexpr (CLIP) coef = clip_coef(sumsq, max_norm);
     int cur = 0;
@@ -706,8 +717,9 @@ template <int MAXT, int SF, int G, class Op, bool CLIP>
 __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(const __grid_constant__ Table<MAXT> tab,
                                                                   const __grid_constant__ HP<typename Op::K> hp,
                                                                   const double* __restrict__ sumsq, double max_norm,
-                                                                  int stages) {
+                                                                  int stages, int skip) {
     using K = typename Op::K;
+    if (skip && !isfinite(sumsq[0])) return;   // loss-scaling found-inf: no update, nothing written
     constexpr int GB = GradBytes<G>::v;
     constexpr int RB = Fmt<SF>::rbytes;
     constexpr int64_t TE = kTileEl;
@@ -953,7 +965,7 @@ constexpr int kSmemBudget = (MPO_CTAS_PER_SM == 1 ? 227 * 1024 : (228 * 1024) / 
 
 template <int MAXT, int SF, int G, class Op, bool CLIP>
 mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typename Op::K>& hp, bool one_hp,
-                             const double* sumsq, double max_norm, cudaStream_t s) {
+                             const double* sumsq, double max_norm, int skip, cudaStream_t s) {
     Table<MAXT> tab;
     const int64_t tiles = fill_table(tab, t, lo, hi, one_hp);
     if (tiles == 0) return MPO_OK;
@@ -963,7 +975,7 @@ mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typen
         auto kern = step_kernel<MAXT, SF, G, Op, CLIP>;
         static int per_sm = resident_blocks(kern);
         const int64_t grid = grid_for(tiles, per_sm);
-        kern<<<unsigned(grid), kThreads, 0, s>>>(tab, hp, sumsq, max_norm);
+        kern<<<unsigned(grid), kThreads, 0, s>>>(tab, hp, sumsq, max_norm, skip);
         ++g_launches;
         return check_launch("step_kernel");
     }
@@ -976,20 +988,21 @@ mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typen
     static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (attr != cudaSuccess) return fail(MPO_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr));
     const int64_t grid = grid_for(tiles, MPO_CTAS_PER_SM);
-    kern<<<unsigned(grid), kTmaThreads, smem, s>>>(tab, hp, sumsq, max_norm, stages);
+    kern<<<unsigned(grid), kTmaThreads, smem, s>>>(tab, hp, sumsq, max_norm, stages, skip);
     ++g_launches;
     return check_launch("step_tma_kernel");
 }
 
 template <int SF, int G, class Op, bool CLIP>
 mpo_status launch_step(const mpo_tensor* t, int nt, const HP<typename Op::K>& hp, bool one_hp, const double* sumsq,
-                       double max_norm, cudaStream_t s) {
+                       double max_norm, int skip, cudaStream_t s) {
     for (int lo = 0; lo < nt; lo += kBigT) {
         const int hi = lo + kBigT < nt ? lo + kBigT : nt;
         mpo_status st;
-        if (hi - lo == 1) st = launch_step_slice<1, SF, G, Op, CLIP>(t, lo, hi, hp, one_hp, sumsq, max_norm, s);
-        else if (hi - lo <= kMidT) st = launch_step_slice<kMidT, SF, G, Op, CLIP>(t, lo, hi, hp, one_hp, sumsq, max_norm, s);
-        else st = launch_step_slice<kBigT, SF, G, Op, CLIP>(t, lo, hi, hp, one_hp, sumsq, max_norm, s);
+        if (hi - lo == 1) st = launch_step_slice<1, SF, G, Op, CLIP>(t, lo, hi, hp, one_hp, sumsq, max_norm, skip, s);
+        else if (hi - lo <= kMidT)
+            st = launch_step_slice<kMidT, SF, G, Op, CLIP>(t, lo, hi, hp, one_hp, sumsq, max_norm, skip, s);
+        else st = launch_step_slice<kBigT, SF, G, Op, CLIP>(t, lo, hi, hp, one_hp, sumsq, max_norm, skip, s);
         if (st != MPO_OK) return st;
     }
     return MPO_OK;
@@ -998,9 +1011,10 @@ mpo_status launch_step(const mpo_tensor* t, int nt, const HP<typename Op::K>& hp
 // Entry points of one storage format, defined in mpo_inst.cu (compiled once per format).
 template <int SF>
 struct FormatOps {
-    static mpo_status sgd(int gdt, const mpo_tensor* t, int nt, const HP<SgdK>& hp, bool one_hp, cudaStream_t s);
+    static mpo_status sgd(int gdt, const mpo_tensor* t, int nt, const HP<SgdK>& hp, bool one_hp, const double* sumsq,
+                          int skip, cudaStream_t s);
     static mpo_status adam(int gdt, const mpo_tensor* t, int nt, const HP<AdamK>& hp, bool one_hp, const double* sumsq,
-                           double max_norm, cudaStream_t s);
+                           double max_norm, int skip, cudaStream_t s);
     static mpo_status split(const float* w, void* value, void* resid, int64_t n, uint64_t seed, uint32_t stream,
                             cudaStream_t s);
     static mpo_status reconstruct(const void* value, const void* resid, float* w, int64_t n, cudaStream_t s);

@@ -29,11 +29,13 @@ class _ResidualOptimizer(torch.optim.Optimizer):
     _kind = None
 
     def __init__(self, params, defaults, fmt: Optional[torch.dtype], exact: bool, scheme: str = "rne",
-                 seed: int = 0):
+                 seed: int = 0, clip_value: float = 0.0, skip_nonfinite: bool = False):
         super().__init__(params, defaults)
         self.exact = exact
         self.scheme = scheme
         self.seed = int(seed)
+        self.clip_value = float(clip_value or 0.0)
+        self.skip_nonfinite = bool(skip_nonfinite)
         self._hooks = []
         self._tables = {}
         self._norm_ws = None
@@ -154,8 +156,28 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         row.grad = g.data_ptr()
         hp = self._hp(self.param_groups[st["group"]], st["step"]).c()
         api.mpo_fused_backward_hook_step(self._kind, api.format_code(p.dtype, self.scheme), api.dtype_code(g.dtype),
-                                         row, hp, exact=self.exact)
+                                         row, hp, exact=self.exact,
+                                         norm_ws=self._ws(p.device) if self.skip_nonfinite else None)
         p.grad = None   # freed now; stream order makes the block's reuse safe
+
+    # -- loss scaling: found-inf -------------------------------------------------------------
+    def _ws(self, device):
+        if self._norm_ws is None:
+            self._norm_ws = torch.zeros(api.norm_ws_doubles(self.exact), dtype=torch.float64, device=device)
+        return self._norm_ws
+
+    def found_inf(self, reset: bool = True) -> bool:
+        """skip_nonfinite: whether a non-finite scaled gradient was seen -- by the last step() (which
+        then updated nothing), or by any hook of the backward passes since the last reset (hook
+        mode skips only the offending parameters).  Synchronises with the device."""
+        if self._norm_ws is None:
+            return False
+        ws = self._norm_ws
+        bad = not bool(torch.isfinite(ws[0]).item()) or not bool(torch.isfinite(ws[-1]).item())
+        if reset:
+            ws[0] = 0.0
+            ws[-1] = 0.0
+        return bad
 
     def _check_hook_mode(self):
         pass
@@ -174,10 +196,11 @@ class ResidualSGD(_ResidualOptimizer):
 
     def __init__(self, params: Iterable, lr: float, momentum: float = 0.0, dampening: float = 0.0,
                  weight_decay: float = 0.0, nesterov: bool = False, grad_scale: float = 1.0,
-                 fmt: Optional[torch.dtype] = None, exact: bool = False, scheme: str = "rne", seed: int = 0):
+                 fmt: Optional[torch.dtype] = None, exact: bool = False, scheme: str = "rne", seed: int = 0,
+                 clip_value: float = 0.0, skip_nonfinite: bool = False):
         defaults = dict(lr=lr, momentum=momentum, dampening=dampening, weight_decay=weight_decay,
                         nesterov=nesterov, grad_scale=grad_scale)
-        super().__init__(params, defaults, fmt, exact, scheme, seed)
+        super().__init__(params, defaults, fmt, exact, scheme, seed, clip_value, skip_nonfinite)
 
     def _init_state(self, p, st):
         group = next(g for g in self.param_groups if any(q is p for q in g["params"]))  # noqa
@@ -187,10 +210,12 @@ class ResidualSGD(_ResidualOptimizer):
     def _hp(self, g, step):
         return api.SgdParams(lr=g["lr"], momentum=g["momentum"], dampening=g["dampening"],
                              weight_decay=g["weight_decay"], grad_scale=g["grad_scale"], nesterov=g["nesterov"],
-                             first_step=(step == 1), seed=api.step_seed(self.seed, step))
+                             first_step=(step == 1), seed=api.step_seed(self.seed, step),
+                             clip_value=self.clip_value, skip_nonfinite=self.skip_nonfinite)
 
     def _launch(self, tab, hps):
-        api.mpo_sgd_step(tab, hps, exact=self.exact)
+        ws = self._ws(tab.values[0].device) if self.skip_nonfinite else None
+        api.mpo_sgd_step(tab, hps, norm_ws=ws, exact=self.exact)
 
 
 class ResidualAdamW(_ResidualOptimizer):
@@ -201,11 +226,11 @@ class ResidualAdamW(_ResidualOptimizer):
     def __init__(self, params: Iterable, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
                  weight_decay: float = 0.0, adamw: bool = True, grad_scale: float = 1.0,
                  max_grad_norm: Optional[float] = None, fmt: Optional[torch.dtype] = None, exact: bool = False,
-                 scheme: str = "rne", seed: int = 0):
+                 scheme: str = "rne", seed: int = 0, clip_value: float = 0.0, skip_nonfinite: bool = False):
         defaults = dict(lr=lr, betas=tuple(betas), eps=eps, weight_decay=weight_decay, adamw=adamw,
                         grad_scale=grad_scale)
         self.max_grad_norm = float(max_grad_norm) if max_grad_norm else 0.0
-        super().__init__(params, defaults, fmt, exact, scheme, seed)
+        super().__init__(params, defaults, fmt, exact, scheme, seed, clip_value, skip_nonfinite)
 
     def _init_state(self, p, st):
         st["m"] = torch.zeros(p.shape, dtype=torch.float32, device=p.device)
@@ -220,15 +245,11 @@ class ResidualAdamW(_ResidualOptimizer):
         b1, b2 = g["betas"]
         return api.AdamParams(lr=g["lr"], beta1=b1, beta2=b2, eps=g["eps"], weight_decay=g["weight_decay"],
                               grad_scale=g["grad_scale"], max_grad_norm=self.max_grad_norm, adamw=g["adamw"],
-                              step=step, seed=api.step_seed(self.seed, step))
+                              step=step, seed=api.step_seed(self.seed, step), clip_value=self.clip_value,
+                              skip_nonfinite=self.skip_nonfinite)
 
     def _launch(self, tab, hps):
-        ws = None
-        if self.max_grad_norm > 0:
-            if self._norm_ws is None:
-                dev = tab.values[0].device
-                self._norm_ws = torch.zeros(api.norm_ws_doubles(self.exact), dtype=torch.float64, device=dev)
-            ws = self._norm_ws
+        ws = self._ws(tab.values[0].device) if (self.max_grad_norm > 0 or self.skip_nonfinite) else None
         api.mpo_adam_step(tab, hps, norm_ws=ws, exact=self.exact)
 
     def last_grad_sumsq(self) -> Optional[torch.Tensor]:

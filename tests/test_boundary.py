@@ -105,7 +105,7 @@ def test_validation_errors(libs):
     assert L.mpo_adam_step(_lib.MPO_BF16, _lib.MPO_BF16, tab, 2, C.byref(hp), 0, None, None) == _lib.MPO_EINVAL
     # SGD: nesterov without momentum
     s = S(0.1, 0.0, 0.0, 0.0, 1.0, 1, 0, 0)
-    rc, msg = _status(L, L.mpo_sgd_step(_lib.MPO_FP16, _lib.MPO_FP16, tab, 2, C.byref(s), 1, None))
+    rc, msg = _status(L, L.mpo_sgd_step(_lib.MPO_FP16, _lib.MPO_FP16, tab, 2, C.byref(s), 1, None, None))
     assert rc == _lib.MPO_EINVAL and "nesterov" in msg
 
 
@@ -115,10 +115,19 @@ def test_hook_refuses_global_clipping(libs):
     one = _lib.Tensor(16, 32, 48, 64, 80, 8, 0, 0)
     clip = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 1.0, 1, 0, 1, 0)
     rc, msg = _status(L, L.mpo_fused_backward_hook_step(_lib.MPO_ADAM, _lib.MPO_BF16, _lib.MPO_BF16, C.byref(one),
-                                                        C.byref(clip), None))
+                                                        C.byref(clip), None, None))
     assert rc == _lib.MPO_EINVAL and "P:186" in msg
     assert L.mpo_fused_backward_hook_step(9, _lib.MPO_BF16, _lib.MPO_BF16, C.byref(one), C.byref(clip),
-                                          None) == _lib.MPO_EINVAL
+                                          None, None) == _lib.MPO_EINVAL
+    # the found-inf skip needs a workspace; clip_value and max_grad_norm are exclusive
+    skip = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1, 0, 0.0, 1, 0)
+    rc, msg = _status(L, L.mpo_fused_backward_hook_step(_lib.MPO_ADAM, _lib.MPO_BF16, _lib.MPO_BF16, C.byref(one),
+                                                        C.byref(skip), None, None))
+    assert rc == _lib.MPO_EINVAL and "workspace" in msg
+    both = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 1.0, 1, 0, 1, 0, 0.5, 0, 0)
+    tab = (_lib.Tensor * 1)(one)
+    rc, msg = _status(L, L.mpo_adam_step(_lib.MPO_BF16, _lib.MPO_BF16, tab, 1, C.byref(both), 1, None, None))
+    assert rc == _lib.MPO_EINVAL and "exclusive" in msg
 
 
 def test_sharded_validation(libs):

@@ -206,3 +206,90 @@ def test_sharded_world1_equals_unsharded(mpo, nccl1, kind, clip):
         sh.step()
     for a, b in zip(pa, pb):
         assert torch.equal(a.data.view(torch.int16), b.data.view(torch.int16))
+
+
+# ---------------------------------------------------------------------------------------------
+# Gradient surgery through the optimizer: clip-by-value, loss-scale found-inf
+# ---------------------------------------------------------------------------------------------
+def test_clip_value_multi_tensor_and_hook_match_oracle(mpo, orc):
+    """clip_value fused into the step: multi-tensor (exact build) == oracle bitwise; hook mode ==
+    multi-tensor bitwise."""
+    from gpu_util import dev16
+    fmt = "bf16"
+    sizes = [4096 + 40, 333, 8192]
+    for kind in ("adam", "sgd"):
+        hs, rs, gs = [], [], []
+        for i, n in enumerate(sizes):
+            h, r = orc.split(fmt, synth.weights(n, 0.02, 40 + i))
+            hs.append(h); rs.append(r); gs.append(synth.grads(n, 5e-2, fmt, 41, i))
+        V = [dev16(h, fmt) for h in hs]
+        R = [torch.from_numpy(r.copy()).cuda() for r in rs]
+        G = [dev16(g, fmt) for g in gs]
+        M = [torch.zeros(n, device="cuda") for n in sizes]
+        W = [torch.zeros(n, device="cuda") for n in sizes]
+        if kind == "adam":
+            hp = mpo.AdamParams(lr=1e-3, weight_decay=0.1, step=1, clip_value=0.03, grad_scale=0.5)
+            mpo.mpo_adam_step(mpo.TensorTable(V, R, G, M, W), hp, exact=True)
+        else:
+            hp = mpo.SgdParams(lr=0.1, momentum=0.9, first_step=True, clip_value=0.03, grad_scale=0.5)
+            mpo.mpo_sgd_step(mpo.TensorTable(V, R, G, M, [None] * 3), hp, exact=True)
+        for i, n in enumerate(sizes):
+            m = np.zeros(n, np.float32); v = np.zeros(n, np.float32)
+            if kind == "adam":
+                orc.adam_step(fmt, fmt, hs[i], rs[i], gs[i], m, v, lr=1e-3, weight_decay=0.1, grad_scale=0.5,
+                              clip_value=0.03)
+            else:
+                orc.sgd_step(fmt, fmt, hs[i], rs[i], gs[i], m, lr=0.1, momentum=0.9, first_step=True,
+                             grad_scale=0.5, clip_value=0.03)
+            assert np.array_equal(host16(V[i]), hs[i]) and np.array_equal(R[i].cpu().numpy(), rs[i])
+    # hook mode == multi-tensor with clip_value
+    a, b, oa, ob = _pair(torch.bfloat16, "adam", mpo, lr=1e-3, clip_value=1e-3)
+    ob.install_backward_hooks()
+    idx = torch.randint(0, 257, (4, 33), device="cuda")
+    _loss(a, idx).backward(); oa.step()
+    _loss(b, idx).backward()
+    for pa, pb in zip(a.parameters(), b.parameters()):
+        assert torch.equal(pa.view(torch.int16), pb.view(torch.int16))
+
+
+def test_skip_nonfinite_multi_tensor(mpo):
+    """Loss-scaling found-inf: one Inf anywhere in the table -> nothing updated (value, residual,
+    m, v bit-identical); finite grads -> a normal step; the optimizer reports it."""
+    torch.manual_seed(5)
+    ps = [torch.nn.Parameter(torch.randn(n, device="cuda") * 0.02) for n in (5000, 77, 4096)]
+    for kind in ("adam", "sgd"):
+        qs = [torch.nn.Parameter(p.detach().clone()) for p in ps]
+        opt = (mpo.ResidualAdamW(qs, lr=1e-3, fmt=torch.float16, skip_nonfinite=True, grad_scale=1 / 1024)
+               if kind == "adam" else
+               mpo.ResidualSGD(qs, lr=0.1, momentum=0.9, fmt=torch.float16, skip_nonfinite=True))
+        for q in qs:
+            q.grad = torch.randn_like(q) * 1e-2
+        qs[1].grad[3] = float("inf")
+        before = [(q.detach().clone(), opt.state[q]["resid"].clone()) for q in qs]
+        opt.step()
+        assert opt.found_inf()
+        for q, (v0, r0) in zip(qs, before):
+            assert torch.equal(q.view(torch.int16), v0.view(torch.int16)) and torch.equal(opt.state[q]["resid"], r0)
+            if opt.state[q].get("m") is not None:
+                assert not opt.state[q]["m"].any()
+        qs[1].grad[3] = 0.0
+        opt.step()
+        assert not opt.found_inf()
+        assert any(not torch.equal(q.view(torch.int16), v0.view(torch.int16)) for q, (v0, _) in zip(qs, before))
+
+
+def test_skip_nonfinite_hook_mode_per_parameter(mpo):
+    """Hook mode can only skip the offending parameter; found_inf() reports it."""
+    torch.manual_seed(6)
+    d = 64
+    model = nn.Sequential(nn.Linear(d, d), nn.Linear(d, d)).cuda()
+    opt = mpo.ResidualAdamW(model.parameters(), lr=1e-3, fmt=torch.float16, skip_nonfinite=True)
+    opt.install_backward_hooks()
+    w0 = [p.detach().clone() for p in model.parameters()]
+    x = torch.randn(8, d, device="cuda", dtype=torch.float16)
+    model[0].weight.register_hook(lambda g: g.index_fill(0, torch.tensor([0], device=g.device), float("inf")))
+    model(x).float().sum().backward()
+    assert opt.found_inf()
+    changed = [not torch.equal(p.view(torch.int16), w.view(torch.int16)) for p, w in zip(model.parameters(), w0)]
+    assert changed == [False, True, True, True]     # only layer 0's weight skipped
+    assert not opt.found_inf()                       # reset
