@@ -144,3 +144,169 @@ class ShardedResidualOptimizer:
         b += 0 if self.m is None else self.m.numel() * 4
         b += 0 if self.v is None else self.v.numel() * 4
         return b
+
+
+# ---------------------------------------------------------------------------------------------
+# Hook mode x sharding: bucketed reduce-scatter issued from the
+# post-accumulate-grad hooks, each bucket's residual-compensated step on this rank's part, and the
+# all-gather of its 16-bit values -- overlapped with the rest of backward on a side stream.
+# ---------------------------------------------------------------------------------------------
+@dataclass
+class BucketLayout:
+    """Parameters grouped into buckets in backward order (last parameter first); every bucket is
+    padded to a multiple of 16*world elements and split into `world` equal contiguous parts, part
+    r owned by rank r.  Flat buffers hold the buckets back to back; the rank's state shard is the
+    concatenation of its parts."""
+    sizes: List[int]
+    world: int
+    bucket_elems: int = 1 << 22
+
+    def __post_init__(self):
+        if self.world < 1:
+            raise ValueError("world must be >= 1")
+        # 16 elements: every bucket part is 16-byte aligned even for the int8 residual formats
+        q = 2 * ALIGN * self.world
+        order = list(range(len(self.sizes)))[::-1]          # autograd produces grads roughly in reverse
+        self.buckets = []                                    # [(offset, length, [param indices])]
+        self.offsets = [0] * len(self.sizes)
+        self.bucket_of = [0] * len(self.sizes)
+        o = 0
+        cur, used = [], 0
+        for i in order:
+            cur.append(i)
+            self.offsets[i] = o + used
+            used += (self.sizes[i] + ALIGN - 1) // ALIGN * ALIGN
+            if used >= self.bucket_elems:
+                length = (used + q - 1) // q * q
+                self.buckets.append((o, length, cur))
+                o += length
+                cur, used = [], 0
+        if cur:
+            length = (used + q - 1) // q * q
+            self.buckets.append((o, length, cur))
+            o += length
+        for b, (_, _, idx) in enumerate(self.buckets):
+            for i in idx:
+                self.bucket_of[i] = b
+        self.total = o
+        self.shard = o // self.world
+        # where each bucket's part of this rank starts inside the rank's shard buffers
+        self.part_offsets = []
+        p = 0
+        for _, length, _ in self.buckets:
+            self.part_offsets.append(p)
+            p += length // self.world
+
+    def views(self, flat: torch.Tensor, shapes: Sequence[torch.Size]):
+        return [flat[o:o + n].view(s) for o, n, s in zip(self.offsets, self.sizes, shapes)]
+
+    def global_range_of_part(self, b: int, rank: int):
+        o, length, _ = self.buckets[b]
+        k = length // self.world
+        return o + rank * k, o + (rank + 1) * k
+
+
+class BucketedShardedOptimizer:
+    """Sharded residual Adam/AdamW or SGD-momentum stepped inside backward, bucket by bucket.
+
+    Parameters are re-pointed at views of one flat value buffer and their .grad at views of one
+    flat gradient buffer (zeroed after each bucket's reduce-scatter, ready for the next backward).
+    When the last gradient of a bucket has been accumulated, its hook records an event on the
+    backward's stream and the bucket's ``mpo_sharded_step`` (NCCL reduce-scatter -> update of this
+    rank's part -> NCCL all-gather of the 16-bit values) runs on a side stream, overlapping the
+    rest of backward.  ``wait()`` (called by the next forward or explicitly) joins the side stream.
+    Global-norm clipping is impossible here; the per-bucket found-inf skip is available."""
+
+    def __init__(self, params, kind: str = "adam", fmt: Optional[torch.dtype] = None, group=None, hp=None,
+                 bucket_elems: int = 1 << 22, exact: bool = False, comm_ptr: Optional[int] = None,
+                 scheme: str = "rne", seed: int = 0):
+        import torch.distributed as dist
+        self.params = [p for p in params]
+        if not self.params:
+            raise MpoError(1, "no parameters")
+        self.kind = MPO_ADAM if kind == "adam" else MPO_SGD
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.exact, self.scheme, self.seed = exact, scheme, int(seed)
+        dev = self.params[0].device
+        vdt = fmt if self.params[0].dtype == torch.float32 else self.params[0].dtype
+        if vdt not in (torch.float16, torch.bfloat16):
+            raise MpoError(3, "fmt must be torch.float16 or torch.bfloat16")
+        self.layout = L = BucketLayout([p.numel() for p in self.params], self.world, bucket_elems)
+        src = torch.zeros(L.total, dtype=torch.float32, device=dev)
+        for p, o in zip(self.params, L.offsets):
+            src[o:o + p.numel()].copy_(p.data.reshape(-1).float())
+        value, resid_full = api.mpo_split(src, vdt, exact=exact, scheme=scheme, seed=api.step_seed(self.seed, 0),
+                                          sr_stream=0)
+        del src
+        self.value = value
+        self.resid = torch.empty(L.shard, dtype=resid_full.dtype, device=dev)
+        for b in range(len(L.buckets)):
+            lo, hi = L.global_range_of_part(b, self.rank)
+            po = L.part_offsets[b]
+            self.resid[po:po + hi - lo].copy_(resid_full[lo:hi])
+        del resid_full
+        self.grad = torch.zeros(L.total, dtype=vdt, device=dev)
+        if hp is None:
+            hp = api.AdamParams(lr=1e-3) if self.kind == MPO_ADAM else api.SgdParams(lr=1e-2)
+        if getattr(hp, "max_grad_norm", 0.0) > 0:
+            raise MpoError(1, "global-norm clipping needs every gradient at once: impossible in the fused "
+                              "backward (P:93, P:186)")
+        self.hp = hp
+        need_m = self.kind == MPO_ADAM or getattr(hp, "momentum", 0.0) != 0.0
+        self.m = torch.zeros(L.shard, dtype=torch.float32, device=dev) if need_m else None
+        self.v = torch.zeros(L.shard, dtype=torch.float32, device=dev) if self.kind == MPO_ADAM else None
+        self.norm_ws = torch.zeros(api.norm_ws_doubles(exact), dtype=torch.float64, device=dev)
+        shapes = [p.shape for p in self.params]
+        for p, vv, gg in zip(self.params, L.views(self.value, shapes), L.views(self.grad, shapes)):
+            p.data = vv
+            p.grad = gg
+        self.comm = comm_ptr if comm_ptr is not None else nccl_comm_ptr(group)
+        self.side = torch.cuda.Stream(device=dev)
+        self.step_count = 0
+        self._pending = [len(idx) for _, _, idx in L.buckets]
+        self._handles = [p.register_post_accumulate_grad_hook(self._make_hook(i)) for i, p in enumerate(self.params)]
+
+    def _make_hook(self, i):
+        def hook(p):
+            b = self.layout.bucket_of[i]
+            self._pending[b] -= 1
+            if self._pending[b] == 0:
+                self._launch_bucket(b)
+        return hook
+
+    def _launch_bucket(self, b):
+        L = self.layout
+        if self._pending.count(0) == 1:        # first bucket of this backward: a new step
+            self.step_count += 1
+        o, length, _ = L.buckets[b]
+        po = L.part_offsets[b]
+        k = length // self.world
+        hp = self.hp
+        if self.kind == MPO_ADAM:
+            hp.step = self.step_count
+        else:
+            hp.first_step = self.step_count == 1
+        hp.seed = api.step_seed(self.seed, self.step_count)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.side.wait_event(ev)
+        with torch.cuda.stream(self.side):
+            api.mpo_sharded_step(self.kind, self.comm, self.rank, self.world, self.value[o:o + length],
+                                 self.grad[o:o + length], self.resid[po:po + k],
+                                 None if self.m is None else self.m[po:po + k],
+                                 None if self.v is None else self.v[po:po + k], hp,
+                                 norm_ws=self.norm_ws if getattr(hp, "skip_nonfinite", False) else None,
+                                 exact=self.exact, scheme=self.scheme, stream=self.side)
+            self.grad[o:o + length].zero_()       # ready for the next backward's accumulation
+        if all(x == 0 for x in self._pending):  # backward done: re-arm the bucket counters
+            self._pending = [len(idx) for _, _, idx in L.buckets]
+
+    def wait(self):
+        """Make the current stream wait for every bucket step issued so far."""
+        torch.cuda.current_stream().wait_stream(self.side)
+
+    def remove_hooks(self):
+        for h in self._handles:
+            h.remove()
+        self._handles = []

@@ -293,3 +293,30 @@ def test_skip_nonfinite_hook_mode_per_parameter(mpo):
     changed = [not torch.equal(p.view(torch.int16), w.view(torch.int16)) for p, w in zip(model.parameters(), w0)]
     assert changed == [False, True, True, True]     # only layer 0's weight skipped
     assert not opt.found_inf()                       # reset
+
+
+@pytest.mark.parametrize("kind", ["adam", "sgd"])
+def test_bucketed_hook_sharding_equals_two_phase(mpo, nccl1, kind):
+    """Hook mode x sharding: bucket steps issued from the hooks on a side stream
+    == the two-phase sharded step, bitwise (world 1)."""
+    torch.manual_seed(11)
+    mk = lambda: nn.Sequential(nn.Linear(48, 96), nn.GELU(), nn.Linear(96, 48), nn.Linear(48, 10)).cuda()
+    a, b = mk(), mk()
+    b.load_state_dict(a.state_dict())
+    hp = (lambda: mpo.AdamParams(lr=1e-3, weight_decay=0.1)) if kind == "adam" else \
+        (lambda: mpo.SgdParams(lr=0.05, momentum=0.9))
+    ref = mpo.ShardedResidualOptimizer(list(a.parameters()), kind=kind, fmt=torch.bfloat16, hp=hp())
+    bk = mpo.BucketedShardedOptimizer(list(b.parameters()), kind=kind, fmt=torch.bfloat16, hp=hp(), bucket_elems=2048)
+    assert len(bk.layout.buckets) > 1
+    for t in range(3):
+        x = torch.randn(16, 48, device="cuda", dtype=torch.bfloat16)
+        ref.zero_grad()
+        a(x).float().square().mean().backward()
+        ref.step()
+        bk.wait()
+        b(x).float().square().mean().backward()
+        bk.wait()
+        for pa, pb in zip(a.parameters(), b.parameters()):
+            assert torch.equal(pa.view(torch.int16), pb.view(torch.int16))
+    assert bk.step_count == 3
+    bk.remove_hooks()

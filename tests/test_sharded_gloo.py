@@ -133,3 +133,24 @@ def test_sharded_equals_unsharded_world2(tmp_path, orc, kind, clip):
         assert np.array_equal(np.load(tmp_path / f"value_{rank}.npy"), h)
         lo, hi = L.shard_range(rank)
         assert np.array_equal(np.load(tmp_path / f"resid_{rank}.npy"), r[lo:hi])
+
+
+def test_bucket_layout_partitions_exactly():
+    from paper_2309_12381_b200.sharded import BucketLayout
+    for world in (1, 2, 4, 8):
+        for be in (64, 4096, 1 << 20):
+            L = BucketLayout(SIZES, world, be)
+            assert L.total % (16 * world) == 0 and L.shard * world == L.total
+            seen = sorted(i for _, _, idx in L.buckets for i in idx)
+            assert seen == list(range(len(SIZES)))                         # every param in one bucket
+            for b, (o, length, idx) in enumerate(L.buckets):
+                assert o % 16 == 0 and length % (16 * world) == 0
+                for i in idx:                                              # params inside their bucket
+                    assert o <= L.offsets[i] and L.offsets[i] + SIZES[i] <= o + length
+                    assert L.offsets[i] % 8 == 0
+                parts = [L.global_range_of_part(b, r) for r in range(world)]
+                assert parts[0][0] == o and parts[-1][1] == o + length
+                assert all(parts[r][1] == parts[r + 1][0] for r in range(world - 1))
+                assert L.part_offsets[b] % 16 == 0
+            spans = sorted((L.offsets[i], L.offsets[i] + n) for i, n in enumerate(SIZES))
+            assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))   # no overlap
