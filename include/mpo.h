@@ -73,7 +73,8 @@ typedef enum {
  *                            round-to-zero"); bf16 is lossless on every finite fp32 value
  *   MPO_FP16_SR              stochastic rounding + int16 signed difference whose sign is the
  *                            paper's "un-round" bit ("fp16 + 13 stochastic"); draws
- *                            from the counter-based generator keyed by (seed, sr_stream, index)
+ *                            from the counter-based generator keyed by (seed, sr_stream, index/2),
+ *                            upper 32 bits for even, lower for odd elements (R14)
  *   MPO_FP16_X8, _BF16_X8    RNE value + 8 extra bits: int8 residual ("keeping only part of
  *                            those bits"; P:134 fp16+8), reading R14
  * Gradients: MPO_FP16, MPO_BF16 or MPO_FP32 (variant formats: their base dtype or MPO_FP32). */

@@ -456,8 +456,13 @@ static void store_resid(int scheme, void* resid, int64_t i, int32_t r) {
     else ((int16_t*)resid)[i] = (int16_t)r;
 }
 
+/* Draw of element i: one 64-bit output serves an element pair -- the upper half for even i,
+ * the lower half for odd i (reading R14). */
 static uint32_t draw(int scheme, uint64_t seed, uint64_t stream, int64_t i) {
-    return scheme == OR_S_SR ? (uint32_t)(or_mix64(seed, stream, (uint64_t)i) >> 32) : 0u;
+    uint64_t x;
+    if (scheme != OR_S_SR) return 0u;
+    x = or_mix64(seed, stream, (uint64_t)i >> 1);
+    return (i & 1) ? (uint32_t)x : (uint32_t)(x >> 32);
 }
 
 void or_split_s(int scheme, int fmt, const float* w, uint16_t* value, void* resid, int64_t n, uint64_t seed,

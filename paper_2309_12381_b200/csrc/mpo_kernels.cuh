@@ -278,8 +278,9 @@ __global__ void __launch_bounds__(kThreads) split_kernel(const float* __restrict
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 uint32_t h0, h1;
-                split1_s<SF>(x[2 * q], sr_draw(seed, stream, uint64_t(e + 2 * q)), h0, code[2 * q]);
-                split1_s<SF>(x[2 * q + 1], sr_draw(seed, stream, uint64_t(e + 2 * q + 1)), h1, code[2 * q + 1]);
+                const uint64_t rr = sr_mix(seed, stream, uint64_t(e + 2 * q) >> 1);   // e is even
+                split1_s<SF>(x[2 * q], static_cast<uint32_t>(rr >> 32), h0, code[2 * q]);
+                split1_s<SF>(x[2 * q + 1], static_cast<uint32_t>(rr), h1, code[2 * q + 1]);
                 hv[q] = h0 | (h1 << 16);
             }
         } else {
@@ -521,8 +522,9 @@ __device__ __forceinline__ void process_unit(const uint4& hv, const ResidUnit<SF
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             uint32_t h0, h1;
-            split1_s<SF>(w[2 * q], sr_draw(c.seed, stream, uint64_t(e0 + 2 * q)), h0, code[2 * q]);
-            split1_s<SF>(w[2 * q + 1], sr_draw(c.seed, stream, uint64_t(e0 + 2 * q + 1)), h1, code[2 * q + 1]);
+            const uint64_t rr = sr_mix(c.seed, stream, uint64_t(e0 + 2 * q) >> 1);   // e0 is even
+            split1_s<SF>(w[2 * q], static_cast<uint32_t>(rr >> 32), h0, code[2 * q]);
+            split1_s<SF>(w[2 * q + 1], static_cast<uint32_t>(rr), h1, code[2 * q + 1]);
             hq[q] = h0 | (h1 << 16);
         }
     } else {
