@@ -272,15 +272,21 @@ def e2e_measure(wl, steps, dist=None):
     sizes = wl.sizes if wl.world == 1 else None
     dev = torch.device("cuda")
     if wl.world == 1:
-        # parameters and gradients are views of two flat buffers (one H2D and one D2H copy per
-        # step, as a data loader / checkpoint stream would do), stepped by the public optimizer
+        # Parameters are views of one flat value buffer; gradients are views of one of two flat
+        # device buffers (double-buffered).  Per step: H2D of the step's grads on a copy-in stream
+        # (overlapping the previous step), ResidualSGD/ResidualAdamW.step() on the compute stream,
+        # a device copy of the updated values into a staging buffer, and the D2H of that staging
+        # buffer on a copy-out stream (overlapping the next step).  PCIe's two directions run
+        # concurrently; every byte still crosses inside the timed region.
         L = wl.layout
         flat_v = torch.empty(L.total, dtype=wl.tdt, device=dev)
         torch_normal_(flat_v, 0.02, 0xB0B, 5000)
-        flat_g = torch.zeros(L.total, dtype=wl.tdt, device=dev)
+        gbuf = [torch.zeros(L.total, dtype=wl.tdt, device=dev) for _ in range(2)]
+        stage = [torch.empty(L.total, dtype=wl.tdt, device=dev) for _ in range(2)]
         shapes = [(n,) for n in sizes]
         params = [torch.nn.Parameter(v) for v in L.views(flat_v, shapes)]
-        for p, g in zip(params, L.views(flat_g, shapes)):
+        gviews = [L.views(g, shapes) for g in gbuf]
+        for p, g in zip(params, gviews[0]):
             p.grad = g
         hk = dict(wl.hpkw)
         if wl.kind == "sgd":
@@ -288,14 +294,53 @@ def e2e_measure(wl, steps, dist=None):
         else:
             b1, b2 = hk.pop("beta1"), hk.pop("beta2")
             opt = mpo.ResidualAdamW(params, betas=(b1, b2), **hk)
-        host = torch.empty(L.total, dtype=wl.tdt, pin_memory=True)
-        host.view(torch.int16).random_(-2000, 2000)
+        host = [torch.empty(L.total, dtype=wl.tdt, pin_memory=True) for _ in range(2)]
+        for h in host:
+            h.view(torch.int16).random_(-2000, 2000)
         out = torch.empty(L.total, dtype=wl.tdt, pin_memory=True)
+        comp = torch.cuda.current_stream()
+        cin, cout = torch.cuda.Stream(), torch.cuda.Stream()
+        state = {"i": 0, "in_ev": [None, None], "used_ev": [None, None], "out_ev": [None, None]}
+
+        def issue_h2d(k):
+            with torch.cuda.stream(cin):
+                if state["used_ev"][k] is not None:
+                    cin.wait_event(state["used_ev"][k])       # step that last read gbuf[k] is done
+                gbuf[k].copy_(host[k], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cin)
+                state["in_ev"][k] = ev
 
         def step():
-            flat_g.copy_(host, non_blocking=True)
+            i = state["i"]
+            k = i % 2
+            if state["in_ev"][k] is None:
+                issue_h2d(k)
+            issue_h2d(1 - k)                                  # prefetch the next step's grads
+            comp.wait_event(state["in_ev"][k])
+            for p, g in zip(params, gviews[k]):
+                p.grad = g
             opt.step()
-            out.copy_(flat_v, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            state["used_ev"][k] = ev
+            if state["out_ev"][k] is not None:
+                comp.wait_event(state["out_ev"][k])           # staging buffer k drained to host
+            stage[k].copy_(flat_v)
+            done = torch.cuda.Event()
+            done.record(comp)
+            with torch.cuda.stream(cout):
+                cout.wait_event(done)
+                out.copy_(stage[k], non_blocking=True)
+                oe = torch.cuda.Event()
+                oe.record(cout)
+                state["out_ev"][k] = oe
+            state["in_ev"][k] = None
+            state["i"] = i + 1
+
+        def drain():
+            comp.wait_stream(cout)
+            comp.wait_stream(cin)
         h2d = d2h = L.total * 2
     else:
         L = wl.layout
@@ -308,10 +353,26 @@ def e2e_measure(wl, steps, dist=None):
             wl.step()
             out.copy_(wl.value, non_blocking=True)
         h2d = d2h = L.total * 2
-    ms, _ = timed(step, steps, 3, dist)
+    if wl.world == 1:
+        def step_and_drain():
+            step()
+            if state["i"] == state_target[0]:
+                drain()                      # the last timed step's D2H lands inside the region
+        state_target = [0]
+        for _ in range(3):
+            step()
+        drain()
+        torch.cuda.synchronize()
+        state["in_ev"] = [None, None]      # the first timed step issues its own H2D inside the region
+        state_target[0] = state["i"] + steps
+        ms, _ = timed(step_and_drain, steps, 0, dist)
+    else:
+        ms, _ = timed(step, steps, 3, dist)
     return {"value": wl.P / (ms * 1e-3), "unit": "params/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": ms, "steps": steps, "path": "public API (ResidualSGD/ResidualAdamW.step) + pinned H2D/D2H"
-            if wl.world == 1 else "mpo_sharded_step + pinned H2D/D2H"}
+            "ms_per_step": ms, "steps": steps,
+            "path": ("public API (ResidualSGD/ResidualAdamW.step); pinned H2D of grads and D2H of values on "
+                     "copy streams overlapping the neighbouring steps") if wl.world == 1
+            else "mpo_sharded_step + pinned H2D/D2H"}
 
 
 def cpu_baseline(name, budget_s=12.0):
