@@ -219,6 +219,33 @@ mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t rank, i
                             int64_t n_total, const void* hp, double* norm_ws,
                             mpo_stream stream);
 
+/* The sharded step fused with its collectives over NVLink SHARP: one kernel
+ * per rank reads the SUM over all ranks of its shard's 16-bit gradients with multimem.ld_reduce
+ * (fp32 accumulation in the switch, one rounding to 16 bits), updates value/residual/state like
+ * mpo_sharded_step, and multicasts the new 16-bit values to every rank's replica with
+ * multimem.st -- no reduce-scatter / all-gather launches and no reduced-gradient buffer.
+ *   value_mc, grad_mc : multicast addresses of the replicated n_total-element value buffer and
+ *                       of the per-rank gradient buffers (a multicast object every rank bound)
+ *   value_uc          : this rank's unicast address of its value replica (read)
+ *   resid_shard, m_shard, v_shard : this rank's shard state (n_total/world entries)
+ *   vdt               : MPO_FP16 | MPO_BF16 (RNE storage); grads of the same dtype
+ *   hp                : mpo_sgd_hp* | mpo_adam_hp*; grad_scale 1/world for a mean; no global-norm
+ *                       clipping and no skip_nonfinite (no pre-pass); clip_value allowed
+ * The caller orders the call after every rank finished writing its gradients and before any
+ * rank reads the values again (cross-rank barriers); the kernel ends with fence.proxy.alias +
+ * fence.acq_rel.sys. */
+mpo_status mpo_nvls_sharded_step(mpo_optim kind, int32_t rank, int32_t world, mpo_dtype vdt,
+                                 void* value_mc, const void* value_uc, const void* grad_mc,
+                                 void* resid_shard, float* m_shard, float* v_shard,
+                                 int64_t n_total, const void* hp, mpo_stream stream);
+
+/* A single-device multicast object bound to fresh device memory (cuMulticastCreate /
+ * cuMulticastBindMem), for running the NVLS step at world 1 and in tests.  *uc_ptr / *mc_ptr
+ * receive the unicast and multicast addresses of the same bytes; *mapped_bytes the size rounded
+ * up to the multicast granularity.  Owned by the caller until mpo_nvls_free_local. */
+mpo_status mpo_nvls_alloc_local(int64_t bytes, void** uc_ptr, void** mc_ptr, int64_t* mapped_bytes);
+mpo_status mpo_nvls_free_local(void* uc_ptr, void* mc_ptr, int64_t mapped_bytes);
+
 /* Diagnostic: checks the branch-free fast sqrt / division sequences of the step kernels against
  * the compiler's IEEE sqrtf() and `/`.  sqrt: ALL 2^32 binary32 patterns;
  * division: `pairs` operand pairs drawn from a counter-based generator keyed by `seed` (bit

@@ -24,7 +24,8 @@ MPO_MAX_HP_GROUPS = 16
 # Every entry point include/mpo.h declares (tests/test_boundary.py checks the header agrees).
 SYMBOLS = ("mpo_split", "mpo_reconstruct", "mpo_sgd_step", "mpo_adam_step", "mpo_norm_ws_doubles",
            "mpo_fused_backward_hook_step", "mpo_sharded_step", "mpo_last_error", "mpo_build_exact",
-           "mpo_launch_count", "mpo_selfcheck_fastmath")
+           "mpo_launch_count", "mpo_selfcheck_fastmath", "mpo_nvls_sharded_step", "mpo_nvls_alloc_local",
+           "mpo_nvls_free_local")
 
 
 class MpoError(RuntimeError):
@@ -76,6 +77,12 @@ def _declare(L):
     L.mpo_norm_ws_doubles.restype = I64
     L.mpo_selfcheck_fastmath.argtypes = [I64, C.c_uint64, P, P]
     L.mpo_selfcheck_fastmath.restype = C.c_int
+    L.mpo_nvls_sharded_step.argtypes = [D, I32, I32, D, P, P, P, P, P, P, I64, P, P]
+    L.mpo_nvls_sharded_step.restype = C.c_int
+    L.mpo_nvls_alloc_local.argtypes = [I64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]
+    L.mpo_nvls_alloc_local.restype = C.c_int
+    L.mpo_nvls_free_local.argtypes = [P, P, I64]
+    L.mpo_nvls_free_local.restype = C.c_int
 
 
 def load(exact: bool = False):

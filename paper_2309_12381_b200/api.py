@@ -275,6 +275,33 @@ def mpo_selfcheck_fastmath(pairs: int = 1 << 30, seed: int = 0xB0B, exact: bool 
     return tuple(int(x) for x in counts.cpu())
 
 
+def mpo_nvls_sharded_step(kind: int, rank: int, world: int, vdt: int, value_mc: int, value_uc: int, grad_mc: int,
+                          resid_shard: torch.Tensor, m_shard: Optional[torch.Tensor], v_shard: Optional[torch.Tensor],
+                          n_total: int, hp, stream=None, exact: bool = False):
+    """The sharded step fused with its collectives over NVLink SHARP (include/mpo.h): multicast
+    addresses are raw device addresses (ints) of a multicast object every rank bound."""
+    L = _lib_of(exact)
+    chp = hp.c() if hasattr(hp, "c") else hp
+    _lib.check(L, L.mpo_nvls_sharded_step(kind, rank, world, vdt, value_mc, value_uc, grad_mc, _ptr(resid_shard),
+                                          _ptr(m_shard), _ptr(v_shard), n_total, C.byref(chp), _stream(stream)))
+
+
+class NvlsLocalBuffer:
+    """A single-device multicast object bound to fresh memory (world-1 NVLS runs and tests):
+    ``uc`` / ``mc`` are the unicast / multicast device addresses of the same bytes."""
+
+    def __init__(self, nbytes: int, exact: bool = False):
+        self._L = _lib_of(exact)
+        uc, mc, sz = C.c_void_p(), C.c_void_p(), C.c_int64()
+        _lib.check(self._L, self._L.mpo_nvls_alloc_local(nbytes, C.byref(uc), C.byref(mc), C.byref(sz)))
+        self.uc, self.mc, self.size = uc.value, mc.value, sz.value
+
+    def free(self):
+        if self.uc:
+            _lib.check(self._L, self._L.mpo_nvls_free_local(self.uc, self.mc, self.size))
+            self.uc = self.mc = None
+
+
 def norm_ws_doubles(exact: bool = False) -> int:
     return int(_lib_of(exact).mpo_norm_ws_doubles())
 

@@ -2,7 +2,11 @@
 // arXiv 2309.12381: argument validation, host-side derivation of the kernel scalars (R7), the
 // global-norm pre-pass (clipping), the NCCL sharded step and diagnostics.  The step kernels
 // themselves live in mpo_kernels.cuh and are instantiated per storage format by mpo_inst.cu.
+#include <cuda.h>   // driver types only: entry points are fetched with cudaGetDriverEntryPoint
 #include <nccl.h>
+
+#include <mutex>
+#include <unordered_map>
 
 #define MPO_ABI_TU
 #include "mpo_kernels.cuh"
@@ -533,5 +537,167 @@ MPO_API mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t
     }
     // 3. all-gather of the 16-bit values only (residual and state never move)
     if (world > 1) MPO_NCCL(ncclAllGather(x.value, value_flat, size_t(shard), nccl_dtype(vdt), comm, s));
+    return MPO_OK;
+}
+
+
+// ------------------------------------------------------------------------------------------
+// NVLS (NVLink SHARP) fused sharded step and a single-device multicast allocator for tests
+// ------------------------------------------------------------------------------------------
+MPO_API mpo_status mpo_nvls_sharded_step(mpo_optim kind, int32_t rank, int32_t world, mpo_dtype vdt, void* value_mc,
+                                         const void* value_uc, const void* grad_mc, void* resid_shard, float* m_shard,
+                                         float* v_shard, int64_t n_total, const void* hp, mpo_stream stream) {
+    g_err.clear();
+    mpo_status st;
+    if (world < 1 || rank < 0 || rank >= world) return fail(MPO_EINVAL, "bad rank / world");
+    if (n_total < 0 || n_total % (int64_t(8) * world) != 0)
+        return fail(MPO_EINVAL, "n_total must be a non-negative multiple of 8*world");
+    if (vdt != MPO_FP16 && vdt != MPO_BF16) return fail(MPO_EDTYPE, "the NVLS step takes MPO_FP16 or MPO_BF16 values");
+    if (!hp) return fail(MPO_EINVAL, "NULL hyper-parameters");
+    if (n_total == 0) return MPO_OK;
+    if (!value_mc || !value_uc || !grad_mc || !resid_shard) return fail(MPO_EINVAL, "NULL buffer");
+    if (!aligned16(value_mc) || !aligned16(value_uc) || !aligned16(grad_mc) || !aligned16(resid_shard))
+        return fail(MPO_EALIGN, "buffer not 16-byte aligned");
+    const int64_t shard = n_total / world;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (kind == MPO_ADAM) {
+        const mpo_adam_hp* h = static_cast<const mpo_adam_hp*>(hp);
+        if ((st = check_adam_hp(h, 1)) != MPO_OK) return st;
+        if (h->max_grad_norm > 0.0 || h->skip_nonfinite)
+            return fail(MPO_EINVAL, "the NVLS step has no norm pre-pass (max_grad_norm / skip_nonfinite)");
+        if (!m_shard || !v_shard || !aligned16(m_shard) || !aligned16(v_shard))
+            return fail(MPO_EALIGN, "m/v shards must be non-NULL and 16-byte aligned");
+        const AdamK k = derive_adam(*h);
+        if (vdt == MPO_BF16)
+            return FormatOps<MPO_BF16>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, v_shard,
+                                             rank * shard, shard, nullptr, &k, s);
+        return FormatOps<MPO_FP16>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, v_shard,
+                                         rank * shard, shard, nullptr, &k, s);
+    }
+    if (kind == MPO_SGD) {
+        const mpo_sgd_hp* h = static_cast<const mpo_sgd_hp*>(hp);
+        if ((st = check_sgd_hp(h, 1)) != MPO_OK) return st;
+        if (h->skip_nonfinite) return fail(MPO_EINVAL, "the NVLS step has no norm pre-pass (skip_nonfinite)");
+        if (h->momentum != 0.0 && (!m_shard || !aligned16(m_shard)))
+            return fail(MPO_EALIGN, "momentum shard must be non-NULL and 16-byte aligned");
+        const SgdK k = derive_sgd(*h);
+        if (vdt == MPO_BF16)
+            return FormatOps<MPO_BF16>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, nullptr,
+                                             rank * shard, shard, &k, nullptr, s);
+        return FormatOps<MPO_FP16>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, nullptr,
+                                         rank * shard, shard, &k, nullptr, s);
+    }
+    return fail(MPO_EINVAL, "unknown optimizer kind");
+}
+
+namespace {
+struct McAlloc {
+    CUmemGenericAllocationHandle mem, mc;
+    size_t size;
+};
+std::mutex g_mc_mu;
+std::unordered_map<uintptr_t, McAlloc> g_mc;
+
+template <class F>
+F driver_fn(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        return nullptr;
+    return reinterpret_cast<F>(p);
+}
+}  // namespace
+
+#define MPO_CU(call, what)                                                                                 \
+    do {                                                                                                   \
+        CUresult r_ = (call);                                                                              \
+        if (r_ != CUDA_SUCCESS) return fail(MPO_ECUDA, std::string(what) + " failed: CUresult " + std::to_string(int(r_))); \
+    } while (0)
+
+MPO_API mpo_status mpo_nvls_alloc_local(int64_t bytes, void** uc_ptr, void** mc_ptr, int64_t* mapped_bytes) {
+    g_err.clear();
+    if (bytes <= 0 || !uc_ptr || !mc_ptr || !mapped_bytes) return fail(MPO_EINVAL, "bad arguments");
+    auto pGet = driver_fn<CUresult (*)(CUdevice*, int)>("cuDeviceGet");
+    auto pGran = driver_fn<CUresult (*)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags)>(
+        "cuMulticastGetGranularity");
+    auto pMcCreate = driver_fn<CUresult (*)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*)>(
+        "cuMulticastCreate");
+    auto pMcAdd = driver_fn<CUresult (*)(CUmemGenericAllocationHandle, CUdevice)>("cuMulticastAddDevice");
+    auto pCreate = driver_fn<CUresult (*)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*,
+                                          unsigned long long)>("cuMemCreate");
+    auto pBind = driver_fn<CUresult (*)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t,
+                                        size_t, unsigned long long)>("cuMulticastBindMem");
+    auto pReserve = driver_fn<CUresult (*)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long)>(
+        "cuMemAddressReserve");
+    auto pMap = driver_fn<CUresult (*)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long)>(
+        "cuMemMap");
+    auto pAccess = driver_fn<CUresult (*)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t)>("cuMemSetAccess");
+    if (!pGet || !pGran || !pMcCreate || !pMcAdd || !pCreate || !pBind || !pReserve || !pMap || !pAccess)
+        return fail(MPO_ECUDA, "driver entry points for multicast are unavailable");
+    int devi = 0;
+    if (cudaGetDevice(&devi) != cudaSuccess) return check_launch("cudaGetDevice");
+    CUdevice dev;
+    MPO_CU(pGet(&dev, devi), "cuDeviceGet");
+    CUmulticastObjectProp mp = {};
+    mp.numDevices = 1;
+    mp.size = size_t(bytes);
+    mp.handleTypes = 0;
+    size_t gran = 0;
+    MPO_CU(pGran(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED), "cuMulticastGetGranularity");
+    const size_t size = (size_t(bytes) + gran - 1) / gran * gran;
+    mp.size = size;
+    McAlloc a;
+    a.size = size;
+    MPO_CU(pMcCreate(&a.mc, &mp), "cuMulticastCreate");
+    MPO_CU(pMcAdd(a.mc, dev), "cuMulticastAddDevice");
+    CUmemAllocationProp ap = {};
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = devi;
+    MPO_CU(pCreate(&a.mem, size, &ap, 0), "cuMemCreate");
+    MPO_CU(pBind(a.mc, 0, a.mem, 0, size, 0), "cuMulticastBindMem");
+    CUdeviceptr uc = 0, mc = 0;
+    MPO_CU(pReserve(&uc, size, gran, 0, 0), "cuMemAddressReserve(uc)");
+    MPO_CU(pMap(uc, size, 0, a.mem, 0), "cuMemMap(uc)");
+    MPO_CU(pReserve(&mc, size, gran, 0, 0), "cuMemAddressReserve(mc)");
+    MPO_CU(pMap(mc, size, 0, a.mc, 0), "cuMemMap(mc)");
+    CUmemAccessDesc ad = {};
+    ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ad.location.id = devi;
+    ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    MPO_CU(pAccess(uc, size, &ad, 1), "cuMemSetAccess(uc)");
+    MPO_CU(pAccess(mc, size, &ad, 1), "cuMemSetAccess(mc)");
+    {
+        std::lock_guard<std::mutex> lk(g_mc_mu);
+        g_mc[uintptr_t(uc)] = a;
+    }
+    *uc_ptr = reinterpret_cast<void*>(uc);
+    *mc_ptr = reinterpret_cast<void*>(mc);
+    *mapped_bytes = int64_t(size);
+    return MPO_OK;
+}
+
+MPO_API mpo_status mpo_nvls_free_local(void* uc_ptr, void* mc_ptr, int64_t mapped_bytes) {
+    g_err.clear();
+    McAlloc a;
+    {
+        std::lock_guard<std::mutex> lk(g_mc_mu);
+        auto it = g_mc.find(uintptr_t(uc_ptr));
+        if (it == g_mc.end()) return fail(MPO_EINVAL, "not an mpo_nvls_alloc_local buffer");
+        a = it->second;
+        g_mc.erase(it);
+    }
+    auto pUnmap = driver_fn<CUresult (*)(CUdeviceptr, size_t)>("cuMemUnmap");
+    auto pFree = driver_fn<CUresult (*)(CUdeviceptr, size_t)>("cuMemAddressFree");
+    auto pRelease = driver_fn<CUresult (*)(CUmemGenericAllocationHandle)>("cuMemRelease");
+    if (!pUnmap || !pFree || !pRelease) return fail(MPO_ECUDA, "driver entry points unavailable");
+    if (cudaDeviceSynchronize() != cudaSuccess) return check_launch("cudaDeviceSynchronize");
+    MPO_CU(pUnmap(CUdeviceptr(mc_ptr), a.size), "cuMemUnmap(mc)");
+    MPO_CU(pUnmap(CUdeviceptr(uc_ptr), a.size), "cuMemUnmap(uc)");
+    MPO_CU(pFree(CUdeviceptr(mc_ptr), a.size), "cuMemAddressFree(mc)");
+    MPO_CU(pFree(CUdeviceptr(uc_ptr), a.size), "cuMemAddressFree(uc)");
+    MPO_CU(pRelease(a.mc), "cuMemRelease(mc)");
+    MPO_CU(pRelease(a.mem), "cuMemRelease(mem)");
+    (void)mapped_bytes;
     return MPO_OK;
 }

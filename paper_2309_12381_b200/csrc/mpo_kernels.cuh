@@ -961,6 +961,91 @@ __global__ void __launch_bounds__(kTmaThreads, 1) sumsq_tma_kernel(const __grid_
 #endif  // MPO_ABI_TU
 
 // ------------------------------------------------------------------------------------------
+// G6: the sharded step fused with its collectives over NVLink SHARP.
+// Each rank's threads read the SUM of all ranks' 16-bit gradients of their shard with one
+// multimem.ld_reduce per 8 elements (the NVSwitch reduces in fp32 and rounds once to 16 bits),
+// update value/residual/state exactly like the multi-tensor step, and write the new 16-bit values
+// to every rank's replica with multimem.st -- reduce-scatter, update and all-gather in one pass,
+// with no intermediate reduced-gradient buffer in HBM.  The caller orders the kernel after every
+// rank's backward (grads written) and before any rank's next use of the values (barriers).
+// ------------------------------------------------------------------------------------------
+template <int B>
+__device__ __forceinline__ uint4 multimem_ld_reduce_v4(const void* mc) {
+    uint4 r;
+    if constexpr (B == kBF16) {
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                     : "l"(mc)
+                     : "memory");
+    } else {
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                     : "l"(mc)
+                     : "memory");
+    }
+    return r;
+}
+
+__device__ __forceinline__ void multimem_st_v4(void* mc, const uint4& v) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+template <int SF, class Op>
+__global__ void __launch_bounds__(kThreads) nvls_step_kernel(uint16_t* __restrict__ value_mc,
+                                                             const uint16_t* __restrict__ value_uc,
+                                                             const uint16_t* __restrict__ grad_mc, void* resid,
+                                                             float* __restrict__ m, float* __restrict__ v,
+                                                             int64_t shard_base, int64_t n,
+                                                             const __grid_constant__ typename Op::K c) {
+    constexpr int B = Fmt<SF>::base;
+    const bool need_m = Op::reads_m(c), has_m = Op::writes_m(c);
+    const int64_t nunits = n / kUnitEl;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < nunits; u += stride) {
+        const int64_t e = u * kUnitEl;                      // index inside the shard
+        GradUnit<B> gu;
+        gu.a = multimem_ld_reduce_v4<B>(grad_mc + shard_base + e);
+        gu.b = gu.a;
+        const uint4 hv = ldv(value_uc + shard_base + e);
+        const ResidUnit<SF> rv = ld_resid<SF>(resid, e);
+        float mm[8], vv[8];
+        if (need_m) {
+            const float4 a = ldf(m + e), b = ldf(m + e + 4);
+            mm[0] = a.x; mm[1] = a.y; mm[2] = a.z; mm[3] = a.w; mm[4] = b.x; mm[5] = b.y; mm[6] = b.z; mm[7] = b.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mm[k] = 0.0f;
+        }
+        if constexpr (Op::kHasV) {
+            const float4 a = ldf(v + e), b = ldf(v + e + 4);
+            vv[0] = a.x; vv[1] = a.y; vv[2] = a.z; vv[3] = a.w; vv[4] = b.x; vv[5] = b.y; vv[6] = b.z; vv[7] = b.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) vv[k] = 0.0f;
+        }
+        uint4 ho;
+        ResidUnit<SF> ro;
+        process_unit<SF, B, Op, false>(hv, rv, gu, mm, vv, c, 1.0f, 0u, shard_base + e, ho, ro);
+        multimem_st_v4(value_mc + shard_base + e, ho);     // every rank's replica
+        st_resid<SF>(resid, e, ro);
+        if (has_m) {
+            stf(m + e, make_float4(mm[0], mm[1], mm[2], mm[3]));
+            stf(m + e + 4, make_float4(mm[4], mm[5], mm[6], mm[7]));
+        }
+        if constexpr (Op::kHasV) {
+            stf(v + e, make_float4(vv[0], vv[1], vv[2], vv[3]));
+            stf(v + e + 4, make_float4(vv[4], vv[5], vv[6], vv[7]));
+        }
+    }
+    // make the multicast stores visible system-wide, and ordered with later accesses through the
+    // unicast alias of the same memory
+    asm volatile("fence.proxy.alias;" ::: "memory");
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
+// ------------------------------------------------------------------------------------------
 // Host launch templates
 // ------------------------------------------------------------------------------------------
 constexpr int kSmemBudget = (MPO_CTAS_PER_SM == 1 ? 227 * 1024 : (228 * 1024) / MPO_CTAS_PER_SM - 1024);
@@ -1020,6 +1105,8 @@ struct FormatOps {
     static mpo_status split(const float* w, void* value, void* resid, int64_t n, uint64_t seed, uint32_t stream,
                             cudaStream_t s);
     static mpo_status reconstruct(const void* value, const void* resid, float* w, int64_t n, cudaStream_t s);
+    static mpo_status nvls(int kind, void* value_mc, const void* value_uc, const void* grad_mc, void* resid, float* m,
+                           float* v, int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak, cudaStream_t s);
 };
 
 }  // namespace mpo

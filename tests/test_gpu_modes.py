@@ -320,3 +320,58 @@ def test_bucketed_hook_sharding_equals_two_phase(mpo, nccl1, kind):
             assert torch.equal(pa.view(torch.int16), pb.view(torch.int16))
     assert bk.step_count == 3
     bk.remove_hooks()
+
+
+def _cudart():
+    import ctypes
+    import glob
+    import nvidia
+    for d in nvidia.__path__:
+        for f in glob.glob(os.path.join(d, "cuda_runtime", "lib", "libcudart.so*")):
+            lib = ctypes.CDLL(f)
+            lib.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+            return lib
+    raise RuntimeError("libcudart not found")
+
+
+@pytest.mark.parametrize("kind,fmt", [("adam", "bf16"), ("sgd", "fp16")])
+def test_nvls_fused_step_world1_matches_oracle(mpo, orc, kind, fmt):
+    """SURVEY 8(f) row 1 at world 1: the fused NVLS kernel (multimem.ld_reduce of the grads,
+    multimem.st of the values through a real single-device multicast object) == the oracle step
+    bit-exactly (exact build)."""
+    from paper_2309_12381_b200 import api
+    from paper_2309_12381_b200._lib import MPO_ADAM, MPO_SGD
+    from gpu_util import TDT
+    rt = _cudart()
+    n = 3 * 4096 + 24
+    w = synth.weights(n, 0.02, 99)
+    h, r = orc.split(fmt, w)
+    g = synth.grads(n, 1e-2, fmt, 99, 1)
+    vbuf = api.NvlsLocalBuffer(n * 2, exact=True)
+    gbuf = api.NvlsLocalBuffer(n * 2, exact=True)
+    try:
+        hh, gg = np.ascontiguousarray(h), np.ascontiguousarray(g)
+        assert rt.cudaMemcpy(vbuf.uc, hh.ctypes.data, n * 2, 1) == 0        # host -> device
+        assert rt.cudaMemcpy(gbuf.uc, gg.ctypes.data, n * 2, 1) == 0
+        R = torch.from_numpy(r.copy()).cuda()
+        M = torch.zeros(n, device="cuda"); V = torch.zeros(n, device="cuda")
+        m = np.zeros(n, np.float32); v = np.zeros(n, np.float32)
+        if kind == "adam":
+            hp = mpo.AdamParams(lr=1e-3, weight_decay=0.1, step=1)
+            api.mpo_nvls_sharded_step(MPO_ADAM, 0, 1, api.dtype_code(TDT[fmt]), vbuf.mc, vbuf.uc, gbuf.mc, R, M, V,
+                                      n, hp, exact=True)
+            orc.adam_step(fmt, fmt, h, r, g, m, v, lr=1e-3, weight_decay=0.1, step=1)
+        else:
+            hp = mpo.SgdParams(lr=0.1, momentum=0.9, first_step=True)
+            api.mpo_nvls_sharded_step(MPO_SGD, 0, 1, api.dtype_code(TDT[fmt]), vbuf.mc, vbuf.uc, gbuf.mc, R, M, None,
+                                      n, hp, exact=True)
+            orc.sgd_step(fmt, fmt, h, r, g, m, lr=0.1, momentum=0.9, first_step=True)
+        torch.cuda.synchronize()
+        out = np.empty(n, np.uint16)
+        assert rt.cudaMemcpy(out.ctypes.data, vbuf.uc, n * 2, 2) == 0        # device -> host
+        assert np.array_equal(out, h)
+        assert np.array_equal(R.cpu().numpy(), r)
+        assert np.array_equal(M.cpu().numpy().view(np.uint32), m.view(np.uint32))
+    finally:
+        vbuf.free()
+        gbuf.free()
