@@ -641,16 +641,31 @@ MPO_API mpo_status mpo_nvls_alloc_local(int64_t bytes, void** uc_ptr, void** mc_
     CUmulticastObjectProp mp = {};
     mp.numDevices = 1;
     mp.size = size_t(bytes);
-    mp.handleTypes = 0;
     size_t gran = 0;
-    MPO_CU(pGran(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED), "cuMulticastGetGranularity");
-    const size_t size = (size_t(bytes) + gran - 1) / gran * gran;
-    mp.size = size;
     McAlloc a;
+    // the driver may require an exportable handle type on the multicast object: try the POSIX FD,
+    // fabric and no-export variants in turn
+    const unsigned long long kinds[3] = {CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, CU_MEM_HANDLE_TYPE_FABRIC, 0};
+    CUresult last = CUDA_ERROR_UNKNOWN;
+    size_t size = 0;
+    unsigned long long chosen = 0;
+    for (unsigned long long hk : kinds) {
+        mp.handleTypes = hk;
+        mp.size = size_t(bytes);
+        if (pGran(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS) continue;
+        size = (size_t(bytes) + gran - 1) / gran * gran;
+        mp.size = size;
+        last = pMcCreate(&a.mc, &mp);
+        if (last == CUDA_SUCCESS) {
+            chosen = hk;
+            break;
+        }
+    }
+    if (last != CUDA_SUCCESS) return fail(MPO_ECUDA, "cuMulticastCreate failed: CUresult " + std::to_string(int(last)));
     a.size = size;
-    MPO_CU(pMcCreate(&a.mc, &mp), "cuMulticastCreate");
     MPO_CU(pMcAdd(a.mc, dev), "cuMulticastAddDevice");
     CUmemAllocationProp ap = {};
+    ap.requestedHandleTypes = CUmemAllocationHandleType(chosen);
     ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     ap.location.id = devi;

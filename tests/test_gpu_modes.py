@@ -347,7 +347,10 @@ def test_nvls_fused_step_world1_matches_oracle(mpo, orc, kind, fmt):
     w = synth.weights(n, 0.02, 99)
     h, r = orc.split(fmt, w)
     g = synth.grads(n, 1e-2, fmt, 99, 1)
-    vbuf = api.NvlsLocalBuffer(n * 2, exact=True)
+    try:
+        vbuf = api.NvlsLocalBuffer(n * 2, exact=True)
+    except mpo.MpoError as e:   # a one-GPU box may refuse a one-device multicast team
+        pytest.skip(f"no multicast object on this box: {e}")
     gbuf = api.NvlsLocalBuffer(n * 2, exact=True)
     try:
         hh, gg = np.ascontiguousarray(h), np.ascontiguousarray(g)
