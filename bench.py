@@ -524,6 +524,9 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
         return torch.nn.functional.cross_entropy(logits.float().reshape(-1, logits.shape[-1]), idx[:, 1:].reshape(-1))
 
     def run(mode):
+        import gc
+        gc.collect()            # the previous mode's hooks <-> params <-> optimizer cycle
+        torch.cuda.empty_cache()
         torch.manual_seed(0)
         model = GPT2LMHeadModel(GPT2Config()).to(dev)
         P = sum(p.numel() for p in model.parameters())
@@ -576,10 +579,7 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
         res = {"ms_per_train_step": s.elapsed_time(e) / steps, "state_bytes_per_param": state / P,
                "persistent_bytes_per_param": persistent / P,
                "peak_bytes_per_param": peak / P, "peak_gb": peak / 1e9, "loss": float(loss)}
-        del model, opt, step
-        import gc
-        gc.collect()          # hooks <-> params <-> optimizer form reference cycles
-        torch.cuda.empty_cache()
+        del model, opt, step, loss
         return res
     for mode in ("hook", "two_phase", "amp_fp32_master"):
         try:
