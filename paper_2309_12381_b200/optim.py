@@ -124,10 +124,21 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         return None
 
     # -- hook mode ---------------------------------------------------------------------------
-    def install_backward_hooks(self):
+    def install_backward_hooks(self, batch_below: int = 1 << 16, flush_elems: int = 1 << 22):
         """Step each parameter inside backward, as soon as its gradient is accumulated, then free
-        the gradient.  Returns the hook handles."""
+        the gradient.  Returns the hook handles.
+
+        Parameters smaller than ``batch_below`` elements (biases, norms) are not launched one by
+        one: their gradients are held until ``flush_elems`` elements are pending or the backward
+        ends, then stepped by one multi-tensor launch (bounded transient memory, far fewer
+        launches).  ``batch_below=0`` steps every parameter individually; batching is off with
+        ``skip_nonfinite`` (whose hook-mode skip is per parameter)."""
         self._check_hook_mode()
+        self._batch_below = 0 if self.skip_nonfinite else int(batch_below)
+        self._flush_elems = int(flush_elems)
+        self._pending = []
+        self._pending_elems = 0
+        self._flush_queued = False
         for gi, group in enumerate(self.param_groups):
             for p in group["params"]:
                 st = self.state[p]
@@ -152,6 +163,16 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         st = self.state[p]
         g = p.grad
         st["step"] += 1
+        if p.numel() < self._batch_below:
+            self._pending.append((p, g))
+            self._pending_elems += p.numel()
+            p.grad = None            # the pending list keeps the (small) gradient until the flush
+            if not self._flush_queued:
+                torch.autograd.Variable._execution_engine.queue_callback(self._flush_pending)
+                self._flush_queued = True
+            if self._pending_elems >= self._flush_elems:
+                self._flush_pending(final=False)
+            return
         row = st["row"]
         row.grad = g.data_ptr()
         hp = self._hp(self.param_groups[st["group"]], st["step"]).c()
@@ -159,6 +180,32 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                                          row, hp, exact=self.exact,
                                          norm_ws=self._ws(p.device) if self.skip_nonfinite else None)
         p.grad = None   # freed now; stream order makes the block's reuse safe
+
+    def _flush_pending(self, final: bool = True):
+        """One multi-tensor launch over the batched small parameters of this backward."""
+        if final:
+            self._flush_queued = False
+        if not self._pending:
+            return
+        pending, self._pending, self._pending_elems = self._pending, [], 0
+        with torch.no_grad():
+            by_dtype = {}
+            for p, g in pending:
+                by_dtype.setdefault((p.dtype, g.dtype), []).append((p, g))
+            for items in by_dtype.values():
+                ps = [p for p, _ in items]
+                sts = [self.state[p] for p in ps]
+                keys, hp_index = {}, []
+                for s_ in sts:
+                    hp_index.append(keys.setdefault((s_["group"], s_["step"]), len(keys)))
+                tab = api.TensorTable([p.data for p in ps], [s_["resid"] for s_ in sts], [g for _, g in items],
+                                      [s_.get("m") for s_ in sts], [s_.get("v") for s_ in sts], hp_index,
+                                      scheme=self.scheme, sr_streams=[s_["index"] for s_ in sts])
+                hps = [self._hp(self.param_groups[gi], stp) for (gi, stp) in keys]
+                if len(hps) > MPO_MAX_HP_GROUPS:
+                    raise MpoError(1, "more than 16 distinct (group, step) pairs in one flush")
+                self._launch(tab, hps)
+        del pending              # the gradients are released (stream order keeps reuse safe)
 
     # -- loss scaling: found-inf -------------------------------------------------------------
     def _ws(self, device):

@@ -63,10 +63,13 @@ def _pair(fmt, kind, mpo, **kw):
 
 @pytest.mark.parametrize("fmt", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("kind", ["adam", "sgd"])
-def test_hook_mode_equals_two_phase(mpo, fmt, kind):
+@pytest.mark.parametrize("batch_below", [0, 1 << 16, 1 << 30])
+def test_hook_mode_equals_two_phase(mpo, fmt, kind, batch_below):
+    """Per-parameter launches (batch_below=0), small parameters batched into one launch at the end
+    of backward (default), and everything batched: all bitwise equal to the two-phase step."""
     kw = dict(lr=1e-3, weight_decay=0.1) if kind == "adam" else dict(lr=0.1, momentum=0.9, weight_decay=1e-4)
     a, b, oa, ob = _pair(fmt, kind, mpo, **kw)
-    ob.install_backward_hooks()
+    ob.install_backward_hooks(batch_below=batch_below)
     gen = torch.Generator(device="cuda").manual_seed(1)
     for step in range(4):
         idx = torch.randint(0, 257, (4, 33), device="cuda", generator=gen)
