@@ -527,6 +527,8 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
         import gc
         gc.collect()            # the previous mode's hooks <-> params <-> optimizer cycle
         torch.cuda.empty_cache()
+        torch.cuda.synchronize()
+        base = torch.cuda.memory_allocated()   # whatever an earlier mode left behind is excluded
         torch.manual_seed(0)
         model = GPT2LMHeadModel(GPT2Config()).to(dev)
         P = sum(p.numel() for p in model.parameters())
@@ -563,11 +565,11 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
                         p.copy_(m_)
                 return loss
         torch.cuda.synchronize()
-        state = torch.cuda.memory_allocated()      # params + residual/master + optimizer state
+        state = torch.cuda.memory_allocated() - base   # params + residual/master + optimizer state
         for _ in range(warmup):
             step()
         torch.cuda.synchronize()
-        persistent = torch.cuda.memory_allocated()  # what survives between training steps
+        persistent = torch.cuda.memory_allocated() - base   # what survives between training steps
         torch.cuda.reset_peak_memory_stats()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
@@ -575,10 +577,10 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
             loss = step()
         e.record()
         torch.cuda.synchronize()
-        peak = torch.cuda.max_memory_allocated()
+        peak = torch.cuda.max_memory_allocated() - base
         res = {"ms_per_train_step": s.elapsed_time(e) / steps, "state_bytes_per_param": state / P,
                "persistent_bytes_per_param": persistent / P,
-               "peak_bytes_per_param": peak / P, "peak_gb": peak / 1e9, "loss": float(loss)}
+               "peak_bytes_per_param": peak / P, "peak_gb": peak / 1e9, "loss": float(loss.detach()), "leftover_bytes_excluded": base}
         del model, opt, step, loss
         return res
     for mode in ("hook", "two_phase", "amp_fp32_master"):
