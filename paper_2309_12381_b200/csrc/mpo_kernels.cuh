@@ -678,7 +678,24 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #endif
 }
+// Wait for the phase of `parity` to complete.  The suspend-time hint lets the hardware park the
+// waiting warp until the phase flips (or the hint expires) instead of re-issuing try_wait in a
+// tight loop, which would steal issue slots from the producer and the computing warps.
+#ifndef MPO_WAIT_HINT_NS
+#define MPO_WAIT_HINT_NS 0x989680
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if MPO_WAIT_HINT_NS > 0
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(MPO_WAIT_HINT_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
@@ -688,6 +705,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 __device__ __forceinline__ uint64_t evict_first_policy() {
     uint64_t pol;

@@ -9,7 +9,7 @@ import torch, bench
 out = {}
 for name, steps in (("resnet50_sgd", 2000), ("gpt2_adamw", 300), ("llama7b_adam", 20)):
     wl = bench.Workload(name)
-    ms, per, n = bench.timed(wl.step, steps, 5)
+    ms, n = bench.timed(wl.step, steps, 5)
     out[name] = round(wl.P * wl.bytes_per_param / (ms * 1e-3) / 1e9)
     del wl; torch.cuda.empty_cache()
 print(json.dumps(out))
