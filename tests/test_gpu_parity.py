@@ -453,3 +453,131 @@ def test_table_larger_than_one_launch(mpo, orc):
         m = np.zeros(n, np.float32); v = np.zeros(n, np.float32)
         orc.adam_step(fmt, fmt, hs[i], rs[i], gs[i], m, v, **_adam_hp_kw(hp))
         assert np.array_equal(host16(V[i]), hs[i]) and np.array_equal(R[i].cpu().numpy(), rs[i]), i
+
+
+# ------------------------------------------------------------------------------------------
+# Full sizes in the bench's launch configuration, checked on sampled windows
+# ------------------------------------------------------------------------------------------
+def _windows(sizes, per_tensor=2, width=4104, seed=7):
+    """Sampled (start, stop) windows of the flat element space: every tensor's head and tail (its
+    ragged end and the tensor boundary) plus random interior windows."""
+    rs = synth.rng(seed, 1)
+    offs = np.cumsum([0] + list(sizes))
+    out = []
+    for i, n in enumerate(sizes):
+        o = int(offs[i])
+        out.append((o, o + min(n, width)))
+        out.append((max(o, o + n - width), o + n))
+        for _ in range(per_tensor if n > 4 * width else 0):
+            a = int(rs.integers(o, o + n - width))
+            out.append((a, a + width))
+    return out
+
+
+def test_llama7b_sharded_world1_sampled(mpo, orc):
+    """configs[3] at N=1 in the bench's launch configuration: the LLaMA-7B parameter set (6.74e9
+    params) as one flat bf16 buffer through mpo_sharded_step (world 1); sampled windows (every
+    tensor's head and tail + random interior) bit-exact against the oracle (exact build)."""
+    import bench
+    if torch.cuda.get_device_properties(0).total_memory < 150e9:
+        pytest.skip("needs a B200-class device (~100 GB)")
+    wl = bench.Workload("llama7b_adam")
+    try:
+        L = wl.layout
+        offs = L.offsets
+        wins = []
+        for (a, b) in _windows(wl.sizes):
+            # map flat (unpadded) windows to the padded layout offsets of the owning tensor
+            i = int(np.searchsorted(np.cumsum([0] + wl.sizes), a, side="right") - 1)
+            base = int(np.cumsum([0] + wl.sizes)[i])
+            wins.append((offs[i] + a - base, offs[i] + b - base))
+        take = lambda t, a, b: t[a:b].detach().cpu().numpy()
+        pre = [(take(wl.value.view(torch.int16), a, b).view(np.uint16), take(wl.resid, a, b), take(wl.grad.view(torch.int16), a, b).view(np.uint16),
+                take(wl.m, a, b), take(wl.v, a, b)) for a, b in wins]
+        from paper_2309_12381_b200._lib import MPO_ADAM
+        wl.t = 1
+        hp = wl.hp()
+        import torch.distributed as tdist
+        # one step through the exact build, same call bench.py times
+        from paper_2309_12381_b200.sharded import nccl_comm_ptr
+        if not tdist.is_initialized():
+            import socket
+            sk = socket.socket(); sk.bind(("127.0.0.1", 0))
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1"); os.environ["MASTER_PORT"] = str(sk.getsockname()[1]); sk.close()
+            tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+        mpo.mpo_sharded_step(MPO_ADAM, nccl_comm_ptr(), 0, 1, wl.value, wl.grad, wl.resid, wl.m, wl.v, hp, exact=True)
+        torch.cuda.synchronize()
+        for (a, b), (h, r, g, m, v) in zip(wins, pre):
+            orc.adam_step("bf16", "bf16", h, r, g, m, v, **_adam_hp_kw(hp))
+            assert np.array_equal(take(wl.value.view(torch.int16), a, b).view(np.uint16), h), (a, b)
+            assert np.array_equal(take(wl.resid, a, b), r), (a, b)
+            assert same_bits_nan_equal(take(wl.m, a, b), m) and same_bits_nan_equal(take(wl.v, a, b), v)
+    finally:
+        del wl
+        torch.cuda.empty_cache()
+
+
+def test_tensor_larger_than_2_31_elements(mpo, orc):
+    """Maximum sizes: one tensor of 2^31 + 4104 elements (64-bit element offsets, > 2^31 / 4096
+    tiles); windows around 2^31 and the ragged end bit-exact (exact build)."""
+    if torch.cuda.get_device_properties(0).total_memory < 80e9:
+        pytest.skip("needs ~32 GB free")
+    n = (1 << 31) + 4104 + 5
+    fmt = "bf16"
+    V = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    synth.torch_normal_(V, 0.02, 3, 0)
+    R = torch.zeros(n, dtype=torch.int16, device="cuda")
+    G = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    synth.torch_normal_(G, 1e-3, 3, 1)
+    M = torch.zeros(n, device="cuda"); W = torch.zeros(n, device="cuda")
+    wins = [(0, 4104), ((1 << 31) - 4100, (1 << 31) + 4100), (n - 9000, n)]
+    take = lambda t, a, b: t[a:b].cpu().numpy()
+    pre = [(take(V.view(torch.int16), a, b).view(np.uint16), take(R, a, b), take(G.view(torch.int16), a, b).view(np.uint16))
+           for a, b in wins]
+    hp = mpo.AdamParams(lr=1e-3, weight_decay=0.1, step=1)
+    mpo.mpo_adam_step(mpo.TensorTable([V], [R], [G], [M], [W]), hp, exact=True)
+    torch.cuda.synchronize()
+    for (a, b), (h, r, g) in zip(wins, pre):
+        m = np.zeros(b - a, np.float32); v = np.zeros(b - a, np.float32)
+        orc.adam_step(fmt, fmt, h, r, g, m, v, **_adam_hp_kw(hp))
+        assert np.array_equal(take(V.view(torch.int16), a, b).view(np.uint16), h), (a, b)
+        assert np.array_equal(take(R, a, b), r) and same_bits_nan_equal(take(M, a, b), m)
+    del V, R, G, M, W
+    torch.cuda.empty_cache()
+
+
+def test_vit_l16_adam_clip_full_sampled(mpo, orc):
+    """configs[4] in the bench's launch configuration (ViT-L/16 set, fp16, Adam + global-norm clip,
+    norm ~4 so clipping is active): S over all 304M grads within 1e-10 of the oracle's pairwise
+    sum; sampled windows bit-exact with the oracle stepping on the GPU's S (hybrid, exact build)."""
+    import bench
+    wl = bench.Workload("vit_l16_adam_clip")
+    try:
+        L = wl.layout
+        cum = np.cumsum([0] + wl.sizes)
+        wins = []
+        for (a, b) in _windows(wl.sizes, per_tensor=1):
+            i = int(np.searchsorted(cum, a, side="right") - 1)
+            wins.append((L.offsets[i] + a - int(cum[i]), L.offsets[i] + b - int(cum[i])))
+        take = lambda t, a, b: t[a:b].detach().cpu().numpy()
+        pre = [(take(wl.value.view(torch.int16), a, b).view(np.uint16), take(wl.resid, a, b),
+                take(wl.grad.view(torch.int16), a, b).view(np.uint16), take(wl.m, a, b), take(wl.v, a, b))
+               for a, b in wins]
+        gall = wl.grad.view(torch.int16).cpu().numpy().view(np.uint16)
+        S_orc = sum(orc.sumsq("fp16", np.ascontiguousarray(gall[o:o + n])) for o, n in zip(L.offsets, wl.sizes))
+        wl.t = 1
+        hp = wl.hp()
+        mpo.mpo_adam_step(wl.table, hp, norm_ws=wl.norm_ws, exact=True)
+        torch.cuda.synchronize()
+        S = float(wl.norm_ws[0].item())
+        assert abs(S - S_orc) <= 1e-10 * S_orc
+        coef = orc.clip_coef(S, hp.max_grad_norm)
+        assert coef < 1.0
+        for (a, b), (h, r, g, m, v) in zip(wins, pre):
+            orc.adam_step("fp16", "fp16", h, r, g, m, v, **_adam_hp_kw(hp), clip_coef=coef)
+            assert np.array_equal(take(wl.value.view(torch.int16), a, b).view(np.uint16), h), (a, b)
+            assert np.array_equal(take(wl.resid, a, b), r), (a, b)
+            assert same_bits_nan_equal(take(wl.m, a, b), m) and same_bits_nan_equal(take(wl.v, a, b), v)
+    finally:
+        del wl
+        torch.cuda.empty_cache()
