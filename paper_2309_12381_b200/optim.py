@@ -15,6 +15,7 @@ Everything numeric runs in libmpo (api.py marshals arguments only).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from typing import Iterable, Optional
 
 import torch
@@ -23,6 +24,19 @@ from . import api
 from ._lib import MPO_ADAM, MPO_SGD, MPO_MAX_HP_GROUPS, MpoError, Tensor
 
 _16 = (torch.float16, torch.bfloat16)
+
+
+def _weak_hook(opt):
+    """A post-accumulate-grad hook that refers to its optimizer weakly: the tensor's hook table is
+    held from C++, where Python's cycle collector cannot see it, so a strong reference would keep
+    the optimizer and its state alive forever."""
+    ref = weakref.ref(opt)
+
+    def hook(p):
+        o = ref()
+        if o is not None:
+            o._hook(p)
+    return hook
 
 
 class _ResidualOptimizer(torch.optim.Optimizer):
@@ -151,7 +165,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                 row.sr_stream = st["index"]
                 st["row"] = row
                 st["group"] = gi
-                self._hooks.append(p.register_post_accumulate_grad_hook(self._hook))
+                self._hooks.append(p.register_post_accumulate_grad_hook(_weak_hook(self)))
         return list(self._hooks)
 
     def remove_backward_hooks(self):

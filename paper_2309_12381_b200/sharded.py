@@ -13,6 +13,7 @@ the CUDA library through torch's NCCL communicator.
 """
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
@@ -268,11 +269,16 @@ class BucketedShardedOptimizer:
         self._handles = [p.register_post_accumulate_grad_hook(self._make_hook(i)) for i, p in enumerate(self.params)]
 
     def _make_hook(self, i):
+        ref = weakref.ref(self)   # hooks live in C++-held tables: no strong cycle back to self
+
         def hook(p):
-            b = self.layout.bucket_of[i]
-            self._pending[b] -= 1
-            if self._pending[b] == 0:
-                self._launch_bucket(b)
+            o = ref()
+            if o is None:
+                return
+            b = o.layout.bucket_of[i]
+            o._pending[b] -= 1
+            if o._pending[b] == 0:
+                o._launch_bucket(b)
         return hook
 
     def _launch_bucket(self, b):

@@ -381,3 +381,24 @@ def test_nvls_fused_step_world1_matches_oracle(mpo, orc, kind, fmt):
     finally:
         vbuf.free()
         gbuf.free()
+
+
+def test_hook_mode_optimizer_is_collectable(mpo):
+    """Hooks hold the optimizer weakly: dropping the model and the optimizer frees all their
+    device memory (no uncollectable hook <-> optimizer cycle)."""
+    import gc
+    import weakref
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+
+    def make():
+        m = nn.Sequential(nn.Linear(256, 256), nn.LayerNorm(256)).cuda()
+        o = mpo.ResidualAdamW(m.parameters(), lr=1e-3, fmt=torch.bfloat16)
+        o.install_backward_hooks()
+        m(torch.randn(4, 256, device="cuda", dtype=torch.bfloat16)).float().sum().backward()
+        return weakref.ref(o)
+    ref = make()
+    gc.collect()
+    torch.cuda.synchronize()
+    assert ref() is None
+    assert torch.cuda.memory_allocated() - base < 1 << 16
