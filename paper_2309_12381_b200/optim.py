@@ -146,7 +146,8 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         one: their gradients are held until ``flush_elems`` elements are pending or the backward
         ends, then stepped by one multi-tensor launch (bounded transient memory, far fewer
         launches).  ``batch_below=0`` steps every parameter individually; batching is off with
-        ``skip_nonfinite`` (whose hook-mode skip is per parameter)."""
+        ``skip_nonfinite`` (whose hook-mode skip is per parameter).  The hooks hold the optimizer
+        weakly: keep a reference to it for as long as training runs."""
         self._check_hook_mode()
         self._batch_below = 0 if self.skip_nonfinite else int(batch_below)
         self._flush_elems = int(flush_elems)
