@@ -461,7 +461,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": "optimizer-step params/sec", "value": value, "unit": "params/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": f"{fmt}+int16 residual / fp32 arithmetic", "data": "synthetic",
+            "dtype": "f32", "storage": f"{fmt} value + int16 residual, fp32 optimizer state", "data": "synthetic",
             "config": {"workload": f"{name} ({wl}, BASELINE configs[{WORKLOADS[name][4]}])",
                        "sample_params_per_step": n, "params_in_workload": P},
             "cpu_baseline": {"value": value, "unit": "params/s", "cores": 1, "kind": "oracle",
@@ -642,7 +642,7 @@ def main():
         "metric": "optimizer-step params/sec", "value": value, "unit": "params/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
-        "dtype": f"{wl.fmt}+int16 residual / fp32 arithmetic", "data": "synthetic",
+        "dtype": "f32", "storage": f"{wl.fmt} value + int16 residual, fp32 optimizer state", "data": "synthetic",
         "config": {"workload": f"{args.workload}: BASELINE configs[{wl.cfg}] parameter set "
                                f"{WORKLOADS[args.workload][0]} ({wl.P} params, {wl.ntensors} tensors)",
                    "optimizer": wl.kind, "hyper_parameters": wl.hpkw, "value_dtype": wl.fmt,
