@@ -130,11 +130,20 @@ AdamK derive_adam(const mpo_adam_hp& h) {
     c.lerp_hi = (c.b1c < 0.5f) ? 0 : 1;
     c.dec1 = c.mode == 1 ? c.dec : 1.0f;
     c.wdl2 = c.mode == 2 ? c.wd : 0.0f;
-    c.fast_ok = !c.lerp_hi && c.bc2s >= 0x1p-60f && c.bc2s < 0x1p61f;
+    c.fast_ok = !c.lerp_hi && c.bc2s >= 0x1p-60f && c.bc2s <= 1.0f && c.eps >= 0.0f && c.eps <= 0x1p59f;
     c._pad = 0;
     c.seed = h.seed;
     c.clip_on = h.clip_value > 0.0;
     c.clipv = float(h.clip_value);
+    // v < (bc2s * 2^60)^2 keeps sqrt(v)/bc2s < 2^60, so s = that + eps < 2^61 (rounded down to a
+    // float that is still <= the real bound)
+    {
+        const double vh = double(c.bc2s) * double(c.bc2s) * 0x1p120;
+        float f = float(vh < 0x1p122 ? vh : 0x1p122);
+        if (double(f) > vh) f = std::nextafter(f, 0.0f);
+        c.vhi = f;
+    }
+    c._pad3 = 0;
     return c;
 }
 

@@ -486,7 +486,11 @@ __device__ __forceinline__ void process_unit(const uint4& hv, const ResidUnit<SF
     const uint32_t* h = &hv.x;
     float w[8], g[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) g[k] = grad_at<G>(gu, k) * c.gs;
+    for (int k = 0; k < 8; ++k) g[k] = grad_at<G>(gu, k);
+    if (c.gs != 1.0f) {   // uniform; g * 1 == g exactly, so skipping it changes nothing
+#pragma unroll
+        for (int k = 0; k < 8; ++k) g[k] = g[k] * c.gs;
+    }
     if (c.clip_on) {   // uniform per tensor
 #pragma unroll
         for (int k = 0; k < 8; ++k) g[k] = clamp_grad(g[k], c.clipv);
