@@ -772,11 +772,12 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
         // ---------------- producer ----------------
         if (lane == 0) {
             const uint64_t pol = evict_first_policy();
-            int cur = 0, it = 0;
-            for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x, ++it) {
-                const int s = it % stages;
-                const uint32_t round = uint32_t(it / stages);
-                mbar_wait(&empty[s], (round & 1u) ^ 1u);
+            // stage index and phase advance incrementally (a runtime `it % stages` costs two
+            // integer divisions per tile)
+            int cur = 0, s = 0;
+            uint32_t ph = 0;
+            for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
+                mbar_wait(&empty[s], ph ^ 1u);
                 while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
                 const KT& T = tab.t[cur];
                 const K c = hp.g[hp_of(T)];
@@ -796,6 +797,10 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
                     if (need_m) bulk_g2s(st + OFF_M, T.m + base, nvec * 4u, &full[s], pol);
                     if constexpr (Op::kHasV) bulk_g2s(st + OFF_V, T.v + base, nvec * 4u, &full[s], pol);
                 }
+                if (++s == stages) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
         }
         return;
@@ -805,10 +810,9 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
     float coef = 1.0f;
     if constexpr (CLIP) coef = clip_coef(sumsq, max_norm);
     const int ct = threadIdx.x;   // 0 .. kCW*32-1, one unit per tile
-    int cur = 0, it = 0;
-    for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x, ++it) {
-        const int s = it % stages;
-        const uint32_t round = uint32_t(it / stages);
+    int cur = 0, s = 0;
+    uint32_t ph = 0;
+    for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
         while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
         const KT& T = tab.t[cur];
         const K c = hp.g[hp_of(T)];
@@ -816,17 +820,19 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
         const int64_t nvalid = T.n - base < TE ? T.n - base : TE;
         const int64_t nvec = nvalid & ~int64_t(kGran - 1u);
         const int64_t el = int64_t(ct) * kUnitEl;
-        mbar_wait(&full[s], round & 1u);
+        mbar_wait(&full[s], ph);
         const bool full_unit = el + kUnitEl <= nvec;
-        uint4 hv = make_uint4(0u, 0u, 0u, 0u);
+        uint4 hv;
         ResidUnit<SF> rv;
-        rv.v = hv;
         GradUnit<G> gu;
-        gu.a = gu.b = hv;
         float mm[8], vv[8];
+        if (!full_unit) {
+            hv = make_uint4(0u, 0u, 0u, 0u);
+            rv.v = hv;
+            gu.a = gu.b = hv;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) mm[k] = vv[k] = 0.0f;
-        if (full_unit) {
+            for (int k = 0; k < 8; ++k) mm[k] = vv[k] = 0.0f;
+        } else {
             const unsigned char* st = ring + size_t(s) * SB;
             hv = *reinterpret_cast<const uint4*>(st + el * 2);
             if constexpr (RB == 2) {
@@ -845,11 +851,17 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
                 const float4 a = *reinterpret_cast<const float4*>(st + OFF_M + el * 4);
                 const float4 b = *reinterpret_cast<const float4*>(st + OFF_M + el * 4 + 16);
                 mm[0] = a.x; mm[1] = a.y; mm[2] = a.z; mm[3] = a.w; mm[4] = b.x; mm[5] = b.y; mm[6] = b.z; mm[7] = b.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) mm[k] = 0.0f;
             }
             if constexpr (Op::kHasV) {
                 const float4 a = *reinterpret_cast<const float4*>(st + OFF_V + el * 4);
                 const float4 b = *reinterpret_cast<const float4*>(st + OFF_V + el * 4 + 16);
                 vv[0] = a.x; vv[1] = a.y; vv[2] = a.z; vv[3] = a.w; vv[4] = b.x; vv[5] = b.y; vv[6] = b.z; vv[7] = b.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) vv[k] = 0.0f;
             }
         }
 #ifdef MPO_RELEASE_EARLY
@@ -882,6 +894,10 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
         } else if (nvec < nvalid && el <= nvec && nvec < el + kUnitEl) {
             process_tail<SF, G, Op, CLIP>(T, base + nvec, base + nvalid, c, coef);
         }
+        if (++s == stages) {
+            s = 0;
+            ph ^= 1u;
+        }
     }
 }
 
@@ -913,10 +929,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) sumsq_tma_kernel(const __grid_
     if (warp == kCW) {
         if (lane == 0) {
             const uint64_t pol = evict_first_policy();
-            int cur = 0, it = 0;
-            for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x, ++it) {
-                const int s = it % stages;
-                mbar_wait(&empty[s], (uint32_t(it / stages) & 1u) ^ 1u);
+            int cur = 0, s = 0;
+            uint32_t ph = 0;
+            for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
+                mbar_wait(&empty[s], ph ^ 1u);
                 while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
                 const KT& T = tab.t[cur];
                 const int64_t base = int64_t(tile - T.tile0) * TE;
@@ -926,6 +942,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) sumsq_tma_kernel(const __grid_
                 if (nvec)
                     bulk_g2s(ring + size_t(s) * SB, static_cast<const unsigned char*>(T.grad) + base * GB, nvec * GB,
                              &full[s], pol);
+                if (++s == stages) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
         }
         return;
@@ -934,16 +954,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) sumsq_tma_kernel(const __grid_
 #pragma unroll
     for (int k = 0; k < kUnitEl; ++k) acc8[k] = 0.0;
     const int64_t el = int64_t(threadIdx.x) * kUnitEl;
-    int cur = 0, it = 0;
-    for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x, ++it) {
-        const int s = it % stages;
+    int cur = 0, s = 0;
+    uint32_t ph = 0;
+    for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
         while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
         const KT& T = tab.t[cur];
         const float gs = gsc.g[hp_of(T)];
         const int64_t base = int64_t(tile - T.tile0) * TE;
         const int64_t nvalid = T.n - base < TE ? T.n - base : TE;
         const int64_t nvec = nvalid & ~int64_t(kUnitEl - 1);
-        mbar_wait(&full[s], uint32_t(it / stages) & 1u);
+        mbar_wait(&full[s], ph);
         const bool full_unit = el + kUnitEl <= nvec;
         GradUnit<G> gu;
         gu.a = gu.b = make_uint4(0u, 0u, 0u, 0u);
@@ -966,6 +986,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) sumsq_tma_kernel(const __grid_
                 const double g = double(grad_scalar<G>(T.grad, i) * gs);
                 acc8[0] = fma(g, g, acc8[0]);
             }
+        }
+        if (++s == stages) {
+            s = 0;
+            ph ^= 1u;
         }
     }
     double acc = ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
