@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -39,7 +40,9 @@ constexpr int kThreads = 256;
 constexpr int kUnitEl = 8;                          // elements per unit (128-bit of 16-bit data)
 constexpr int64_t kTileEl = int64_t(MPO_CW) * 32 * kUnitEl;   // 4096 elements: one unit per consumer thread
 constexpr int kUnroll = int(kTileEl / (kThreads * kUnitEl));  // LSU kernel: units per thread per tile
-static_assert(kUnroll >= 1, "tile smaller than one LSU pass");
+#ifdef MPO_WITH_LSU
+static_assert(kUnroll >= 1 && kTileEl % (kThreads * kUnitEl) == 0, "LSU kernel needs whole 2048-element passes");
+#endif
 constexpr int kNormBlocksMax = 2048;                // partial sums of the norm pre-pass
 constexpr int kBigT = 512;    // 512 x 56 B + 16 groups fits the 32 KB kernel-parameter limit
 constexpr int kMidT = 32;
