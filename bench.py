@@ -467,7 +467,7 @@ def run_reference(args):
             "cpu_baseline": {"value": value, "unit": "params/s", "cores": 1, "kind": "oracle",
                              "sample": f"{n} of {P} params per step, {args.steps} steps"},
             "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    emit(line)
 
 
 def secondary(names, steps, warmup, hbm_peak):
@@ -593,7 +593,28 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
     return out
 
 
+_JSON_OUT = None
+
+
+def _claim_stdout():
+    """Keep stdout for the one JSON line: libraries that print to fd 1 (NCCL's version banner on
+    communicator creation, for one) are redirected to stderr for the rest of the run."""
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+        sys.stdout = sys.stderr
+
+
+def emit(line):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3000)
@@ -685,7 +706,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.workload)
     if rank == 0:
-        print(json.dumps(line))
+        emit(line)
     if dist is not None:
         dist.destroy_process_group()
 

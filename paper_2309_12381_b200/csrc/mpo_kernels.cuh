@@ -733,6 +733,14 @@ struct GradBytes {
     static constexpr int v = G == kFP32 ? 4 : 2;
 };
 
+// the piece a stage holds, published by the producer (tensor index < 0: end of schedule)
+struct __align__(16) StageDesc {
+    int64_t base;
+    int32_t cur;
+    int32_t nvalid;
+};
+constexpr int kDescBytes = kMaxStages * int(sizeof(StageDesc));   // keeps the ring 128-B aligned
+
 // bytes of one stage: value 2 + resid rb + grad gb + m 4 [+ v 4] per element
 template <int RB, int G, bool HAS_V>
 __host__ __device__ constexpr int stage_bytes() {
@@ -759,7 +767,8 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + kMaxStages;
-    unsigned char* ring = smem + kBarBytes;
+    StageDesc* desc = reinterpret_cast<StageDesc*>(smem + kBarBytes);
+    unsigned char* ring = smem + kBarBytes + kDescBytes;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -772,26 +781,28 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
     __syncthreads();
 
     if (warp == kCW) {
-        // ---------------- producer ----------------
+        // ---------------- producer: scheduler + bulk copies ----------------
+        // The producer alone walks the schedule and publishes each stage's piece (tensor, offset,
+        // length) in the stage descriptor before arming the stage's barrier; the consumers read it
+        // after their wait (mbarrier release/acquire orders the shared store), so the 16 consumer
+        // warps carry no scheduling arithmetic and no walker registers.
         if (lane == 0) {
             const uint64_t pol = evict_first_policy();
             // stage index and phase advance incrementally (a runtime `it % stages` costs two
             // integer divisions per tile)
-            int cur = 0, s = 0;
+            int s = 0;
             uint32_t ph = 0;
-            for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
+            auto issue = [&](int cur, int64_t base, int64_t nvalid) {
                 mbar_wait(&empty[s], ph ^ 1u);
-                while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
                 const KT& T = tab.t[cur];
                 const K c = hp.g[hp_of(T)];
-                const int64_t base = int64_t(tile - T.tile0) * TE;
-                const int64_t nvalid = T.n - base < TE ? T.n - base : TE;
                 const uint32_t nvec = uint32_t(nvalid) & ~(kGran - 1u);
                 const bool need_m = Op::reads_m(c);
                 uint32_t bytes = nvec * (2u + RB + GB);
                 if (need_m) bytes += nvec * 4u;
                 if constexpr (Op::kHasV) bytes += nvec * 4u;
                 unsigned char* st = ring + size_t(s) * SB;
+                desc[s] = StageDesc{base, cur, int32_t(nvalid)};
                 mbar_arrive_expect_tx(&full[s], bytes);
                 if (nvec) {
                     bulk_g2s(st, static_cast<const uint16_t*>(T.value) + base, nvec * 2u, &full[s], pol);
@@ -804,7 +815,21 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
                     s = 0;
                     ph ^= 1u;
                 }
+            };
+            // schedule: tile k of the launch's tile space goes to CTA k mod G, so the grid sweeps
+            // memory together (one contiguous window per stream at any moment).  A/B on one box:
+            // contiguous per-CTA ranges balanced to 16 elements lost 5 %, a balanced sweep of
+            // chunks < 1 tile lost 1-2 % on ResNet-50 (profiles/r01_ab7..10*.log).
+            int cur = 0;
+            for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
+                while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
+                const int64_t base = int64_t(tile - tab.t[cur].tile0) * TE;
+                issue(cur, base, tab.t[cur].n - base < TE ? tab.t[cur].n - base : TE);
             }
+            // end of schedule: a descriptor with no tensor, completed by a plain arrive
+            mbar_wait(&empty[s], ph ^ 1u);
+            desc[s] = StageDesc{0, -1, 0};
+            mbar_arrive(&full[s]);
         }
         return;
     }
@@ -813,17 +838,17 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
     float coef = 1.0f;
     if constexpr (CLIP) coef = clip_coef(sumsq, max_norm);
     const int ct = threadIdx.x;   // 0 .. kCW*32-1, one unit per tile
-    int cur = 0, s = 0;
+    const int64_t el = int64_t(ct) * kUnitEl;
+    int s = 0;
     uint32_t ph = 0;
-    for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
-        while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
-        const KT& T = tab.t[cur];
-        const K c = hp.g[hp_of(T)];
-        const int64_t base = int64_t(tile - T.tile0) * TE;
-        const int64_t nvalid = T.n - base < TE ? T.n - base : TE;
-        const int64_t nvec = nvalid & ~int64_t(kGran - 1u);
-        const int64_t el = int64_t(ct) * kUnitEl;
+    for (;;) {
         mbar_wait(&full[s], ph);
+        const StageDesc d = desc[s];
+        if (d.cur < 0) break;
+        const KT& T = tab.t[d.cur];
+        const K c = hp.g[hp_of(T)];
+        const int64_t base = d.base, nvalid = d.nvalid;
+        const int64_t nvec = nvalid & ~int64_t(kGran - 1u);
         const bool full_unit = el + kUnitEl <= nvec;
         uint4 hv;
         ResidUnit<SF> rv;
@@ -1116,14 +1141,15 @@ mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typen
         return check_launch("step_kernel");
     }
 #endif
+    const int64_t grid = grid_for(tiles, MPO_CTAS_PER_SM);
     auto kern = step_tma_kernel<MAXT, SF, G, Op, CLIP>;
     constexpr int SB = stage_bytes<Fmt<SF>::rbytes, G, Op::kHasV>();
-    constexpr int stages = (kSmemBudget - kBarBytes) / SB < kMaxStages ? (kSmemBudget - kBarBytes) / SB : kMaxStages;
+    constexpr int kFree = kSmemBudget - kBarBytes - kDescBytes;
+    constexpr int stages = kFree / SB < kMaxStages ? kFree / SB : kMaxStages;
     static_assert(stages >= 2, "need at least two pipeline stages");
-    constexpr int smem = kBarBytes + stages * SB;
+    constexpr int smem = kBarBytes + kDescBytes + stages * SB;
     static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (attr != cudaSuccess) return fail(MPO_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr));
-    const int64_t grid = grid_for(tiles, MPO_CTAS_PER_SM);
     kern<<<unsigned(grid), kTmaThreads, smem, s>>>(tab, hp, sumsq, max_norm, stages, skip);
     ++g_launches;
     return check_launch("step_tma_kernel");

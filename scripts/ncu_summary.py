@@ -48,3 +48,15 @@ if __name__ == "__main__":
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full.json"), "w") as fh:
         json.dump(res, fh, indent=1)
     print(json.dumps(res, indent=1)[:6000])
+    # per-workload step-kernel figures read by bench.py (roofline.traffic)
+    summ = {}
+    for wl, ks in res.items():
+        st = [k for k in ks if "step_tma_kernel" in k["kernel"]]
+        if not st:
+            continue
+        summ[wl] = {"kernel": st[0]["kernel"],
+                    "dram_bytes_per_launch": sum(k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"] for k in st) / len(st),
+                    "gpu_time_us_per_launch": sum(k["gpu__time_duration.sum"] for k in st) / len(st),
+                    "source": f"profiles/{tag}_ncu_full.json (ncu --set full, cache control all: cold L2 per replay)"}
+    with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as fh:
+        json.dump(summ, fh, indent=1)

@@ -143,3 +143,73 @@ def test_sr_hook_mode_equals_multi_tensor(mpo):
     for pa, pb in zip(a.parameters(), b.parameters()):
         assert torch.equal(pa.view(torch.int16), pb.view(torch.int16))
         assert torch.equal(oa.state[pa]["resid"], ob.state[pb]["resid"])
+
+
+@pytest.mark.parametrize("scheme,fmt,kind", [("rne", "bf16", "adam"), ("x8", "fp16", "sgd"), ("rne", "fp16", "sgd")])
+def test_schedule_many_tensors_with_guards(mpo, orc, scheme, fmt, kind):
+    """The step kernel's schedule (tiles dealt round-robin to the CTAs, each
+    stage's piece published by the producer warp): 400 tensors of mixed sizes (empty, tiny,
+    ragged, several tiles) over every CTA, more tiles than one wave, tails of the int8 residual's
+    16-element granule.  Every tensor is a view into a flat buffer with a guard gap after it: the
+    exact build matches the oracle bit for bit and no guard word changes."""
+    rng = np.random.default_rng(2023)
+    sizes = [int(s) for s in rng.choice([0, 1, 3, 8, 15, 16, 17, 64, 100, 4095, 4096, 4097, 9000, 20011], 400)]
+    GUARD = 64   # elements after every tensor (keeps every view 16-B aligned for any residual width)
+    offs, o = [], 0
+    for n in sizes:
+        offs.append(o)
+        o += (n + 15) // 16 * 16 + GUARD
+    total = o
+    rdt = RDT[scheme]
+    hs, rs, ms, vs, gs = [], [], [], [], []
+    for i, n in enumerate(sizes):
+        w = synth.weights(n, 0.05, 0xB0B + i)
+        h, r = orc.split_s(scheme, fmt, w, seed=5, stream=i)
+        hs.append(h); rs.append(r)
+        ms.append(synth.normal_f32(n, 1e-3, 5, i)); vs.append(np.abs(synth.normal_f32(n, 1e-5, 6, i)))
+        gs.append(synth.grads(n, 1e-2, fmt, 0xC0FFEE, i))
+    # flat host images, guards filled with a recognisable pattern
+    fh = np.full(total, 0x7E57, np.uint16)
+    fr = np.full(total, 0x55 if rdt == np.int8 else 0x5A5A, np.uint8 if rdt == np.int8 else np.uint16)
+    fg = np.full(total, 0x3C00, np.uint16)
+    fm = np.full(total, 7.0, np.float32)
+    fv = np.full(total, 9.0, np.float32)
+    for i, n in enumerate(sizes):
+        s = slice(offs[i], offs[i] + n)
+        fh[s] = hs[i]; fr[s] = rs[i].view(fr.dtype); fg[s] = gs[i]; fm[s] = ms[i]; fv[s] = vs[i]
+    H, G = dev16(fh, fmt), dev16(fg, fmt)
+    R = torch.from_numpy(fr.view(np.int8 if rdt == np.int8 else np.int16).copy()).cuda()
+    M, W = devf(fm), devf(fv)
+    view = lambda t, i: t[offs[i]:offs[i] + sizes[i]]
+    grp = [i % 2 for i in range(len(sizes))]
+    if kind == "adam":
+        hps = [mpo.AdamParams(lr=1e-3, weight_decay=0.1, adamw=True, step=2),
+               mpo.AdamParams(lr=2e-3, beta2=0.95, step=2, grad_scale=0.5)]
+        tab = mpo.TensorTable([view(H, i) for i in range(len(sizes))], [view(R, i) for i in range(len(sizes))],
+                              [view(G, i) for i in range(len(sizes))], [view(M, i) for i in range(len(sizes))],
+                              [view(W, i) for i in range(len(sizes))], grp, scheme=scheme)
+        mpo.mpo_adam_step(tab, hps, exact=True)
+    else:
+        hps = [mpo.SgdParams(lr=0.1, momentum=0.9, weight_decay=1e-4),
+               mpo.SgdParams(lr=0.05, momentum=0.9, nesterov=True)]
+        tab = mpo.TensorTable([view(H, i) for i in range(len(sizes))], [view(R, i) for i in range(len(sizes))],
+                              [view(G, i) for i in range(len(sizes))], [view(M, i) for i in range(len(sizes))],
+                              [None] * len(sizes), grp, scheme=scheme)
+        mpo.mpo_sgd_step(tab, hps, exact=True)
+    for i, n in enumerate(sizes):
+        hp = hps[grp[i]]
+        if kind == "adam":
+            orc.adam_step_s(scheme, fmt, fmt, hs[i], rs[i], gs[i], ms[i], vs[i], seed=0, stream=i, **_kw(hp))
+        else:
+            orc.sgd_step_s(scheme, fmt, fmt, hs[i], rs[i], gs[i], ms[i], lr=hp.lr, momentum=hp.momentum,
+                           weight_decay=hp.weight_decay, nesterov=hp.nesterov, first_step=hp.first_step,
+                           seed=0, stream=i)
+        s = slice(offs[i], offs[i] + n)
+        fh[s] = hs[i]; fr[s] = rs[i].view(fr.dtype); fm[s] = ms[i]
+        if kind == "adam":
+            fv[s] = vs[i]
+    assert np.array_equal(host16(H), fh), "value (tensor or guard) differs"
+    assert np.array_equal(R.cpu().numpy().view(fr.dtype), fr), "residual (tensor or guard) differs"
+    assert np.array_equal(M.cpu().numpy().view(np.uint32), fm.view(np.uint32)), "m (tensor or guard) differs"
+    assert np.array_equal(W.cpu().numpy().view(np.uint32), fv.view(np.uint32)), "v (tensor or guard) differs"
+    assert np.array_equal(host16(G), fg), "gradients must be read-only"
