@@ -262,6 +262,50 @@ def timed(fn, steps, warmup, dist=None, sampler=None):
     return ms, launches
 
 
+NVLINK_GBS = 900.0   # NVLink 5 per direction per GPU
+
+
+def multi_gpu_breakdown(wl, dist, steps, warmup):
+    """N > 1 only (every rank runs it; collectives in the same order on all ranks).  SURVEY 8(e):
+    (i) the update alone on this rank's shard (same step kernel through mpo_sgd_step /
+    mpo_adam_step on a one-tensor table of the shard), aggregate params/s = P / max-rank time --
+    the part that should scale ~linearly in N; (ii) the two collectives of the sharded step alone
+    (NCCL reduce-scatter of the 16-bit grads, all-gather of the 16-bit values, torch's process
+    group, same byte counts), as algbw and busbw = bytes*(N-1)/N / t against NVLink's 900 GB/s."""
+    import torch
+    mpo = wl.mpo
+    L, N = wl.layout, wl.world
+    lo, hi = L.shard_range(wl.rank)
+    tab = mpo.TensorTable([wl.value[lo:hi]], [wl.resid], [wl.grad[lo:hi]], [wl.m],
+                          [wl.v if wl.v is not None else None], scheme=wl.scheme)
+
+    def upd():
+        wl.t += 1
+        if wl.kind == "sgd":
+            mpo.mpo_sgd_step(tab, wl.hp())
+        else:
+            mpo.mpo_adam_step(tab, wl.hp(), norm_ws=wl.norm_ws if wl.clip else None)
+
+    out = {}
+    t_upd, _ = timed(upd, steps, warmup, dist)
+    out["update_only"] = {"ms_per_step": t_upd, "params_per_s": wl.P / (t_upd * 1e-3),
+                          "shard_params": hi - lo,
+                          "achieved_gbs_per_rank": (hi - lo) * wl.bytes_per_param / (t_upd * 1e-3) / 1e9}
+    rs_out = torch.empty(hi - lo, dtype=wl.grad.dtype, device=wl.grad.device)
+    ag_out = torch.empty_like(wl.value)
+    nbytes = wl.value.numel() * wl.value.element_size()
+    for name, fn in (("reduce_scatter_grad16", lambda: dist.reduce_scatter_tensor(rs_out, wl.grad)),
+                     ("all_gather_value16", lambda: dist.all_gather_into_tensor(ag_out, wl.value[lo:hi]))):
+        ms, _ = timed(fn, max(10, steps // 10), warmup, dist)
+        algbw = nbytes / (ms * 1e-3) / 1e9
+        busbw = algbw * (N - 1) / N
+        out[name] = {"ms": ms, "bytes": nbytes, "algbw_gbs": algbw, "busbw_gbs": busbw,
+                     "frac_of_nvlink_900": busbw / NVLINK_GBS}
+    del rs_out, ag_out
+    out["nccl_algo"] = os.environ.get("NCCL_ALGO", "auto (NCCL's choice; NCCL_DEBUG=INFO names it)")
+    return out
+
+
 def e2e_measure(wl, steps, dist=None):
     """Same metric end to end through the public optimizer API with host buffers: every step copies
     the step's 16-bit gradients host(pinned)->device, runs ResidualSGD/ResidualAdamW.step(), and
@@ -617,13 +661,15 @@ def main():
     _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3000)
+    ap.add_argument("--steps", type=int, default=12000)   # ~1 s timed region (clock samples)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="mpo", choices=["mpo", "reference"])
     ap.add_argument("--workload", default="resnet50_sgd", choices=sorted(WORKLOADS))
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=30)
+    ap.add_argument("--mg-breakdown", action="store_true",
+                    help="run the N>1 update/collective breakdown at world 1 too (code-path check)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -654,11 +700,26 @@ def main():
     value = wl.P / (ms * 1e-3)
     n_upd = wl.layout.shard if world > 1 else wl.P
     alg_bytes = n_upd * wl.bytes_per_param
-    # dominant kernel: at N=1 the step is one launch of the step kernel; at N>1 the per-launch
-    # window also holds the NCCL collectives, so the kernel share is reported from ncu.
+    # dominant kernel: at N=1 the step is one launch of the step kernel; at N>1 the step window
+    # also holds the NCCL collectives, so the kernel's own time comes from the update-only
+    # measurement of multi_gpu_breakdown below.
     achieved = alg_bytes / (per_launch * 1e-3) / 1e9
     e2e = e2e_measure(wl, min(args.e2e_steps, args.steps), dist)
     traffic = ncu_traffic(args.workload)
+    mg = None
+    if world > 1 or args.mg_breakdown:
+        try:
+            if dist is None:   # --mg-breakdown at world 1: the single-rank NCCL group (code-path check)
+                import torch.distributed as tdist
+                wl.step(sharded=True)
+                dist = tdist
+            mg = multi_gpu_breakdown(wl, dist, args.steps, args.warmup)
+            # the step kernel's own launch time on the shard (the whole-step window also holds
+            # the NCCL collectives, reported with their NVLink fractions in multi_gpu)
+            per_launch = mg["update_only"]["ms_per_step"]
+            achieved = alg_bytes / (per_launch * 1e-3) / 1e9
+        except Exception as ex:   # reported, never fatal to the JSON line
+            mg = {"error": f"{type(ex).__name__}: {ex}"}
     line = {
         "metric": "optimizer-step params/sec", "value": value, "unit": "params/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -673,10 +734,12 @@ def main():
                    "l2": f"working set {alg_bytes / 1e6:.0f} MB/step > L2 {L2_BYTES / 2**20:.0f} MiB (no flush)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "step_kernel (reconstruct -> update -> re-split)",
+                     "frac_of_8tbs_spec": achieved / 8000.0,
+                     "kernel": "step_tma_kernel (reconstruct -> update -> re-split)",
                      "algorithmic_bytes_per_launch": alg_bytes, "bytes_per_param": wl.bytes_per_param,
                      "mean_launch_ms": per_launch},
         "gpu_launches": launches,
+        **({"multi_gpu": mg} if mg is not None else {}),
         "clocks": clocks,
         "e2e": e2e,
         "memory": {"persistent_bytes_per_param": wl.persistent_bytes / wl.P,

@@ -526,13 +526,43 @@ __device__ __forceinline__ void process_unit(const uint4& hv, const ResidUnit<SF
     uint32_t hq[4];
     int32_t code[8];
     if constexpr (FM::scheme == kSR) {
+        // Fast unit path when all 8 magnitudes lie in fp16's normal range below the largest finite
+        // value, [2^-14, 65504): there t = RTZ(x) is the top 10 mantissa bits, the spacing U is
+        // 2^13 binary32 patterns, D = the 13 dropped bits, so sr1's rule "up iff rnd < D*2^32/U"
+        // is rnd < D << 19 and the residual is D - up*2^13 -- the same integers as sr1 /
+        // resid_code, without their range branches and the 64-bit division kept for subnormals.
+        uint32_t a[8];
+        bool fast = true;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            uint32_t h0, h1;
-            const uint64_t rr = sr_mix(c.seed, stream, uint64_t(e0 + 2 * q) >> 1);   // e0 is even
-            split1_s<SF>(w[2 * q], static_cast<uint32_t>(rr >> 32), h0, code[2 * q]);
-            split1_s<SF>(w[2 * q + 1], static_cast<uint32_t>(rr), h1, code[2 * q + 1]);
-            hq[q] = h0 | (h1 << 16);
+        for (int k = 0; k < 8; ++k) {
+            a[k] = __float_as_uint(w[k]) & 0x7FFFFFFFu;
+            fast &= (a[k] - 0x38800000u) < (0x477FE000u - 0x38800000u);
+        }
+        if (__builtin_expect(fast, 1)) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint64_t rr = sr_mix(c.seed, stream, uint64_t(e0 + 2 * q) >> 1);   // e0 is even
+                uint32_t hh[2];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int k = 2 * q + j;
+                    const uint32_t rnd = j == 0 ? static_cast<uint32_t>(rr >> 32) : static_cast<uint32_t>(rr);
+                    const uint32_t d = a[k] & 0x1FFFu;
+                    const uint32_t up = rnd < (d << 19) ? 1u : 0u;
+                    hh[j] = ((__float_as_uint(w[k]) >> 16) & 0x8000u) | ((a[k] >> 13) - 0x1C000u + up);
+                    code[k] = static_cast<int32_t>(d) - static_cast<int32_t>(up << 13);
+                }
+                hq[q] = hh[0] | (hh[1] << 16);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t h0, h1;
+                const uint64_t rr = sr_mix(c.seed, stream, uint64_t(e0 + 2 * q) >> 1);   // e0 is even
+                split1_s<SF>(w[2 * q], static_cast<uint32_t>(rr >> 32), h0, code[2 * q]);
+                split1_s<SF>(w[2 * q + 1], static_cast<uint32_t>(rr), h1, code[2 * q + 1]);
+                hq[q] = h0 | (h1 << 16);
+            }
         }
     } else {
         split8_s<SF>(w, hq, code);
