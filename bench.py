@@ -181,6 +181,12 @@ class Workload:
             self.table = mpo.TensorTable(V, R, G, M, W, scheme=scheme)
         self.comm = None
 
+    def release(self):
+        """Drop the device buffers (host-side attributes stay for reporting)."""
+        import torch
+        self.value = self.resid = self.grad = self.m = self.v = self.table = None
+        torch.cuda.empty_cache()
+
     @property
     def clip(self):
         return self.kind == "adam" and self.hpkw.get("max_grad_norm", 0.0) > 0
@@ -303,7 +309,43 @@ def multi_gpu_breakdown(wl, dist, steps, warmup):
                      "frac_of_nvlink_900": busbw / NVLINK_GBS}
     del rs_out, ag_out
     out["nccl_algo"] = os.environ.get("NCCL_ALGO", "auto (NCCL's choice; NCCL_DEBUG=INFO names it)")
+    # the same step fused with its collectives over NVLink peer memory (mpo_p2p_sharded_step on
+    # torch symmetric memory, between symmetric-memory barriers), when the box provides it
+    if not wl.clip:
+        try:
+            out["p2p_fused_step"] = _p2p_fused_timing(wl, dist, steps, warmup)
+        except Exception as ex:
+            out["p2p_fused_step"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
     return out
+
+
+def _p2p_fused_timing(wl, dist, steps, warmup):
+    from paper_2309_12381_b200 import api
+    from paper_2309_12381_b200._lib import MPO_ADAM, MPO_SGD
+    from paper_2309_12381_b200.sharded import _peer_addrs, _rendezvous, _symm_empty
+    L, N, r = wl.layout, wl.world, wl.rank
+    val = _symm_empty(L.total, wl.value.dtype, wl.value.device)
+    grd = _symm_empty(L.total, wl.grad.dtype, wl.grad.device)
+    val.copy_(wl.value)
+    grd.copy_(wl.grad)
+    hv, hg = _rendezvous(val, None), _rendezvous(grd, None)
+    vp, gp = _peer_addrs(hv, val, r), _peer_addrs(hg, grd, r)
+    kind = MPO_ADAM if wl.kind == "adam" else MPO_SGD
+
+    def step():
+        wl.t += 1
+        hg.barrier(channel=0)
+        api.mpo_p2p_sharded_step(kind, r, N, vp, gp, wl.resid, wl.m, wl.v, L.total, wl.hp(), wl.value.dtype,
+                                 scheme=wl.scheme)
+        hv.barrier(channel=0)
+
+    ms, launches = timed(step, steps, warmup, dist)
+    res = {"ms_per_step": ms, "params_per_s": wl.P / (ms * 1e-3), "launches_per_step": launches / steps,
+           "nvlink_bytes_per_rank_per_step": 2 * 2 * L.shard * (N - 1),
+           "note": "one kernel per rank: P2P loads of every rank's grad shard (fp32 sum in rank order), "
+                   "update, P2P stores of the new values into every replica; + 2 symmetric-memory barriers"}
+    del val, grd
+    return res
 
 
 def e2e_measure(wl, steps, dist=None):
@@ -704,7 +746,6 @@ def main():
     # also holds the NCCL collectives, so the kernel's own time comes from the update-only
     # measurement of multi_gpu_breakdown below.
     achieved = alg_bytes / (per_launch * 1e-3) / 1e9
-    e2e = e2e_measure(wl, min(args.e2e_steps, args.steps), dist)
     traffic = ncu_traffic(args.workload)
     mg = None
     if world > 1 or args.mg_breakdown:
@@ -714,12 +755,18 @@ def main():
                 wl.step(sharded=True)
                 dist = tdist
             mg = multi_gpu_breakdown(wl, dist, args.steps, args.warmup)
-            # the step kernel's own launch time on the shard (the whole-step window also holds
-            # the NCCL collectives, reported with their NVLink fractions in multi_gpu)
-            per_launch = mg["update_only"]["ms_per_step"]
-            achieved = alg_bytes / (per_launch * 1e-3) / 1e9
+            if world > 1:
+                # the step kernel's own launch time on the shard (the whole-step window also
+                # holds the NCCL collectives, reported with their NVLink fractions in multi_gpu)
+                per_launch = mg["update_only"]["ms_per_step"]
+                achieved = alg_bytes / (per_launch * 1e-3) / 1e9
         except Exception as ex:   # reported, never fatal to the JSON line
             mg = {"error": f"{type(ex).__name__}: {ex}"}
+    # at N=1 the e2e leg builds its own parameters / optimizer: release this workload's device
+    # buffers first (the LLaMA-7B set would not fit twice); at N>1 it steps this workload
+    if world == 1:
+        wl.release()
+    e2e = e2e_measure(wl, min(args.e2e_steps, args.steps), dist)
     line = {
         "metric": "optimizer-step params/sec", "value": value, "unit": "params/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,

@@ -239,6 +239,36 @@ mpo_status mpo_nvls_sharded_step(mpo_optim kind, int32_t rank, int32_t world, mp
                                  void* resid_shard, float* m_shard, float* v_shard,
                                  int64_t n_total, const void* hp, mpo_stream stream);
 
+/* The sharded step fused with its collectives over NVLink peer memory (the
+ * P2P form; needs no multicast object): one kernel per rank that, for each 8-element unit of its
+ * shard [rank*S, (rank+1)*S), S = n_total/world,
+ *   1. loads the 16-bit gradients of EVERY rank from grad_peers[k] (NVLink P2P loads) and sums
+ *      them in fp32 in rank order, ((g_0 + g_1) + g_2) + ... (deterministic; R15),
+ *   2. reconstructs, updates and re-splits exactly like mpo_sharded_step's shard update, the
+ *      sum entering as an fp32 gradient (times grad_scale: 1/world for a mean),
+ *   3. stores the new 16-bit values into EVERY rank's replica value_peers[k] (P2P stores);
+ *      residual / m / v stay local.
+ * It replaces reduce-scatter + update + all-gather by one launch with no reduced-gradient
+ * buffer; the NVLink traffic per rank equals RS + AG (2 B * S * (world-1) each way).
+ *   value_peers, grad_peers : HOST arrays of `world` device pointers (16-B aligned) to every
+ *                 rank's n_total-element value replica and 16-bit gradient buffer, mapped into
+ *                 this process (CUDA IPC, torch symmetric memory, or, for tests, buffers of the
+ *                 same device); value_peers[rank] / grad_peers[rank] are this rank's own
+ *   resid_shard, m_shard, v_shard : this rank's shard state (S entries; m NULL for SGD without
+ *                 momentum; v ignored for SGD)
+ *   vdt         : any storage format; gradients are its base 16-bit dtype
+ *   world       : 1 .. 8;  n_total : multiple of 8*world
+ *   hp          : mpo_sgd_hp* | mpo_adam_hp* (HOST); no global-norm clipping, no
+ *                 skip_nonfinite (no pre-pass: MPO_EINVAL); clip_value allowed
+ * Stochastic-rounding draws: stream = rank, index inside the shard (as mpo_sharded_step).
+ * The caller orders the call after every rank finished writing its gradients and before any
+ * rank reads values or overwrites gradients again (cross-rank barriers); the kernel ends with
+ * fence.acq_rel.sys. */
+mpo_status mpo_p2p_sharded_step(mpo_optim kind, int32_t rank, int32_t world, mpo_dtype vdt,
+                                void* const* value_peers, const void* const* grad_peers,
+                                void* resid_shard, float* m_shard, float* v_shard,
+                                int64_t n_total, const void* hp, mpo_stream stream);
+
 /* A single-device multicast object bound to fresh device memory (cuMulticastCreate /
  * cuMulticastBindMem), for running the NVLS step at world 1 and in tests.  *uc_ptr / *mc_ptr
  * receive the unicast and multicast addresses of the same bytes; *mapped_bytes the size rounded

@@ -86,6 +86,7 @@ def lib():
                                     C.c_uint64, C.c_uint64]
         L.or_adam_step_s.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, P, P, C.c_int64, C.POINTER(AdamHP),
                                      C.c_float, C.c_uint64, C.c_uint64]
+        L.or_reduce_sum16.argtypes = [C.c_int, C.c_int, P, P, C.c_int64]
         L.or_bytes_per_param.restype = C.c_int
         L.or_bytes_per_param.argtypes = [C.c_int, C.c_int]
         L.or_fpenv_clear()
@@ -192,6 +193,18 @@ def adam_step_master(gfmt, w, grad, m, v, *, lr, beta1=0.9, beta2=0.999, eps=1e-
 def sumsq(gfmt, grad, grad_scale=1.0) -> float:
     _grad_fmt(grad, gfmt)
     return lib().or_sumsq(FMT[gfmt], _ptr(grad), grad.size, grad_scale)
+
+
+def reduce_sum16(fmt: str, grads) -> np.ndarray:
+    """R15: the P2P sharded step's reduction over ranks: each rank's 16-bit gradient
+    widened exactly to binary32 and summed in binary32 in rank order."""
+    gs = [_chk(np.ascontiguousarray(g, dtype=np.uint16), np.uint16) for g in grads]
+    n = gs[0].size
+    assert all(g.size == n for g in gs)
+    arr = (C.c_void_p * len(gs))(*[g.ctypes.data for g in gs])
+    out = np.empty(n, np.float32)
+    lib().or_reduce_sum16(FMT[fmt], len(gs), arr, _ptr(out), n)
+    return out
 
 
 def clip_coef(sumsq_: float, max_norm: float) -> float:

@@ -549,6 +549,23 @@ float or_clip_coef(double sumsq, double max_norm) {
 }
 
 /* ------------------------------------------------------------------------------------- */
+/* Data-parallel gradient reduction of the P2P fused sharded step (BJ north_star (c);     */
+/* reading R15: the sum over ranks of the 16-bit gradients, each widened exactly to        */
+/* binary32 and accumulated in binary32 in rank order, g = ((g_0 + g_1) + g_2) + ...)       */
+/* ------------------------------------------------------------------------------------- */
+
+/* grads: `world` pointers to n 16-bit gradient patterns of format fmt (rank order). */
+void or_reduce_sum16(int fmt, int world, const uint16_t* const* grads, float* out, int64_t n) {
+    int64_t i;
+    int k;
+    for (i = 0; i < n; i++) {
+        float s = u2f(or_widen16(fmt, grads[0][i]));
+        for (k = 1; k < world; k++) s = s + u2f(or_widen16(fmt, grads[k][i]));
+        out[i] = s;
+    }
+}
+
+/* ------------------------------------------------------------------------------------- */
 /* Per-parameter byte accounting (reading R11)                                   */
 /* ------------------------------------------------------------------------------------- */
 

@@ -6,12 +6,13 @@ driver (``sharded``).  Importing it does not touch the GPU; calling into it with
 library raises (there is no CPU fallback).
 """
 from .api import (AdamParams, SgdParams, TensorTable, mpo_adam_step, mpo_fused_backward_hook_step,  # noqa: F401
-                  mpo_reconstruct, mpo_sgd_step, mpo_sharded_step, mpo_split, norm_ws_doubles)
+                  mpo_p2p_sharded_step, mpo_reconstruct, mpo_sgd_step, mpo_sharded_step, mpo_split,
+                  norm_ws_doubles)
 from ._lib import MpoError  # noqa: F401
 from .optim import ResidualAdamW, ResidualSGD  # noqa: F401
 from .sharded import BucketedShardedOptimizer, BucketLayout, ShardedResidualOptimizer, ShardLayout  # noqa: F401
 
 __all__ = ["mpo_split", "mpo_reconstruct", "mpo_sgd_step", "mpo_adam_step", "mpo_fused_backward_hook_step",
-           "mpo_sharded_step", "TensorTable", "SgdParams", "AdamParams", "ResidualSGD", "ResidualAdamW",
+           "mpo_sharded_step", "mpo_p2p_sharded_step", "TensorTable", "SgdParams", "AdamParams", "ResidualSGD", "ResidualAdamW",
            "ShardedResidualOptimizer", "ShardLayout", "BucketedShardedOptimizer", "BucketLayout", "MpoError",
            "norm_ws_doubles"]

@@ -25,7 +25,7 @@ MPO_MAX_HP_GROUPS = 16
 SYMBOLS = ("mpo_split", "mpo_reconstruct", "mpo_sgd_step", "mpo_adam_step", "mpo_norm_ws_doubles",
            "mpo_fused_backward_hook_step", "mpo_sharded_step", "mpo_last_error", "mpo_build_exact",
            "mpo_launch_count", "mpo_selfcheck_fastmath", "mpo_nvls_sharded_step", "mpo_nvls_alloc_local",
-           "mpo_nvls_free_local")
+           "mpo_nvls_free_local", "mpo_p2p_sharded_step")
 
 
 class MpoError(RuntimeError):
@@ -83,6 +83,8 @@ def _declare(L):
     L.mpo_nvls_alloc_local.restype = C.c_int
     L.mpo_nvls_free_local.argtypes = [P, P, I64]
     L.mpo_nvls_free_local.restype = C.c_int
+    L.mpo_p2p_sharded_step.argtypes = [D, I32, I32, D, P, P, P, P, P, I64, P, P]
+    L.mpo_p2p_sharded_step.restype = C.c_int
 
 
 def load(exact: bool = False):

@@ -275,6 +275,25 @@ def mpo_selfcheck_fastmath(pairs: int = 1 << 30, seed: int = 0xB0B, exact: bool 
     return tuple(int(x) for x in counts.cpu())
 
 
+def mpo_p2p_sharded_step(kind: int, rank: int, world: int, value_peers: Sequence[int], grad_peers: Sequence[int],
+                         resid_shard: torch.Tensor, m_shard: Optional[torch.Tensor], v_shard: Optional[torch.Tensor],
+                         n_total: int, hp, value_dtype: torch.dtype, stream=None, exact: bool = False,
+                         scheme: str = "rne"):
+    """The sharded step fused with its collectives over NVLink peer memory (include/mpo.h): one
+    kernel reads every rank's gradient shard (P2P), updates, and writes the new values into every
+    rank's replica.  value_peers / grad_peers: raw device addresses (ints) of every rank's value
+    replica and gradient buffer, mapped into this process (rank order)."""
+    if len(value_peers) != world or len(grad_peers) != world:
+        raise MpoError(_lib.MPO_EINVAL, "need one value and one gradient address per rank")
+    L = _lib_of(exact)
+    chp = hp.c() if hasattr(hp, "c") else hp
+    vp = (C.c_void_p * world)(*[C.c_void_p(int(a)) for a in value_peers])
+    gp = (C.c_void_p * world)(*[C.c_void_p(int(a)) for a in grad_peers])
+    _lib.check(L, L.mpo_p2p_sharded_step(kind, rank, world, format_code(value_dtype, scheme), vp, gp,
+                                         _ptr(resid_shard), _ptr(m_shard), _ptr(v_shard), n_total, C.byref(chp),
+                                         _stream(stream)))
+
+
 def mpo_nvls_sharded_step(kind: int, rank: int, world: int, vdt: int, value_mc: int, value_uc: int, grad_mc: int,
                           resid_shard: torch.Tensor, m_shard: Optional[torch.Tensor], v_shard: Optional[torch.Tensor],
                           n_total: int, hp, stream=None, exact: bool = False):

@@ -550,6 +550,67 @@ MPO_API mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t
 }
 
 
+MPO_API mpo_status mpo_p2p_sharded_step(mpo_optim kind, int32_t rank, int32_t world, mpo_dtype vdt,
+                                        void* const* value_peers, const void* const* grad_peers, void* resid_shard,
+                                        float* m_shard, float* v_shard, int64_t n_total, const void* hp,
+                                        mpo_stream stream) {
+    g_err.clear();
+    mpo_status st;
+    if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+        return fail(MPO_EINVAL, "bad rank / world (1 <= world <= 8)");
+    if (n_total < 0 || n_total % (int64_t(8) * world) != 0)
+        return fail(MPO_EINVAL, "n_total must be a non-negative multiple of 8*world");
+    if (!hp) return fail(MPO_EINVAL, "NULL hyper-parameters");
+    if (!is_value_format(vdt)) return fail(MPO_EDTYPE, "unsupported storage format");
+    const mpo_dtype gdt = mpo_dtype(base_of(vdt));
+    if ((st = check_dtypes(vdt, gdt)) != MPO_OK) return st;
+    if (kind != MPO_SGD && kind != MPO_ADAM) return fail(MPO_EINVAL, "unknown optimizer kind");
+    if (n_total == 0) return MPO_OK;
+    if (!value_peers || !grad_peers) return fail(MPO_EINVAL, "NULL peer pointer array");
+    Peers peers{};
+    for (int k = 0; k < world; ++k) {
+        if (!value_peers[k] || !grad_peers[k]) return fail(MPO_EINVAL, "NULL peer buffer (rank " + std::to_string(k) + ")");
+        if (!aligned16(value_peers[k]) || !aligned16(grad_peers[k]))
+            return fail(MPO_EALIGN, "peer buffer not 16-byte aligned (rank " + std::to_string(k) + ")");
+        peers.g[k] = static_cast<const uint16_t*>(grad_peers[k]);
+        peers.v[k] = static_cast<uint16_t*>(value_peers[k]);
+    }
+    const int64_t shard = n_total / world;
+    mpo_tensor x;   // this rank's shard, for the common table validation
+    x.value = static_cast<uint16_t*>(value_peers[rank]) + rank * shard;
+    x.resid = resid_shard;
+    x.grad = static_cast<const uint16_t*>(grad_peers[rank]) + rank * shard;
+    x.m = m_shard;
+    x.v = v_shard;
+    x.n = shard;
+    x.hp = 0;
+    x.sr_stream = rank;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (kind == MPO_ADAM) {
+        const mpo_adam_hp* h = static_cast<const mpo_adam_hp*>(hp);
+        if ((st = check_adam_hp(h, 1)) != MPO_OK) return st;
+        if (h->max_grad_norm > 0.0 || h->skip_nonfinite)
+            return fail(MPO_EINVAL, "the P2P step has no norm pre-pass (max_grad_norm / skip_nonfinite)");
+        if ((st = check_table(&x, 1, 1, true, nullptr)) != MPO_OK) return st;
+        const AdamK k = derive_adam(*h);
+#define X(F) \
+    if (vdt == F) return FormatOps<F>::p2p(kind, peers, world, rank, resid_shard, m_shard, v_shard, rank * shard, shard, nullptr, &k, s);
+        MPO_FORMATS(X)
+#undef X
+    } else {
+        const mpo_sgd_hp* h = static_cast<const mpo_sgd_hp*>(hp);
+        if ((st = check_sgd_hp(h, 1)) != MPO_OK) return st;
+        if (h->skip_nonfinite) return fail(MPO_EINVAL, "the P2P step has no norm pre-pass (skip_nonfinite)");
+        if ((st = check_table(&x, 1, 1, false, h)) != MPO_OK) return st;
+        const SgdK k = derive_sgd(*h);
+#define X(F) \
+    if (vdt == F) return FormatOps<F>::p2p(kind, peers, world, rank, resid_shard, m_shard, nullptr, rank * shard, shard, &k, nullptr, s);
+        MPO_FORMATS(X)
+#undef X
+    }
+    return fail(MPO_EDTYPE, "unsupported storage format");
+}
+
 // ------------------------------------------------------------------------------------------
 // NVLS (NVLink SHARP) fused sharded step and a single-device multicast allocator for tests
 // ------------------------------------------------------------------------------------------

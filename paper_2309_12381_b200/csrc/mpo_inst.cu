@@ -72,4 +72,18 @@ mpo_status FormatOps<SF>::nvls(int kind, void* value_mc, const void* value_uc, c
     return check_launch("nvls_step_kernel");
 }
 
+template <>
+mpo_status FormatOps<SF>::p2p(int kind, const Peers& peers, int world, int rank, void* resid, float* m, float* v,
+                              int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak, cudaStream_t s) {
+    const int64_t grid = grid_for((n / kUnitEl + kThreads - 1) / kThreads, 8);
+    if (kind == MPO_ADAM)
+        p2p_step_kernel<SF, AdamOp><<<unsigned(grid), kThreads, 0, s>>>(peers, world, rank, resid, m, v, shard_base, n,
+                                                                         *ak);
+    else
+        p2p_step_kernel<SF, SgdOp><<<unsigned(grid), kThreads, 0, s>>>(peers, world, rank, resid, m, v, shard_base, n,
+                                                                        *sk);
+    ++g_launches;
+    return check_launch("p2p_step_kernel");
+}
+
 }  // namespace mpo

@@ -1149,6 +1149,93 @@ __global__ void __launch_bounds__(kThreads) nvls_step_kernel(uint16_t* __restric
     asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
+// ---- sharded step fused with its collectives over NVLink peer memory (P2P loads / stores) ----
+// Rank r owns elements [r*S, (r+1)*S) of the flat buffers.  Per 8-element unit of its shard the
+// kernel loads the 16-bit gradients of EVERY rank straight from their buffers (NVLink P2P loads;
+// rank order, fp32 accumulation: g = ((g_0 + g_1) + g_2) + ..., deterministic and one rounding
+// path), runs the same reconstruct -> update -> re-split as every other entry point (the summed
+// gradient enters as an fp32 gradient), keeps residual / m / v local, and stores the new 16-bit
+// values into EVERY rank's replica (P2P stores).  This is the reduce-scatter + update +
+// all-gather of mpo_sharded_step as one kernel: no collective launches, no reduced-gradient
+// buffer, and the NVLink transfers overlap the arithmetic unit by unit.
+constexpr int kMaxPeers = 8;
+struct Peers {
+    const uint16_t* g[kMaxPeers];
+    uint16_t* v[kMaxPeers];
+};
+
+template <int SF, class Op>
+__global__ void __launch_bounds__(kThreads) p2p_step_kernel(const __grid_constant__ Peers P, int world, int rank,
+                                                            void* resid, float* __restrict__ m, float* __restrict__ v,
+                                                            int64_t shard_base, int64_t n,
+                                                            const __grid_constant__ typename Op::K c) {
+    constexpr int B = Fmt<SF>::base;
+    const bool need_m = Op::reads_m(c), has_m = Op::writes_m(c);
+    const int64_t nunits = n / kUnitEl;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < nunits; u += stride) {
+        const int64_t e = u * kUnitEl;                      // index inside the shard
+        uint4 gk[kMaxPeers];
+#pragma unroll
+        for (int k = 0; k < kMaxPeers; ++k)
+            if (k < world) gk[k] = ldv(P.g[k] + shard_base + e);   // all loads in flight first
+        float gsum[8];
+        GradUnit<B> g0;
+        g0.a = gk[0];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) gsum[i] = grad_at<B>(g0, i);
+#pragma unroll
+        for (int k = 1; k < kMaxPeers; ++k) {
+            if (k < world) {
+                GradUnit<B> gx;
+                gx.a = gk[k];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) gsum[i] = gsum[i] + grad_at<B>(gx, i);
+            }
+        }
+        GradUnit<kFP32> gu;
+        gu.a = make_uint4(__float_as_uint(gsum[0]), __float_as_uint(gsum[1]), __float_as_uint(gsum[2]),
+                          __float_as_uint(gsum[3]));
+        gu.b = make_uint4(__float_as_uint(gsum[4]), __float_as_uint(gsum[5]), __float_as_uint(gsum[6]),
+                          __float_as_uint(gsum[7]));
+        const uint4 hv = ldv(P.v[rank] + shard_base + e);
+        const ResidUnit<SF> rv = ld_resid<SF>(resid, e);
+        float mm[8], vv[8];
+        if (need_m) {
+            const float4 a = ldf(m + e), b = ldf(m + e + 4);
+            mm[0] = a.x; mm[1] = a.y; mm[2] = a.z; mm[3] = a.w; mm[4] = b.x; mm[5] = b.y; mm[6] = b.z; mm[7] = b.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mm[k] = 0.0f;
+        }
+        if constexpr (Op::kHasV) {
+            const float4 a = ldf(v + e), b = ldf(v + e + 4);
+            vv[0] = a.x; vv[1] = a.y; vv[2] = a.z; vv[3] = a.w; vv[4] = b.x; vv[5] = b.y; vv[6] = b.z; vv[7] = b.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) vv[k] = 0.0f;
+        }
+        uint4 ho;
+        ResidUnit<SF> ro;
+        // stochastic-rounding draws keyed like mpo_sharded_step: stream = rank, index in the shard
+        process_unit<SF, kFP32, Op, false>(hv, rv, gu, mm, vv, c, 1.0f, uint32_t(rank), e, ho, ro);
+#pragma unroll
+        for (int k = 0; k < kMaxPeers; ++k)
+            if (k < world) stv(P.v[k] + shard_base + e, ho);    // every rank's replica
+        st_resid<SF>(resid, e, ro);
+        if (has_m) {
+            stf(m + e, make_float4(mm[0], mm[1], mm[2], mm[3]));
+            stf(m + e + 4, make_float4(mm[4], mm[5], mm[6], mm[7]));
+        }
+        if constexpr (Op::kHasV) {
+            stf(v + e, make_float4(vv[0], vv[1], vv[2], vv[3]));
+            stf(v + e + 4, make_float4(vv[4], vv[5], vv[6], vv[7]));
+        }
+    }
+    // peer stores visible system-wide before the caller's cross-rank barrier
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
 // ------------------------------------------------------------------------------------------
 // Host launch templates
 // ------------------------------------------------------------------------------------------
@@ -1212,6 +1299,8 @@ struct FormatOps {
     static mpo_status reconstruct(const void* value, const void* resid, float* w, int64_t n, cudaStream_t s);
     static mpo_status nvls(int kind, void* value_mc, const void* value_uc, const void* grad_mc, void* resid, float* m,
                            float* v, int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak, cudaStream_t s);
+    static mpo_status p2p(int kind, const Peers& peers, int world, int rank, void* resid, float* m, float* v,
+                          int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak, cudaStream_t s);
 };
 
 }  // namespace mpo

@@ -71,17 +71,52 @@ def nccl_comm_ptr(group=None) -> int:
     return int(pg._get_backend(torch.device("cuda"))._comm_ptr())
 
 
+def _symm_empty(n: int, dtype: torch.dtype, device) -> torch.Tensor:
+    import torch.distributed._symmetric_memory as symm
+    return symm.empty(n, dtype=dtype, device=device)
+
+
+def _rendezvous(t: torch.Tensor, group):
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+    pg = group if group is not None else dist.group.WORLD
+    name = pg.group_name
+    try:
+        return symm.rendezvous(t, name)
+    except Exception:
+        if not hasattr(symm, "enable_symm_mem_for_group"):
+            raise
+        symm.enable_symm_mem_for_group(name)   # older torch needs the opt-in
+        return symm.rendezvous(t, name)
+
+
+def _peer_addrs(h, t: torch.Tensor, rank: int) -> List[int]:
+    """Device addresses of every rank's copy of the symmetric tensor t, in rank order."""
+    ptrs = list(h.buffer_ptrs)
+    off = t.data_ptr() - int(ptrs[rank])
+    return [int(p) + off for p in ptrs]
+
+
 class ShardedResidualOptimizer:
     """Sharded residual-compensated Adam/AdamW (``kind='adam'``) or SGD-momentum (``kind='sgd'``).
 
     ``params``: CUDA parameters (fp32 -> split into ``fmt``; 16-bit -> residual 0).  They are
     re-pointed at views of one flat value buffer and their ``.grad`` at views of one flat
-    gradient buffer, which backward accumulates into."""
+    gradient buffer, which backward accumulates into.
+
+    ``transport='nccl'`` (default): ``mpo_sharded_step`` (NCCL reduce-scatter -> shard update ->
+    NCCL all-gather).  ``transport='p2p'``: value and gradient buffers live in torch symmetric
+    memory and one ``mpo_p2p_sharded_step`` kernel per rank reads every rank's gradient shard and
+    writes the new values into every rank's replica over NVLink (no collective launches; no
+    global-norm clipping)."""
 
     def __init__(self, params, kind: str = "adam", fmt: Optional[torch.dtype] = None, group=None,
                  hp=None, exact: bool = False, comm_ptr: Optional[int] = None, scheme: str = "rne",
-                 seed: int = 0):
+                 seed: int = 0, transport: str = "nccl"):
         import torch.distributed as dist
+        if transport not in ("nccl", "p2p"):
+            raise MpoError(1, "transport must be 'nccl' or 'p2p'")
+        self.transport = transport
         self.params = [p for p in params]
         if not self.params:
             raise MpoError(1, "no parameters")
@@ -107,10 +142,23 @@ class ShardedResidualOptimizer:
             # 16-bit params are exactly representable: their residual is zero (P1)
             pass
         del src
-        self.value = value
         self.resid = resid[lo:hi].clone()
         del resid
-        self.grad = torch.zeros(L.total, dtype=vdt, device=dev)
+        if transport == "p2p":
+            # value replica and gradient buffer in symmetric memory: every rank maps every peer's
+            # buffers, and mpo_p2p_sharded_step reads / writes them over NVLink
+            self.value = _symm_empty(L.total, vdt, dev)
+            self.value.copy_(value)
+            self.grad = _symm_empty(L.total, vdt, dev)
+            self.grad.zero_()
+            self._hv = _rendezvous(self.value, group)
+            self._hg = _rendezvous(self.grad, group)
+            self._vpeers = _peer_addrs(self._hv, self.value, self.rank)
+            self._gpeers = _peer_addrs(self._hg, self.grad, self.rank)
+        else:
+            self.value = value
+            self.grad = torch.zeros(L.total, dtype=vdt, device=dev)
+        del value
         need_m = self.kind == MPO_ADAM or (hp is not None and getattr(hp, "momentum", 0.0) != 0.0)
         self.m = torch.zeros(L.shard, dtype=torch.float32, device=dev) if need_m else None
         self.v = torch.zeros(L.shard, dtype=torch.float32, device=dev) if self.kind == MPO_ADAM else None
@@ -122,7 +170,9 @@ class ShardedResidualOptimizer:
         self.hp = hp if hp is not None else (api.AdamParams(lr=1e-3) if self.kind == MPO_ADAM
                                              else api.SgdParams(lr=1e-2))
         self.step_count = 0
-        self.comm = comm_ptr if comm_ptr is not None else nccl_comm_ptr(group)
+        if transport == "p2p" and getattr(self.hp, "max_grad_norm", 0.0) > 0:
+            raise MpoError(1, "the P2P fused step has no norm pre-pass: use transport='nccl' for max_grad_norm")
+        self.comm = None if transport == "p2p" else (comm_ptr if comm_ptr is not None else nccl_comm_ptr(group))
 
     def zero_grad(self):
         self.grad.zero_()
@@ -136,6 +186,15 @@ class ShardedResidualOptimizer:
         else:
             hp.first_step = self.step_count == 1
         hp.seed = api.step_seed(self.seed, self.step_count)
+        if self.transport == "p2p":
+            # every rank's gradients are complete before any rank reads them, and every rank's
+            # new values are in place before any rank reads its replica again
+            self._hg.barrier(channel=0)
+            api.mpo_p2p_sharded_step(self.kind, self.rank, self.world, self._vpeers, self._gpeers, self.resid,
+                                     self.m, self.v, self.layout.total, hp, self.value.dtype, exact=self.exact,
+                                     scheme=self.scheme)
+            self._hv.barrier(channel=0)
+            return
         api.mpo_sharded_step(self.kind, self.comm, self.rank, self.world, self.value, self.grad, self.resid, self.m,
                              self.v, hp, norm_ws=self.norm_ws if getattr(hp, "max_grad_norm", 0.0) > 0 else None,
                              exact=self.exact, scheme=self.scheme)

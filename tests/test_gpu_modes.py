@@ -211,6 +211,44 @@ def test_sharded_world1_equals_unsharded(mpo, nccl1, kind, clip):
         assert torch.equal(a.data.view(torch.int16), b.data.view(torch.int16))
 
 
+@pytest.mark.parametrize("kind", ["adam", "sgd"])
+def test_sharded_p2p_transport_world1_equals_nccl(mpo, nccl1, kind):
+    """transport='p2p' (torch symmetric memory + mpo_p2p_sharded_step between symmetric-memory
+    barriers) == transport='nccl' bitwise at world 1 in the exact build (the fp32 sum of one
+    rank's gradient is its exact widening, R15)."""
+    try:
+        import torch.distributed._symmetric_memory as symm
+        t = symm.empty(16, dtype=torch.bfloat16, device="cuda")
+        from paper_2309_12381_b200.sharded import _rendezvous
+        _rendezvous(t, None)
+    except Exception as e:   # pragma: no cover - depends on the box
+        pytest.skip(f"torch symmetric memory unavailable here: {type(e).__name__}: {e}")
+    torch.manual_seed(5)
+    shapes = [(33, 17), (4096,), (5,), (128, 64)]
+    src = [torch.randn(s, device="cuda") * 0.02 for s in shapes]
+    pa = [nn.Parameter(t.clone()) for t in src]
+    pb = [nn.Parameter(t.clone()) for t in src]
+    if kind == "adam":
+        mk = lambda: mpo.AdamParams(lr=1e-3, weight_decay=0.1)
+    else:
+        mk = lambda: mpo.SgdParams(lr=0.1, momentum=0.9)
+    # exact builds: the two kernels are different instantiations (16-bit vs fp32 gradient ingest),
+    # which the FMA build may contract differently (R12)
+    a = mpo.ShardedResidualOptimizer(pa, kind=kind, fmt=torch.bfloat16, hp=mk(), exact=True)
+    b = mpo.ShardedResidualOptimizer(pb, kind=kind, fmt=torch.bfloat16, hp=mk(), transport="p2p", exact=True)
+    for t in range(3):
+        grads = [torch.randn(s, device="cuda").to(torch.bfloat16) * 1e-2 for s in shapes]
+        for opt, ps in ((a, pa), (b, pb)):
+            opt.zero_grad()
+            for p, g in zip(ps, grads):
+                p.grad.copy_(g)
+            opt.step()
+    torch.cuda.synchronize()
+    for x, y in zip(pa, pb):
+        assert torch.equal(x.data.view(torch.int16), y.data.view(torch.int16))
+    assert torch.equal(a.resid, b.resid)
+
+
 # ---------------------------------------------------------------------------------------------
 # Gradient surgery through the optimizer (P:91, P:186-193): clip-by-value, loss-scale found-inf
 # ---------------------------------------------------------------------------------------------
@@ -402,3 +440,86 @@ def test_hook_mode_optimizer_is_collectable(mpo):
     torch.cuda.synchronize()
     assert ref() is None
     assert torch.cuda.memory_allocated() - base < 1 << 16
+
+
+def _kw_adam(hp):
+    return dict(lr=hp.lr, beta1=hp.beta1, beta2=hp.beta2, eps=hp.eps, weight_decay=hp.weight_decay,
+                adamw=hp.adamw, grad_scale=hp.grad_scale, step=hp.step)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("kind,fmt,scheme", [("adam", "bf16", "rne"), ("sgd", "fp16", "rne"),
+                                             ("adam", "fp16", "sr"), ("adam", "bf16", "x8")])
+def test_p2p_fused_sharded_step_emulated_peers(mpo, orc, world, kind, fmt, scheme):
+    """SURVEY 8(f) row 1, P2P form: `world` ranks emulated on one device (each with its own
+    gradient buffer and value replica; the kernel of rank r reads every rank's gradient shard r
+    and writes its new values into every replica).  After all ranks stepped, every replica and
+    every shard's residual / m / v equal the oracle: reduce_sum16 (R15) of the ranks' gradients,
+    then the oracle step of the shard with grad_scale 1/world (exact build, bit-exact)."""
+    from paper_2309_12381_b200 import api
+    from paper_2309_12381_b200._lib import MPO_ADAM, MPO_SGD
+    from gpu_util import TDT
+    S = 8 * (3 * 4096 // 8 + 5)                 # shard: several units past a ragged thread count
+    n = S * world
+    w = synth.weights(n, 0.02, 7)
+    h, r = orc.split_s(scheme, fmt, w, seed=3, stream=0)
+    gs = [synth.grads(n, 1e-2, fmt, 0xC0FFEE, k) for k in range(world)]
+    rdt = torch.int8 if scheme == "x8" else torch.int16
+    tdt = TDT[fmt]
+    V = [torch.from_numpy(h.view(np.int16).copy()).view(tdt).cuda() for _ in range(world)]   # replicas
+    G = [torch.from_numpy(g.view(np.int16).copy()).view(tdt).cuda() for g in gs]
+    Rs, Ms, Ws = [], [], []
+    ms = [synth.normal_f32(S, 1e-3, 5, k) for k in range(world)]
+    vs = [np.abs(synth.normal_f32(S, 1e-5, 6, k)) for k in range(world)]
+    for k in range(world):
+        rk = r[k * S:(k + 1) * S].copy()
+        Rs.append(torch.from_numpy(rk.view(np.int8) if scheme == "x8" else rk.view(np.int16)).cuda().view(rdt))
+        Ms.append(torch.from_numpy(ms[k].copy()).cuda())
+        Ws.append(torch.from_numpy(vs[k].copy()).cuda())
+    seed = 1234
+    if kind == "adam":
+        hp = mpo.AdamParams(lr=1e-3, weight_decay=0.1, step=4, grad_scale=1.0 / world, seed=seed)
+    else:
+        hp = mpo.SgdParams(lr=0.1, momentum=0.9, weight_decay=1e-4, grad_scale=1.0 / world, seed=seed)
+    vp = [t.data_ptr() for t in V]
+    gp = [t.data_ptr() for t in G]
+    for k in range(world):
+        api.mpo_p2p_sharded_step(MPO_ADAM if kind == "adam" else MPO_SGD, k, world, vp, gp, Rs[k], Ms[k],
+                                 Ws[k] if kind == "adam" else None, n, hp, tdt, exact=True, scheme=scheme)
+    torch.cuda.synchronize()
+    for k in range(world):
+        sl = slice(k * S, (k + 1) * S)
+        gsum = orc.reduce_sum16(fmt, [g[sl] for g in gs])
+        hk, rk = h[sl].copy(), r[sl].copy()
+        if kind == "adam":
+            orc.adam_step_s(scheme, fmt, "fp32", hk, rk, gsum, ms[k], vs[k], seed=seed, stream=k, **_kw_adam(hp))
+        else:
+            orc.sgd_step_s(scheme, fmt, "fp32", hk, rk, gsum, ms[k], lr=hp.lr, momentum=hp.momentum,
+                           weight_decay=hp.weight_decay, grad_scale=hp.grad_scale, seed=seed, stream=k)
+        for rep in V:
+            assert np.array_equal(host16(rep)[sl], hk), (k, "value replica")
+        got_r = Rs[k].cpu().numpy()
+        assert np.array_equal(got_r.view(rk.dtype) if scheme != "x8" else got_r, rk), (k, "residual")
+        assert np.array_equal(Ms[k].cpu().numpy().view(np.uint32), ms[k].view(np.uint32)), (k, "m")
+        if kind == "adam":
+            assert np.array_equal(Ws[k].cpu().numpy().view(np.uint32), vs[k].view(np.uint32)), (k, "v")
+    assert all(np.array_equal(host16(G[k]), gs[k]) for k in range(world))
+
+
+def test_p2p_fused_sharded_step_rejects(mpo):
+    from paper_2309_12381_b200 import api
+    from paper_2309_12381_b200._lib import MPO_ADAM
+    n = 64
+    v = torch.zeros(n, dtype=torch.bfloat16, device="cuda")
+    g = torch.zeros(n, dtype=torch.bfloat16, device="cuda")
+    R = torch.zeros(n, dtype=torch.int16, device="cuda")
+    M = torch.zeros(n, device="cuda"); W = torch.zeros(n, device="cuda")
+    with pytest.raises(mpo.MpoError, match="pre-pass"):
+        api.mpo_p2p_sharded_step(MPO_ADAM, 0, 1, [v.data_ptr()], [g.data_ptr()], R, M, W, n,
+                                 mpo.AdamParams(lr=1e-3, max_grad_norm=1.0), torch.bfloat16)
+    with pytest.raises(mpo.MpoError, match="world"):
+        api.mpo_p2p_sharded_step(MPO_ADAM, 0, 9, [v.data_ptr()] * 9, [g.data_ptr()] * 9, R, M, W, 72 * 9,
+                                 mpo.AdamParams(lr=1e-3), torch.bfloat16)
+    with pytest.raises(mpo.MpoError, match="8\\*world"):
+        api.mpo_p2p_sharded_step(MPO_ADAM, 0, 2, [v.data_ptr()] * 2, [g.data_ptr()] * 2, R, M, W, 60,
+                                 mpo.AdamParams(lr=1e-3), torch.bfloat16)

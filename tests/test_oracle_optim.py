@@ -314,3 +314,46 @@ def test_clip_value_in_residual_steps_matches_master(orc):
         lossy = (r == 32767)
         assert np.array_equal(rec.view(np.uint32)[~lossy], wm.view(np.uint32)[~lossy])
         assert np.array_equal(m, mm)
+
+
+# ------------------------------------------------------------------------------------------
+# R15: reduction over ranks of the P2P fused sharded step (BJ north_star (c))
+# ------------------------------------------------------------------------------------------
+def test_reduce_sum16_world1_is_the_exact_widening(orc):
+    """One rank: the 'sum' is the gradient widened to binary32, i.e. numpy's own exact
+    float16 -> float32 cast (library routine), over all 2^16 fp16 patterns."""
+    h = np.arange(1 << 16, dtype=np.uint32).astype(np.uint16)
+    out = orc.reduce_sum16("fp16", [h])
+    ref = h.view(np.float16).astype(np.float32)
+    nan = np.isnan(ref)
+    assert np.array_equal(np.isnan(out), nan)
+    assert np.array_equal(out[~nan].view(np.uint32), ref[~nan].view(np.uint32))
+
+
+def test_reduce_sum16_exact_when_no_rounding_and_bound_otherwise(orc):
+    """Exact-sum construction: multiples of 2^-10 below 2^10 summed over 8 ranks are exact in
+    binary32, so the result equals math.fsum of the widened values.  Random gradients: the error
+    of recursive summation obeys |s - exact| <= (W-1) u sum|g_k| (u = 2^-24, Higham)."""
+    import math
+    rng = np.random.default_rng(2023)
+    W, n = 8, 4096
+    ks = [rng.integers(-2 ** 20, 2 ** 20, n) for _ in range(W)]
+    gs = [(k.astype(np.float64) * 2.0 ** -10).astype(np.float16).view(np.uint16) for k in ks]
+    exact = np.array([math.fsum(float(g.view(np.float16)[i]) for g in gs) for i in range(n)])
+    out = orc.reduce_sum16("fp16", gs)
+    assert np.array_equal(out.astype(np.float64), exact)
+    gs = [rng.normal(0, 1, n).astype(np.float16).view(np.uint16) for _ in range(W)]
+    wid = [g.view(np.float16).astype(np.float64) for g in gs]
+    exact = np.array([math.fsum(w[i] for w in wid) for i in range(n)])
+    bound = (W - 1) * 2.0 ** -24 * np.sum(np.abs(np.stack(wid)), axis=0)
+    out = orc.reduce_sum16("fp16", gs).astype(np.float64)
+    assert np.all(np.abs(out - exact) <= bound)
+    assert np.any(out != exact)          # rounding really happens: the test is not vacuous
+
+
+def test_reduce_sum16_is_in_rank_order(orc):
+    """bf16: 2^24 + 1 + 1 in binary32 is 2^24 in rank order ((2^24 + 1) ties to even), but
+    2^24 + 2 if the two ones were added first: the oracle adds in rank order."""
+    big, one = np.array([0x4B80], np.uint16), np.array([0x3F80], np.uint16)   # 2^24, 1.0 in bf16
+    assert orc.reduce_sum16("bf16", [big, one, one])[0] == np.float32(2.0 ** 24)
+    assert orc.reduce_sum16("bf16", [one, one, big])[0] == np.float32(2.0 ** 24 + 2)
