@@ -34,5 +34,17 @@ opt = mpo.ResidualAdamW(model.parameters(), lr=1e-3, fmt=torch.bfloat16, skip_no
 opt.install_backward_hooks()
 model(torch.randn(4, 32, device=dev, dtype=torch.bfloat16)).float().sum().backward()
 opt.found_inf()
+# P2P fused sharded step, 2 ranks emulated on this device (separate grad buffers / replicas)
+from paper_2309_12381_b200 import api  # noqa: E402
+from paper_2309_12381_b200._lib import MPO_ADAM  # noqa: E402
+n, W2 = 2 * 4104, 2
+reps = [(torch.randn(n, device=dev) * 0.02).to(torch.bfloat16) for _ in range(W2)]
+reps[1].copy_(reps[0])
+grads = [(torch.randn(n, device=dev) * 1e-2).to(torch.bfloat16) for _ in range(W2)]
+for k in range(W2):
+    S = n // W2
+    api.mpo_p2p_sharded_step(MPO_ADAM, k, W2, [t.data_ptr() for t in reps], [t.data_ptr() for t in grads],
+                             torch.zeros(S, dtype=torch.int16, device=dev), torch.zeros(S, device=dev),
+                             torch.zeros(S, device=dev), n, mpo.AdamParams(lr=1e-3, step=1), torch.bfloat16)
 torch.cuda.synchronize()
 print("sanitize run ok")
