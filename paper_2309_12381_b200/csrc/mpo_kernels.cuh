@@ -127,6 +127,14 @@ __device__ __forceinline__ uint4 ldv(const void* p) { return __ldcs(reinterpret_
 __device__ __forceinline__ float4 ldf(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ void stv(void* p, uint4 x) { __stcs(reinterpret_cast<uint4*>(p), x); }
 __device__ __forceinline__ void stf(float* p, float4 x) { __stcs(reinterpret_cast<float4*>(p), x); }
+// 8 fp32 of one unit (m, v, reconstructed w): two 128-bit streaming stores.  (sm_100's 256-bit
+// st.global.v8.f32 -- SASS STG.E.EF.ENL2.256 -- makes each warp store cover whole sectors instead
+// of half sectors at a 32-B thread stride, but measured -0.5 % ResNet-50 / +0.5 % GPT-2 / -2 %
+// LLaMA-7B: L2 merges the halves before write-back; profiles/r01_ab13_st256.log.)
+__device__ __forceinline__ void stf8(float* p, const float (&x)[8]) {
+    stf(p, make_float4(x[0], x[1], x[2], x[3]));
+    stf(p + 4, make_float4(x[4], x[5], x[6], x[7]));
+}
 
 // 8 gradient values of a unit.
 template <int G>
@@ -318,8 +326,7 @@ __global__ void __launch_bounds__(kThreads) reconstruct_kernel(const uint16_t* _
         float o[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) o[k] = reconstruct1_s<SF>((k & 1) ? hi16(h[k >> 1]) : lo16(h[k >> 1]), code_at<SF>(rv, k));
-        stf(w + e, make_float4(o[0], o[1], o[2], o[3]));
-        stf(w + e + 4, make_float4(o[4], o[5], o[6], o[7]));
+        stf8(w + e, o);
     }
     const int64_t t = nunits * kUnitEl + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t < n && t < nunits * kUnitEl + kUnitEl) {
@@ -606,12 +613,10 @@ __device__ __forceinline__ void store_unit(const KT& T, int64_t e, const uint4& 
     stv(static_cast<uint16_t*>(T.value) + e, ho);
     st_resid<SF>(T.resid, e, ro);
     if (has_m) {
-        stf(T.m + e, make_float4(mm[0], mm[1], mm[2], mm[3]));
-        stf(T.m + e + 4, make_float4(mm[4], mm[5], mm[6], mm[7]));
+        stf8(T.m + e, mm);
     }
     if constexpr (Op::kHasV) {
-        stf(T.v + e, make_float4(vv[0], vv[1], vv[2], vv[3]));
-        stf(T.v + e + 4, make_float4(vv[4], vv[5], vv[6], vv[7]));
+        stf8(T.v + e, vv);
     }
 }
 
@@ -1135,12 +1140,10 @@ __global__ void __launch_bounds__(kThreads) nvls_step_kernel(uint16_t* __restric
         multimem_st_v4(value_mc + shard_base + e, ho);     // every rank's replica
         st_resid<SF>(resid, e, ro);
         if (has_m) {
-            stf(m + e, make_float4(mm[0], mm[1], mm[2], mm[3]));
-            stf(m + e + 4, make_float4(mm[4], mm[5], mm[6], mm[7]));
+            stf8(m + e, mm);
         }
         if constexpr (Op::kHasV) {
-            stf(v + e, make_float4(vv[0], vv[1], vv[2], vv[3]));
-            stf(v + e + 4, make_float4(vv[4], vv[5], vv[6], vv[7]));
+            stf8(v + e, vv);
         }
     }
     // make the multicast stores visible system-wide, and ordered with later accesses through the
@@ -1224,12 +1227,10 @@ __global__ void __launch_bounds__(kThreads) p2p_step_kernel(const __grid_constan
             if (k < world) stv(P.v[k] + shard_base + e, ho);    // every rank's replica
         st_resid<SF>(resid, e, ro);
         if (has_m) {
-            stf(m + e, make_float4(mm[0], mm[1], mm[2], mm[3]));
-            stf(m + e + 4, make_float4(mm[4], mm[5], mm[6], mm[7]));
+            stf8(m + e, mm);
         }
         if constexpr (Op::kHasV) {
-            stf(v + e, make_float4(vv[0], vv[1], vv[2], vv[3]));
-            stf(v + e + 4, make_float4(vv[4], vv[5], vv[6], vv[7]));
+            stf8(v + e, vv);
         }
     }
     // peer stores visible system-wide before the caller's cross-rank barrier
