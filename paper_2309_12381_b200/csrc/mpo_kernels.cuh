@@ -125,8 +125,13 @@ int64_t fill_table(Table<MAXT>& tab, const mpo_tensor* t, int lo, int hi, bool o
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ uint4 ldv(const void* p) { return __ldcs(reinterpret_cast<const uint4*>(p)); }
 __device__ __forceinline__ float4 ldf(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
+#ifdef MPO_ST_DEFAULT   // A/B knob: default (evict-normal) stores instead of streaming ones
+__device__ __forceinline__ void stv(void* p, uint4 x) { *reinterpret_cast<uint4*>(p) = x; }
+__device__ __forceinline__ void stf(float* p, float4 x) { *reinterpret_cast<float4*>(p) = x; }
+#else
 __device__ __forceinline__ void stv(void* p, uint4 x) { __stcs(reinterpret_cast<uint4*>(p), x); }
 __device__ __forceinline__ void stf(float* p, float4 x) { __stcs(reinterpret_cast<float4*>(p), x); }
+#endif
 // 8 fp32 of one unit (m, v, reconstructed w): two 128-bit streaming stores.  (sm_100's 256-bit
 // st.global.v8.f32 -- SASS STG.E.EF.ENL2.256 -- makes each warp store cover whole sectors instead
 // of half sectors at a 32-B thread stride, but measured -0.5 % ResNet-50 / +0.5 % GPT-2 / -2 %
@@ -690,7 +695,7 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const __grid_constant__ 
 // ---- variant B ("tma", default): warp-specialised bulk-copy pipeline ----------------------
 // One producer warp streams each tile's value / residual / grad / m / v from HBM into a ring of
 // shared-memory stages with 1-D TMA bulk copies (cp.async.bulk, mbarrier complete_tx, L2
-// evict-first); kCW consumer warps read the stage from shared memory, compute, and store the
+// evict-normal); kCW consumer warps read the stage from shared memory, compute, and store the
 // results straight to HBM with 128-bit stores, then release the stage.  Loads are therefore
 // issued independently of the arithmetic, several tiles ahead.
 constexpr int kCW = MPO_CW;                              // consumer warps per CTA
@@ -749,9 +754,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 #endif
 }
-__device__ __forceinline__ uint64_t evict_first_policy() {
+// L2 policy of the bulk-copy loads.  evict_normal: a loaded line stays until the unit's store
+// of the same line (value, residual, m, v are updated in place) hits it in L2; evict_first
+// measured 0.2-0.9 % slower (profiles/r01_ab14_cache_policy.log).
+__device__ __forceinline__ uint64_t load_policy() {
     uint64_t pol;
+#ifdef MPO_LD_EVICT_FIRST   // A/B knob
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#endif
     return pol;
 }
 // 1-D bulk copy global -> shared, completing `bytes` of transaction on `bar`.
@@ -822,7 +834,7 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
         // after their wait (mbarrier release/acquire orders the shared store), so the 16 consumer
         // warps carry no scheduling arithmetic and no walker registers.
         if (lane == 0) {
-            const uint64_t pol = evict_first_policy();
+            const uint64_t pol = load_policy();
             // stage index and phase advance incrementally (a runtime `it % stages` costs two
             // integer divisions per tile)
             int s = 0;
@@ -991,7 +1003,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) sumsq_tma_kernel(const __grid_
     __syncthreads();
     if (warp == kCW) {
         if (lane == 0) {
-            const uint64_t pol = evict_first_policy();
+            const uint64_t pol = load_policy();
             int cur = 0, s = 0;
             uint32_t ph = 0;
             for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
