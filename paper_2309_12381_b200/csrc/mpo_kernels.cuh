@@ -835,6 +835,12 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
         // warps carry no scheduling arithmetic and no walker registers.
         if (lane == 0) {
             const uint64_t pol = load_policy();
+#ifdef MPO_GRAD_EVICT_FIRST   // A/B knob: the read-only gradient stream leaves L2 first
+            uint64_t gpol;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(gpol));
+#else
+            const uint64_t gpol = pol;
+#endif
             // stage index and phase advance incrementally (a runtime `it % stages` costs two
             // integer divisions per tile)
             int s = 0;
@@ -854,7 +860,7 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
                 if (nvec) {
                     bulk_g2s(st, static_cast<const uint16_t*>(T.value) + base, nvec * 2u, &full[s], pol);
                     bulk_g2s(st + OFF_R, static_cast<const unsigned char*>(T.resid) + base * RB, nvec * RB, &full[s], pol);
-                    bulk_g2s(st + OFF_G, static_cast<const unsigned char*>(T.grad) + base * GB, nvec * GB, &full[s], pol);
+                    bulk_g2s(st + OFF_G, static_cast<const unsigned char*>(T.grad) + base * GB, nvec * GB, &full[s], gpol);
                     if (need_m) bulk_g2s(st + OFF_M, T.m + base, nvec * 4u, &full[s], pol);
                     if constexpr (Op::kHasV) bulk_g2s(st + OFF_V, T.v + base, nvec * 4u, &full[s], pol);
                 }
