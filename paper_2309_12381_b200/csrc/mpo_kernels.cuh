@@ -756,7 +756,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 // L2 policy of the bulk-copy loads.  evict_normal: a loaded line stays until the unit's store
 // of the same line (value, residual, m, v are updated in place) hits it in L2; evict_first
-// measured 0.2-0.9 % slower (profiles/r01_ab14_cache_policy.log).
+// measured 0.2-0.9 % slower (profiles/r01_ab14_cache_policy.log); evict_first for the read-only
+// gradient stream alone -0.9 % ResNet-50, -0.7 % GPT-2, +0.4 % LLaMA-7B (r01_ab15_*.log).
 __device__ __forceinline__ uint64_t load_policy() {
     uint64_t pol;
 #ifdef MPO_LD_EVICT_FIRST   // A/B knob
@@ -835,12 +836,6 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
         // warps carry no scheduling arithmetic and no walker registers.
         if (lane == 0) {
             const uint64_t pol = load_policy();
-#ifdef MPO_GRAD_EVICT_FIRST   // A/B knob: the read-only gradient stream leaves L2 first
-            uint64_t gpol;
-            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(gpol));
-#else
-            const uint64_t gpol = pol;
-#endif
             // stage index and phase advance incrementally (a runtime `it % stages` costs two
             // integer divisions per tile)
             int s = 0;
@@ -860,7 +855,7 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
                 if (nvec) {
                     bulk_g2s(st, static_cast<const uint16_t*>(T.value) + base, nvec * 2u, &full[s], pol);
                     bulk_g2s(st + OFF_R, static_cast<const unsigned char*>(T.resid) + base * RB, nvec * RB, &full[s], pol);
-                    bulk_g2s(st + OFF_G, static_cast<const unsigned char*>(T.grad) + base * GB, nvec * GB, &full[s], gpol);
+                    bulk_g2s(st + OFF_G, static_cast<const unsigned char*>(T.grad) + base * GB, nvec * GB, &full[s], pol);
                     if (need_m) bulk_g2s(st + OFF_M, T.m + base, nvec * 4u, &full[s], pol);
                     if constexpr (Op::kHasV) bulk_g2s(st + OFF_V, T.v + base, nvec * 4u, &full[s], pol);
                 }
