@@ -1,5 +1,5 @@
 """A/B (GPU): time kernel variants of the step on the same box, alternating, each in a subprocess.
-usage: python scripts/ab_variants.py NAME=path.so [NAME=path.so ...]   (path 'default' = lib/libmpo.so)"""
+usage: python scripts/ab_variants.py NAME=path.so[,VAR[=VALUE]] ...   (path 'default' = lib/libmpo.so)"""
 import json, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CHILD = r'''
@@ -18,6 +18,10 @@ variants = [a.split("=", 1) for a in sys.argv[1:]]
 for rep in range(2):
     for name, path in variants:
         env = dict(os.environ)
+        if "," in path:                      # name=path,VAR[=VALUE]: also set VAR (workload-side knob)
+            path, var = path.split(",", 1)
+            k, _, val = var.partition("=")
+            env[k] = val or "1"
         if path.startswith("lsu"):
             env["MPO_STEP_KERNEL"] = "lsu"
         elif path != "default":
