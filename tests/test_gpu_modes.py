@@ -529,8 +529,9 @@ def test_p2p_fused_sharded_step_rejects(mpo):
                                  mpo.AdamParams(lr=1e-3), torch.bfloat16)
 
 
+@pytest.mark.parametrize("kind", ["adamw", "sgd"])
 @pytest.mark.parametrize("fmt", [torch.bfloat16, torch.float16])
-def test_residual_adamw_tracks_fp32_master_over_many_steps(mpo, fmt):
+def test_residual_adamw_tracks_fp32_master_over_many_steps(mpo, fmt, kind):
     """The paper's claim on the GPU path: a 16-bit model whose optimizer keeps the
     residual follows the fp32-master optimizer.  300 AdamW steps on identical 16-bit gradients:
     ResidualAdamW's reconstructed fp32 weights stay within a few fp32 ulps per step of torch's own
@@ -545,10 +546,16 @@ def test_residual_adamw_tracks_fp32_master_over_many_steps(mpo, fmt):
     ref = [w.clone().requires_grad_() for w in w0]
     ps = [nn.Parameter(w.clone()) for w in w0]
     low = [w.to(fmt).requires_grad_() for w in w0]
-    kw = dict(lr=1e-4, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01)
-    o_ref = torch.optim.AdamW(ref, foreach=False, **kw)
-    o_low = torch.optim.AdamW(low, foreach=False, **kw)
-    opt = mpo.ResidualAdamW(ps, fmt=fmt, **kw)
+    if kind == "adamw":
+        kw = dict(lr=1e-4, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01)
+        o_ref = torch.optim.AdamW(ref, foreach=False, **kw)
+        o_low = torch.optim.AdamW(low, foreach=False, **kw)
+        opt = mpo.ResidualAdamW(ps, fmt=fmt, **kw)
+    else:   # SGD-momentum (the ResNet-50 recipe's optimizer), small lr
+        kw = dict(lr=1e-3, momentum=0.9, weight_decay=2e-4)
+        o_ref = torch.optim.SGD(ref, foreach=False, **kw)
+        o_low = torch.optim.SGD(low, foreach=False, **kw)
+        opt = mpo.ResidualSGD(ps, fmt=fmt, **kw)
     for _ in range(300):
         g = [(torch.randn(s, device="cuda") * 1e-2).to(fmt) for s in shapes]
         for r, x in zip(ref, g):
