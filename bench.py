@@ -834,6 +834,10 @@ def main():
             line["secondary"]["gpt2_hook_mode"] = hook_mode_secondary()
         except Exception as ex:
             line["secondary"]["gpt2_hook_mode"] = {"error": f"{type(ex).__name__}: {ex}"}
+        try:   # small activations (B=1, T=128): gradients are a large share of the peak
+            line["secondary"]["gpt2_hook_mode_b1_t128"] = hook_mode_secondary(batch=1, seq=128)
+        except Exception as ex:
+            line["secondary"]["gpt2_hook_mode_b1_t128"] = {"error": f"{type(ex).__name__}: {ex}"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.workload)
     if rank == 0:

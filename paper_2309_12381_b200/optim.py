@@ -154,6 +154,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         self._pending = []
         self._pending_elems = 0
         self._flush_queued = False
+        self._hp_c, self._codes = {}, {}
         for gi, group in enumerate(self.param_groups):
             for p in group["params"]:
                 st = self.state[p]
@@ -190,9 +191,18 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             return
         row = st["row"]
         row.grad = g.data_ptr()
-        hp = self._hp(self.param_groups[st["group"]], st["step"]).c()
-        api.mpo_fused_backward_hook_step(self._kind, api.format_code(p.dtype, self.scheme), api.dtype_code(g.dtype),
-                                         row, hp, exact=self.exact,
+        # host cost per hook matters when backward is short: the ctypes hyper-parameters are built
+        # once per (group, step) and shared by the group's parameters; format codes are cached
+        key = (st["group"], st["step"])
+        hp = self._hp_c.get(key)
+        if hp is None:
+            if len(self._hp_c) > 64:
+                self._hp_c.clear()
+            hp = self._hp_c[key] = self._hp(self.param_groups[st["group"]], st["step"]).c()
+        codes = self._codes.get((p.dtype, g.dtype))
+        if codes is None:
+            codes = self._codes[(p.dtype, g.dtype)] = (api.format_code(p.dtype, self.scheme), api.dtype_code(g.dtype))
+        api.mpo_fused_backward_hook_step(self._kind, codes[0], codes[1], row, hp, exact=self.exact,
                                          norm_ws=self._ws(p.device) if self.skip_nonfinite else None)
         p.grad = None   # freed now; stream order makes the block's reuse safe
 
