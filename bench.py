@@ -491,8 +491,19 @@ def cpu_baseline(name, budget_s=12.0):
         el = time.perf_counter() - t0
         if el >= budget_s:
             break
-    return {"value": done / el, "unit": "params/s", "cores": 1, "kind": "oracle",
+    return {"value": done / el, "unit": "params/s", "cores": 1, "kind": "oracle", "cpu": cpu_model(),
+            "host_cores": len(os.sched_getaffinity(0)),
             "sample": f"{steps} steps x {n} params ({kind}, {fmt}) of the {wl} workload's recipe, {el:.1f} s"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args):
@@ -550,7 +561,8 @@ def run_reference(args):
             "dtype": "f32", "storage": f"{fmt} value + int16 residual, fp32 optimizer state", "data": "synthetic",
             "config": {"workload": f"{name} ({wl}, BASELINE configs[{WORKLOADS[name][4]}])",
                        "sample_params_per_step": n, "params_in_workload": P},
-            "cpu_baseline": {"value": value, "unit": "params/s", "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": "params/s", "cores": 1, "kind": "oracle", "cpu": cpu_model(),
+                             "host_cores": len(os.sched_getaffinity(0)),
                              "sample": f"{n} of {P} params per step, {args.steps} steps"},
             "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
