@@ -581,3 +581,37 @@ def test_vit_l16_adam_clip_full_sampled(mpo, orc):
     finally:
         del wl
         torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------------------------------
+# P2P fused sharded step in the FMA build (R12 tolerance), 4 ranks emulated on one device
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+def test_p2p_fused_step_fma_build_within_tolerance(mpo, orc, fmt):
+    from paper_2309_12381_b200 import api
+    from paper_2309_12381_b200._lib import MPO_ADAM
+    world, S = 4, 8 * 4101
+    n = S * world
+    h, r = orc.split(fmt, synth.weights(n, 0.02, 11))
+    gs = [synth.grads(n, 1e-2, fmt, 0xB0B, k) for k in range(world)]
+    V = [dev16(h, fmt) for _ in range(world)]
+    G = [dev16(g, fmt) for g in gs]
+    ms = [synth.normal_f32(S, 1e-3, 5, k) for k in range(world)]
+    vs = [np.abs(synth.normal_f32(S, 1e-5, 6, k)) for k in range(world)]
+    R = [devi16(r[k * S:(k + 1) * S]) for k in range(world)]
+    M, W = [devf(m) for m in ms], [devf(v) for v in vs]
+    hp = mpo.AdamParams(lr=1e-3, weight_decay=0.1, step=5, grad_scale=1.0 / world)
+    for k in range(world):
+        api.mpo_p2p_sharded_step(MPO_ADAM, k, world, [t.data_ptr() for t in V], [t.data_ptr() for t in G], R[k],
+                                 M[k], W[k], n, hp, TDT[fmt], exact=False)
+    torch.cuda.synchronize()
+    for k in range(world):
+        sl = slice(k * S, (k + 1) * S)
+        gsum = orc.reduce_sum16(fmt, [g[sl] for g in gs])
+        pre = (h[sl].copy(), r[sl].copy(), ms[k].copy(), vs[k].copy())
+        ho, ro, mo, vo = h[sl].copy(), r[sl].copy(), ms[k].copy(), vs[k].copy()
+        orc.adam_step(fmt, "fp32", ho, ro, gsum, mo, vo, **_adam_hp_kw(hp))
+        gpu = (host16(V[0])[sl], R[k].cpu().numpy(), M[k].cpu().numpy(), W[k].cpu().numpy())
+        _check_fma_tolerance(fmt, pre, gpu, (ho, ro, mo, vo), gsum, _adam_uscale(hp, pre[2], gsum, vo))
+        for rep in V[1:]:
+            assert np.array_equal(host16(rep)[sl], gpu[0])      # every replica got the same values
