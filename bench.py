@@ -271,7 +271,7 @@ def timed(fn, steps, warmup, dist=None, sampler=None):
 NVLINK_GBS = 900.0   # NVLink 5 per direction per GPU
 
 
-def multi_gpu_breakdown(wl, dist, steps, warmup):
+def multi_gpu_breakdown(wl, dist, steps, warmup, p2p=False):
     """N > 1 only (every rank runs it; collectives in the same order on all ranks).  SURVEY 8(e):
     (i) the update alone on this rank's shard (same step kernel through mpo_sgd_step /
     mpo_adam_step on a one-tensor table of the shard), aggregate params/s = P / max-rank time --
@@ -311,7 +311,9 @@ def multi_gpu_breakdown(wl, dist, steps, warmup):
     out["nccl_algo"] = os.environ.get("NCCL_ALGO", "auto (NCCL's choice; NCCL_DEBUG=INFO names it)")
     # the same step fused with its collectives over NVLink peer memory (mpo_p2p_sharded_step on
     # torch symmetric memory, between symmetric-memory barriers), when the box provides it
-    if not wl.clip:
+    # opt-in (--p2p): a symmetric-memory rendezvous that fails on some ranks only would hang the
+    # others, and the default run must always deliver its line
+    if p2p and not wl.clip:
         try:
             out["p2p_fused_step"] = _p2p_fused_timing(wl, dist, steps, warmup)
         except Exception as ex:
@@ -743,6 +745,8 @@ def main():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=30)
+    ap.add_argument("--p2p", action="store_true",
+                    help="N>1 (or --mg-breakdown): also time the P2P fused sharded step on torch symmetric memory")
     ap.add_argument("--mg-breakdown", action="store_true",
                     help="run the N>1 update/collective breakdown at world 1 too (code-path check)")
     args = ap.parse_args()
@@ -787,7 +791,7 @@ def main():
                 import torch.distributed as tdist
                 wl.step(sharded=True)
                 dist = tdist
-            mg = multi_gpu_breakdown(wl, dist, args.steps, args.warmup)
+            mg = multi_gpu_breakdown(wl, dist, args.steps, args.warmup, p2p=args.p2p)
             if world > 1:
                 # the step kernel's own launch time on the shard (the whole-step window also
                 # holds the NCCL collectives, reported with their NVLink fractions in multi_gpu)
