@@ -71,6 +71,20 @@ struct HP {
 };
 
 __device__ __forceinline__ int hp_of(const KT& T) { return T.hps & 15; }
+
+// The tensor owning `tile`: the last entry whose first tile is <= tile (empty tensors share
+// their successor's tile0 and are skipped), by binary search -- ~log2(nt) parameter-space loads
+// instead of a dependent walk from entry 0.
+template <int MAXT>
+__device__ __forceinline__ int first_tensor(const Table<MAXT>& tab, int tile) {
+    int l = 0, h = tab.nt - 1;
+    while (l < h) {
+        const int mid = (l + h + 1) >> 1;
+        if (tab.t[mid].tile0 <= tile) l = mid;
+        else h = mid - 1;
+    }
+    return l;
+}
 __device__ __forceinline__ uint32_t stream_of(const KT& T) { return static_cast<uint32_t>(T.hps) >> 4; }
 
 // ------------------------------------------------------------------------------------------
@@ -386,7 +400,7 @@ __global__ void __launch_bounds__(kThreads) sumsq_kernel(const __grid_constant__
     double acc8[kUnitEl];
 #pragma unroll
     for (int k = 0; k < kUnitEl; ++k) acc8[k] = 0.0;
-    int cur = 0;
+    int cur = first_tensor(tab, int(blockIdx.x));   // not a dependent walk from tensor 0
     for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
         while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
         const KT& T = tab.t[cur];
@@ -868,7 +882,16 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
             // memory together (one contiguous window per stream at any moment).  A/B on one box:
             // contiguous per-CTA ranges balanced to 16 elements lost 5 %, a balanced sweep of
             // chunks < 1 tile lost 1-2 % on ResNet-50 (profiles/r01_ab7..10*.log).
-            int cur = 0;
+            // first tile's tensor by binary search: a linear walk from tensor 0 costs the last
+            // CTAs tens of dependent parameter-space loads before their first copy (ResNet-50's
+            // first wave spans ~40 tensors); later tiles advance the cursor a few entries at a time
+            // First tile's tensor by binary search: a linear walk from tensor 0 costs the last
+            // CTAs tens of dependent parameter-space loads (~100+ cycles each) before their first
+            // copy -- ResNet-50's first wave spans ~40 tensors; +1.8 % on that step.  Later tiles
+            // advance the cursor a few entries at a time while the ring is full.  (A warp-parallel
+            // ballot search gave the same on ResNet-50 and cost 0.6 % on the large sets:
+            // profiles/r01_ab20_bsearch_start.log, r01_ab21_cursor.log.)
+            int cur = first_tensor(tab, int(blockIdx.x));
             for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
                 while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
                 const int64_t base = int64_t(tile - tab.t[cur].tile0) * TE;
