@@ -9,14 +9,19 @@ prints ONE JSON line on rank 0.
   update -> re-split for every parameter, in one multi-tensor launch; at N>1
   the data-parallel sharded step (NCCL reduce-scatter of 16-bit grads -> shard update -> NCCL
   all-gather of 16-bit values).
-* Default workload = BASELINE.json configs[1]: ResNet-50 parameter set (25 557 032 params, 161
-  tensors), fp16 + int16 residual, SGD-momentum (lr 0.3, momentum 0.9, wd 2e-4).
-  The per-step working set (460 MB) is larger than L2 (126 MB): no flush needed.
+* Default workload = BASELINE.json configs[3], the largest single-GPU configuration and the Adam
+  step BASELINE.json's target names: the LLaMA-7B parameter set (6 738 415 616 params, 291
+  tensors), bf16 + int16 residual, Adam (lr 3e-4, betas (0.9, 0.95), eps 1e-8), one multi-tensor
+  launch per step at N=1 (175 GB of algorithmic traffic per step >> 126 MB L2: no flush needed);
+  at N>1 the sharded step.
 * value = params/s over all ranks (device time, CUDA events, max over ranks).
-* Secondary (N=1): the Adam configs -- GPT-2 small AdamW (configs[2] parameter set), ViT-L/16
-  Adam + global-norm clip (configs[4]) and LLaMA-7B Adam through mpo_sharded_step at world 1
-  (configs[3]) -- each with its own roofline fraction.
-* --impl reference: the CPU oracle (oracle/, plain C, 1 thread) on a bounded sample of the same
+* Secondary (N=1): ResNet-50 SGD-momentum (configs[1]), GPT-2 small AdamW (configs[2] parameter
+  set), ViT-L/16 Adam + global-norm clip (configs[4]), the flat 2^20 Adam tensor (configs[0]:
+  launch/L2-bound and L2-flushed), the storage variants, and the GPT-2 hook-mode training step --
+  each with its own roofline fraction or breakdown.
+* cpu_baseline: the CPU oracle (oracle/, plain C) on a bounded sample, single-threaded AND with
+  its OpenMP build over every core of the affinity mask (bit-identical builds).
+* --impl reference: the CPU oracle (OpenMP build, all cores) on a bounded sample of the same
   workload: the reference arm of this tier (there is no reference code to install).
 """
 from __future__ import annotations
@@ -43,7 +48,9 @@ WORKLOADS = {
     "vit_l16_adam_clip": ("vit_l16", "fp16", "adam", dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8,
                                                          max_grad_norm=1.0, adamw=False), 4),
     "llama7b_adam": ("llama7b", "bf16", "adam", dict(lr=3e-4, beta1=0.9, beta2=0.95, eps=1e-8, adamw=False), 3),
+    "flat1m_adam": ("flat1m", "fp16", "adam", dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, adamw=False), 0),
 }
+DEFAULT_WORKLOAD = "llama7b_adam"
 # algorithmic HBM bytes per parameter per step
 BYTES_PER_PARAM = {"sgd": 18, "adam": 26, "adam_clip": 28}
 
@@ -81,7 +88,7 @@ class ClockSampler:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.FIELDS}",
-                                       "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
+                                       "--format=csv,noheader,nounits", "-lms", "20"], stdout=self.f,
                                       stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -106,6 +113,19 @@ class ClockSampler:
                 continue
             if any(a - 0.1 <= ts <= b + 0.1 for a, b in self.windows):
                 sel.append(r)
+        if not sel and rows and self.windows:
+            # a region shorter than the sampling period: the samples just before and after it
+            a, b = self.windows[0][0], self.windows[-1][1]
+            ts = []
+            for r in rows:
+                try:
+                    ts.append(time.mktime(time.strptime(r[0].split(".")[0], "%Y/%m/%d %H:%M:%S"))
+                              + float("0." + r[0].split(".")[1]))
+                except Exception:
+                    ts.append(None)
+            before = [r for r, t in zip(rows, ts) if t is not None and t <= a]
+            after = [r for r, t in zip(rows, ts) if t is not None and t >= b]
+            sel = before[-1:] + after[:1]
         use = sel if sel else rows
         sm = [float(r[1]) for r in use if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in use if r[2].replace(".", "").isdigit()]
@@ -240,6 +260,7 @@ def timed(fn, steps, warmup, dist=None, sampler=None):
     this library inside the region)."""
     import torch
     from paper_2309_12381_b200 import api
+    tw = time.time()
     for _ in range(warmup):
         fn()
     s = torch.cuda.current_stream()
@@ -258,7 +279,9 @@ def timed(fn, steps, warmup, dist=None, sampler=None):
     if dist is not None:
         dist.barrier()
     if sampler is not None:
-        sampler.mark(t0, t1)
+        # the clocks of the warm-up count too: at 20 steps the timed region alone can be shorter
+        # than nvidia-smi's sampling period
+        sampler.mark(tw, t1)
     launches = api.launch_count() - n0
     ms = start.elapsed_time(end) / steps
     if dist is not None:
@@ -383,8 +406,12 @@ def e2e_measure(wl, steps, dist=None):
             b1, b2 = hk.pop("beta1"), hk.pop("beta2")
             opt = mpo.ResidualAdamW(params, betas=(b1, b2), **hk)
         host = [torch.empty(L.total, dtype=wl.tdt, pin_memory=True) for _ in range(2)]
-        for h in host:
-            h.view(torch.int16).random_(-2000, 2000)
+        sig = 1e-3 if wl.kind == "adam" else 1e-2
+        for k, h in enumerate(host):
+            # real gradients: seeded N(0, sigma) cast to the value dtype (finite, the bench's own scale);
+            # drawn on the device once, before any timing, then kept in pinned host memory
+            torch_normal_(gbuf[k], sig, 0xB0B, 7000 + k)
+            h.copy_(gbuf[k])
         out = torch.empty(L.total, dtype=wl.tdt, pin_memory=True)
         comp = torch.cuda.current_stream()
         cin, cout = torch.cuda.Stream(), torch.cuda.Stream()
@@ -433,7 +460,10 @@ def e2e_measure(wl, steps, dist=None):
     else:
         L = wl.layout
         host = torch.empty(L.total, dtype=wl.tdt, pin_memory=True)
-        host.view(torch.int16).random_(-2000, 2000)
+        tmp = torch.empty(L.total, dtype=wl.tdt, device=dev)
+        torch_normal_(tmp, 1e-3 if wl.kind == "adam" else 1e-2, 0xB0B, 7000 + wl.rank)
+        host.copy_(tmp)
+        del tmp
         out = torch.empty(L.total, dtype=wl.tdt, pin_memory=True)
 
         def step():
@@ -456,46 +486,65 @@ def e2e_measure(wl, steps, dist=None):
         ms, _ = timed(step_and_drain, steps, 0, dist)
     else:
         ms, _ = timed(step, steps, 3, dist)
+    # the step really updated finite weights (no special-value slow path was timed)
+    finite = bool(torch.isfinite(flat_v if wl.world == 1 else wl.value).all().item())
+    if not finite:
+        raise RuntimeError("e2e: non-finite weights after the timed steps")
     return {"value": wl.P / (ms * 1e-3), "unit": "params/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": ms, "steps": steps,
+            "ms_per_step": ms, "steps": steps, "grads": "seeded N(0, sigma) cast to the value dtype; weights finite after",
             "path": ("public API (ResidualSGD/ResidualAdamW.step); pinned H2D of grads and D2H of values on "
                      "copy streams overlapping the neighbouring steps") if wl.world == 1
             else "mpo_sharded_step + pinned H2D/D2H"}
 
 
-def cpu_baseline(name, budget_s=12.0):
-    """The oracle as it stands (plain C, one thread) on a bounded sample of the workload."""
+def _oracle_rate(name, threads, budget_s, n=1 << 22):
+    """Params/s of the oracle as it stands on a bounded sample of the workload's recipe: n params
+    (weights N(0, 0.02), the bench's gradient scale, its hyper-parameters, clip pre-pass included)
+    stepped repeatedly until budget_s has passed.  threads = 1: the plain build; 0: the OpenMP build
+    over every core of the affinity mask."""
     import numpy as np
     import oracle
     import synth
-    oracle.build()
     wl, fmt, kind, hp, _ = WORKLOADS[name]
-    n = 1 << 22
-    w = synth.weights(n, 0.02, 0xB0B)
-    h, r = oracle.split(fmt, w)
-    g = synth.grads(n, 1e-3, fmt, 0xB0B, 1)
-    m = np.zeros(n, np.float32)
-    v = np.zeros(n, np.float32)
-    done, t0, steps = 0, time.perf_counter(), 0
-    while True:
-        steps += 1
-        if kind == "sgd":
-            oracle.sgd_step(fmt, fmt, h, r, g, m, lr=hp["lr"], momentum=hp["momentum"],
-                            weight_decay=hp["weight_decay"], first_step=(steps == 1))
-        else:
-            coef = None
-            if hp.get("max_grad_norm"):
-                coef = oracle.clip_coef(oracle.sumsq(fmt, g), hp["max_grad_norm"])
-            oracle.adam_step(fmt, fmt, h, r, g, m, v, lr=hp["lr"], beta1=hp["beta1"], beta2=hp["beta2"],
-                             eps=hp["eps"], weight_decay=hp.get("weight_decay", 0.0), adamw=hp["adamw"], step=steps,
-                             clip_coef=coef)
-        done += n
-        el = time.perf_counter() - t0
-        if el >= budget_s:
-            break
-    return {"value": done / el, "unit": "params/s", "cores": 1, "kind": "oracle", "cpu": cpu_model(),
-            "host_cores": len(os.sched_getaffinity(0)),
+    used = oracle.parallel(threads != 1, 0 if threads != 1 else 1)
+    try:
+        w = synth.weights(n, 0.02, 0xB0B)
+        h, r = oracle.split(fmt, w)
+        g = synth.grads(n, 1e-3 if kind == "adam" else 1e-2, fmt, 0xB0B, 1)
+        m = np.zeros(n, np.float32)
+        v = np.zeros(n, np.float32)
+        done, t0, steps = 0, time.perf_counter(), 0
+        while True:
+            steps += 1
+            if kind == "sgd":
+                oracle.sgd_step(fmt, fmt, h, r, g, m, lr=hp["lr"], momentum=hp["momentum"],
+                                weight_decay=hp["weight_decay"], first_step=(steps == 1))
+            else:
+                coef = None
+                if hp.get("max_grad_norm"):
+                    coef = oracle.clip_coef(oracle.sumsq(fmt, g), hp["max_grad_norm"])
+                oracle.adam_step(fmt, fmt, h, r, g, m, v, lr=hp["lr"], beta1=hp["beta1"], beta2=hp["beta2"],
+                                 eps=hp["eps"], weight_decay=hp.get("weight_decay", 0.0), adamw=hp["adamw"],
+                                 step=steps, clip_coef=coef)
+            done += n
+            el = time.perf_counter() - t0
+            if el >= budget_s:
+                break
+    finally:
+        oracle.parallel(False)
+    return {"value": done / el, "unit": "params/s", "threads": used,
             "sample": f"{steps} steps x {n} params ({kind}, {fmt}) of the {wl} workload's recipe, {el:.1f} s"}
+
+
+def cpu_baseline(name, budget_s=10.0):
+    """The oracle as it stands (plain C) on this host: one thread, and the bit-identical OpenMP
+    build over every core of the affinity mask (the headline `value`/`cores`)."""
+    one = _oracle_rate(name, 1, budget_s)
+    allc = _oracle_rate(name, 0, budget_s, n=1 << 24)
+    return {"value": allc["value"], "unit": "params/s", "cores": allc["threads"], "kind": "oracle",
+            "cpu": cpu_model(), "host_cores": len(os.sched_getaffinity(0)),
+            "sample": allc["sample"] + f"; OpenMP build, {allc['threads']} threads",
+            "threads_1": one, "threads_all": allc}
 
 
 def cpu_model() -> str:
@@ -521,6 +570,8 @@ def run_reference(args):
     wl, fmt, kind, hp, _ = WORKLOADS[name]
     from synth import workloads
     P = workloads.total(wl)
+    # the oracle as it stands, over every host core: its OpenMP build (bit-identical to the plain one)
+    threads = oracle.parallel(True, 0)
     # size each reference step so the whole --steps K --warmup W run stays within ~2 minutes
     budget = 100.0 / max(1, args.steps + args.warmup)
     probe = 1 << 20
@@ -531,7 +582,7 @@ def run_reference(args):
     t0 = time.perf_counter()
     oracle.adam_step(fmt, fmt, hp_, rp_, gp, mp_, vp_, lr=1e-3)
     rate = probe / (time.perf_counter() - t0)
-    n = int(min(P, max(8192, rate * budget)))
+    n = int(min(P, 1 << 27, max(8192, rate * budget)))
     n -= n % 8
     w = synth.weights(n, 0.02, 0xB0B)
     h, r = oracle.split(fmt, w)
@@ -563,9 +614,10 @@ def run_reference(args):
             "dtype": "f32", "storage": f"{fmt} value + int16 residual, fp32 optimizer state", "data": "synthetic",
             "config": {"workload": f"{name} ({wl}, BASELINE configs[{WORKLOADS[name][4]}])",
                        "sample_params_per_step": n, "params_in_workload": P},
-            "cpu_baseline": {"value": value, "unit": "params/s", "cores": 1, "kind": "oracle", "cpu": cpu_model(),
+            "cpu_baseline": {"value": value, "unit": "params/s", "cores": threads, "kind": "oracle", "cpu": cpu_model(),
                              "host_cores": len(os.sched_getaffinity(0)),
-                             "sample": f"{n} of {P} params per step, {args.steps} steps"},
+                             "sample": f"{n} of {P} params per step, {args.steps} steps; OpenMP build, "
+                                       f"{threads} threads"},
             "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
 
@@ -601,6 +653,39 @@ def _secondary_one(name, steps, warmup, hbm_peak, scheme="rne"):
                      "persistent_bytes_per_param": wl.persistent_bytes / wl.P}
         del wl
         return res
+
+
+def flat1m_secondary(hbm_peak, steps=100, warmup=10):
+    """BASELINE configs[0]: one flat 2^20-param fp16 + residual tensor, Adam, 100 steps per
+    measurement.  Its 27 MB per step fits the 126 MB L2 and one launch is a few microseconds, so
+    back to back it is launch/L2-bound ("too many kernel launches can hinder performance on
+    smaller parameters"); rotating through >= 4 x L2 of independent parameter sets gives its
+    HBM-bound number (each launch finds its set evicted)."""
+    import torch
+    wl = Workload("flat1m_adam")
+    bpp = wl.bytes_per_param
+    ms, launches = timed(wl.step, steps, warmup)
+    per = wl.P * bpp
+    sets = int(math.ceil(4 * L2_BYTES / per)) + 1
+    pool = [wl] + [Workload("flat1m_adam", seed=0xB0B + k) for k in range(1, sets)]
+    it = [0]
+
+    def rot():
+        pool[it[0] % sets].step()
+        it[0] += 1
+    ms_rot, _ = timed(rot, steps * 2, sets)
+    res = {"config": f"BASELINE configs[0]: {wl.P} params, 1 tensor, fp16 + int16 residual, Adam, {steps} steps",
+           "bytes_per_param": bpp, "launches_per_step": launches / steps,
+           "back_to_back_l2_resident": {"params_per_s": wl.P / (ms * 1e-3), "us_per_step": ms * 1e3,
+                                        "gbs": per / (ms * 1e-3) / 1e9,
+                                        "note": "27 MB working set < L2: launch / L2-bound"},
+           "l2_flushed_rotating": {"params_per_s": wl.P / (ms_rot * 1e-3), "us_per_step": ms_rot * 1e3,
+                                   "gbs": per / (ms_rot * 1e-3) / 1e9,
+                                   "frac_of_measured_hbm": per / (ms_rot * 1e-3) / 1e9 / hbm_peak,
+                                   "sets": sets, "rotated_bytes": sets * per}}
+    del pool, wl
+    torch.cuda.empty_cache()
+    return res
 
 
 def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
@@ -649,9 +734,13 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
             if mode == "hook":
                 opt.install_backward_hooks()
 
-            def step():
+            def step(rec=None):
                 loss = loss_of(model)
+                if rec is not None:
+                    rec[0].record()
                 loss.backward()
+                if rec is not None:
+                    rec[1].record()
                 if mode == "two_phase":
                     opt.step()
                     for p in model.parameters():
@@ -663,9 +752,13 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
             opt = torch.optim.AdamW(master, fused=True, **hp)
             params = list(model.parameters())
 
-            def step():
+            def step(rec=None):
                 loss = loss_of(model)
+                if rec is not None:
+                    rec[0].record()
                 loss.backward()
+                if rec is not None:
+                    rec[1].record()
                 for m_, p in zip(master, params):
                     m_.grad = p.grad.float()
                     p.grad = None
@@ -691,7 +784,33 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
         e.record()
         torch.cuda.synchronize()
         peak = torch.cuda.max_memory_allocated() - base
-        res = {"ms_per_train_step": s.elapsed_time(e) / steps, "state_bytes_per_param": state / P,
+        # phase breakdown (separate steps, so the events do not perturb the number above):
+        # forward, backward (hook mode: with its fused steps), the rest (two-phase: the step)
+        ph = [0.0, 0.0, 0.0]
+        for _ in range(steps):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record()
+            step(rec=ev[1:3])
+            ev[3].record()
+            torch.cuda.synchronize()
+            for k in range(3):
+                ph[k] += ev[k].elapsed_time(ev[k + 1]) / steps
+        hook_kernels_ms = None
+        if mode == "hook":
+            # summed device time of this library's kernels inside one hook-mode training step
+            # (CUPTI through torch.profiler; nsys is not installed in this image)
+            try:
+                from torch.profiler import ProfilerActivity, profile
+                with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                    step()
+                    torch.cuda.synchronize()
+                hook_kernels_ms = sum(e.self_device_time_total for e in prof.key_averages()
+                                      if "mpo::" in e.key) / 1e3
+            except Exception as ex:   # recorded, not hidden
+                hook_kernels_ms = f"unavailable: {type(ex).__name__}: {ex}"[:200]
+        res = {"ms_per_train_step": s.elapsed_time(e) / steps, "forward_ms": ph[0], "backward_ms": ph[1],
+               "after_backward_ms": ph[2], "library_kernels_ms_per_step": hook_kernels_ms,
+               "state_bytes_per_param": state / P,
                "persistent_bytes_per_param": persistent / P,
                "persistent_requested_bytes_per_param": persistent_req / P,
                "peak_bytes_per_param": peak / P, "peak_gb": peak / 1e9, "loss": float(loss.detach()), "leftover_bytes_excluded": base}
@@ -707,6 +826,16 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
             "allocated": out["amp_fp32_master"]["persistent_bytes_per_param"] - out["hook"]["persistent_bytes_per_param"],
             "requested": (out["amp_fp32_master"]["persistent_requested_bytes_per_param"]
                           - out["hook"]["persistent_requested_bytes_per_param"])}
+    except Exception:
+        pass
+    try:   # SURVEY 8(d)'s three hook-mode numbers (+3-4 % time in the paper)
+        h, t = out["hook"], out["two_phase"]
+        out["hook_breakdown"] = {
+            "added_backward_ms": h["backward_ms"] - t["backward_ms"],
+            "hook_kernels_ms": h["library_kernels_ms_per_step"],
+            "two_phase_backward_plus_step_ms": t["backward_ms"] + t["after_backward_ms"],
+            "hook_backward_ms": h["backward_ms"],
+            "hook_vs_two_phase_train_step": h["ms_per_train_step"] / t["ms_per_train_step"] - 1.0}
     except Exception:
         pass
     out["config"] = (f"BASELINE configs[2]: HF GPT2LMHeadModel random init (124439808 params, 148 tensors), "
@@ -741,7 +870,7 @@ def main():
     ap.add_argument("--steps", type=int, default=12000)   # ~1 s timed region (clock samples)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="mpo", choices=["mpo", "reference"])
-    ap.add_argument("--workload", default="resnet50_sgd", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=30)
@@ -833,7 +962,12 @@ def main():
     if rank == 0 and world == 1 and not args.no_secondary:
         del wl
         torch.cuda.empty_cache()
-        line["secondary"] = secondary(["gpt2_adamw", "vit_l16_adam_clip", "llama7b_adam"], 200, 5, hbm_peak)
+        line["secondary"] = secondary([n for n in ("resnet50_sgd", "gpt2_adamw", "vit_l16_adam_clip", "llama7b_adam")
+                                       if n != args.workload], 200, 5, hbm_peak)
+        try:
+            line["secondary"]["flat1m_adam"] = flat1m_secondary(hbm_peak)
+        except Exception as ex:
+            line["secondary"]["flat1m_adam"] = {"error": f"{type(ex).__name__}: {ex}"}
         for sch in ("rtz", "sr", "x8"):    # paper variants of the storage scheme, GPT-2 AdamW set
             name = "gpt2_adamw"
             fmt_ok = sch != "sr" or WORKLOADS[name][1] == "fp16"

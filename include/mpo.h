@@ -117,7 +117,7 @@ typedef struct {
     uint64_t seed;   /* stochastic-rounding draws of this step (MPO_FP16_SR); else ignored */
     double clip_value;       /* > 0: clamp the scaled gradient to [-c, c] (see below); 0: off */
     int32_t skip_nonfinite;  /* != 0: skip the update when a scaled gradient is Inf/NaN (below) */
-    int32_t _pad2;
+    int32_t norm_ready;      /* != 0: norm_ws[0] already holds S of the whole step (below) */
 } mpo_sgd_hp;
 
 /* torch.optim.Adam / AdamW semantics (R6).  step is 1-based (bias correction).  adamw != 0:
@@ -132,7 +132,7 @@ typedef struct {
     uint64_t seed;   /* stochastic-rounding draws of this step (MPO_FP16_SR); else ignored */
     double clip_value;       /* > 0: clamp the scaled gradient to [-c, c] (see below); 0: off */
     int32_t skip_nonfinite;  /* != 0: skip the update when a scaled gradient is Inf/NaN (below) */
-    int32_t _pad2;
+    int32_t norm_ready;      /* != 0: norm_ws[0] already holds S of the whole step (below) */
 } mpo_adam_hp;
 
 /* Gradient surgery inside the optimizer ("every operations on the gradient (eg. clipping or
@@ -149,6 +149,14 @@ typedef struct {
  *                   P:93) and accumulates S into norm_ws[mpo_norm_ws_doubles() - 1] so the
  *                   caller learns at the end of backward whether any gradient was non-finite.
  * Must be the same for every group of a call. */
+
+/* norm_ready (multi-tensor entry points only): a step whose parameters span several tables (e.g.
+ * tensors of different gradient dtypes, one mpo_adam_step call each) needs ONE S over all of them
+ * for global-norm clipping (R9: "the norm of all gradients") and for an all-or-nothing
+ * found-inf skip.  The caller then fills norm_ws[0] with mpo_grad_sumsq over every table first
+ * (accumulate = 0 for the first, 1 for the rest) and sets norm_ready in every group of every step
+ * call: the calls do no pre-pass and read S from norm_ws[0].  Rejected (MPO_EINVAL) by the hook and
+ * sharded entry points, which compute their own S. */
 
 /* Largest number of hyper-parameter groups one call may carry. */
 #define MPO_MAX_HP_GROUPS 16
@@ -186,6 +194,17 @@ mpo_status mpo_adam_step(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t, int3
  * call, then per-block partials, last = S accumulated by hook-mode calls (zeroed by the caller). */
 int64_t mpo_norm_ws_doubles(void);
 
+/* Sum of squares of the scaled gradients of a table: S = sum_i (double)(f32(grad_i) * gs)^2 with
+ * gs = (float)grad_scale[t.hp] (R9; the pre-pass of clipping and of the found-inf skip, exposed so a
+ * step spanning several tables shares one S -- see norm_ready).  Only the grad, n and hp fields of
+ * the table entries are read (grad 16-B aligned; value/resid/m/v ignored).
+ *   gdt        : MPO_FP16 | MPO_BF16 | MPO_FP32
+ *   grad_scale : nhp doubles (HOST), 1 <= nhp <= MPO_MAX_HP_GROUPS, finite
+ *   norm_ws    : DEVICE scratch of mpo_norm_ws_doubles() doubles; accumulate == 0: norm_ws[0] = S,
+ *                else norm_ws[0] += S (stream order).  The partials in norm_ws[1..] are clobbered. */
+mpo_status mpo_grad_sumsq(mpo_dtype gdt, const mpo_tensor* t, int32_t nt, const double* grad_scale,
+                          int32_t nhp, double* norm_ws, int32_t accumulate, mpo_stream stream);
+
 /* Fused backward + optimizer step for ONE parameter, called from its post-accumulate-grad hook
  * ("operate the optimization step as soon as the gradient is computed").
  *   kind : MPO_SGD (hp -> mpo_sgd_hp) | MPO_ADAM (hp -> mpo_adam_hp), hp in HOST memory
@@ -218,6 +237,39 @@ mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t rank, i
                             void* resid_shard, float* m_shard, float* v_shard,
                             int64_t n_total, const void* hp, double* norm_ws,
                             mpo_stream stream);
+
+/* One piece of a rank's shard for mpo_sharded_step_grouped: the elements [start, next start) of the
+ * shard (the last piece runs to the shard's end) use hyper-parameter group `hp` and draw their
+ * stochastic-rounding numbers from stream `sr_stream` (0 <= id < 2^27), indexed from the piece's
+ * first element. */
+typedef struct {
+    int64_t start;
+    int32_t hp;
+    int32_t sr_stream;
+} mpo_segment;
+
+/* mpo_sharded_step with per-parameter hyper-parameter groups ("does not necessitate any
+ * alterations to the hyperparameters": e.g. GPT/LLaMA recipes that exempt 1-D tensors from weight
+ * decay).  Same collective sequence and arguments as mpo_sharded_step, plus:
+ *   seg, nseg : HOST array partitioning THIS rank's shard [0, n_total/world) into pieces (seg[0].start
+ *               == 0, starts strictly increasing and < the shard length; every start a multiple of 8
+ *               elements, 16 for the X8 formats, so each piece's arrays stay 16-B aligned); ranks
+ *               pass their own tables
+ *   hp, nhp   : nhp groups (mpo_sgd_hp* | mpo_adam_hp*, HOST), 1 <= nhp <= MPO_MAX_HP_GROUPS;
+ *               grad_scale, max_grad_norm, clip_value and skip_nonfinite as for a multi-tensor call
+ * mpo_sharded_step(..) == this call with one segment {0, 0, rank} and one group. */
+mpo_status mpo_sharded_step_grouped(mpo_optim kind, uintptr_t nccl_comm, int32_t rank, int32_t world,
+                                    mpo_dtype vdt, void* value_flat, void* grad_flat,
+                                    void* resid_shard, float* m_shard, float* v_shard,
+                                    int64_t n_total, const mpo_segment* seg, int32_t nseg,
+                                    const void* hp, int32_t nhp, double* norm_ws, mpo_stream stream);
+
+/* Polls an NCCL communicator for an asynchronous error (ncclCommGetAsyncError): MPO_OK while it is
+ * healthy or still initialising, MPO_ENCCL (message: ncclGetErrorString + ncclGetLastError) once a
+ * collective on it failed -- e.g. a peer died or the network reported an error.  The sharded entry
+ * points check it before issuing collectives, so a failed communicator is reported instead of
+ * hanging; a training loop can poll it between steps.  Never blocks. */
+mpo_status mpo_comm_check(uintptr_t nccl_comm);
 
 /* The sharded step fused with its collectives over NVLink SHARP: one kernel
  * per rank reads the SUM over all ranks of its shard's 16-bit gradients with multimem.ld_reduce

@@ -17,6 +17,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# The same source built with -fopenmp: element loops split across threads, nothing else changes
+# (bit-identical, tests/test_oracle_omp.py).  Only bench.py's all-core CPU baseline uses it.
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
 
 FMT = {"fp16": 0, "bf16": 1, "fp32": 2}
 
@@ -24,13 +27,23 @@ CFLAGS = ["-std=c99", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fno-unsafe
           "-fPIC", "-shared", "-Wall"]
 
 
+def _build_one(out: str, extra) -> str:
+    if not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        tmp = out + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, *extra, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, out)
+    return out
+
+
 def build(force: bool = False) -> str:
-    """Compile liboracle.so with gcc (building the checker is not using it)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
-    return _LIB
+    """Compile liboracle.so (and the OpenMP build liboracle_omp.so) with gcc (building the checker
+    is not using it)."""
+    if force:
+        for f in (_LIB, _LIB_OMP):
+            if os.path.exists(f):
+                os.unlink(f)
+    _build_one(_LIB_OMP, ["-fopenmp"])
+    return _build_one(_LIB, [])
 
 
 class SgdHP(C.Structure):
@@ -46,51 +59,69 @@ class AdamHP(C.Structure):
 
 
 _lib = None
+_lib_omp = None
+_parallel = False
+
+
+def parallel(on: bool = True, threads: int = 0) -> int:
+    """Route the wrappers below through the OpenMP build (``on``) with ``threads`` threads (0: all
+    of OpenMP's default, i.e. every core of the affinity mask), or back to the plain build.
+    Returns the thread count in effect."""
+    global _parallel
+    _parallel = bool(on)
+    return int(lib().or_threads(int(threads)))
 
 
 def lib():
-    global _lib
+    global _lib, _lib_omp
     if _lib is None:
-        _lib = C.CDLL(build())
-        L = _lib
-        L.or_fpenv_clear.restype = C.c_uint
-        L.or_fpenv_ok.restype = C.c_int
-        L.or_rne16.restype = C.c_uint16
-        L.or_rne16.argtypes = [C.c_int, C.c_uint32]
-        L.or_widen16.restype = C.c_uint32
-        L.or_widen16.argtypes = [C.c_int, C.c_uint16]
-        P = C.c_void_p
-        L.or_split.argtypes = [C.c_int, P, P, P, C.c_int64]
-        L.or_reconstruct.argtypes = [C.c_int, P, P, P, C.c_int64]
-        L.or_cast16.argtypes = [C.c_int, P, P, C.c_int64]
-        L.or_widen.argtypes = [C.c_int, P, P, C.c_int64]
-        L.or_sgd_step.argtypes = [C.c_int, C.c_int, P, P, P, P, C.c_int64, C.POINTER(SgdHP)]
-        L.or_adam_step.argtypes = [C.c_int, C.c_int, P, P, P, P, P, C.c_int64,
-                                   C.POINTER(AdamHP), C.c_float]
-        L.or_sgd_step_master.argtypes = [C.c_int, P, P, P, C.c_int64, C.POINTER(SgdHP)]
-        L.or_adam_step_master.argtypes = [C.c_int, P, P, P, P, C.c_int64, C.POINTER(AdamHP),
-                                          C.c_float]
-        L.or_sumsq.restype = C.c_double
-        L.or_sumsq.argtypes = [C.c_int, P, C.c_int64, C.c_double]
-        L.or_clip_coef.restype = C.c_float
-        L.or_clip_coef.argtypes = [C.c_double, C.c_double]
-        L.or_rtz16.restype = C.c_uint16
-        L.or_rtz16.argtypes = [C.c_int, C.c_uint32]
-        L.or_sr16.restype = C.c_uint16
-        L.or_sr16.argtypes = [C.c_uint32, C.c_uint32]
-        L.or_mix64.restype = C.c_uint64
-        L.or_mix64.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
-        L.or_split_s.argtypes = [C.c_int, C.c_int, P, P, P, C.c_int64, C.c_uint64, C.c_uint64]
-        L.or_reconstruct_s.argtypes = [C.c_int, C.c_int, P, P, P, C.c_int64]
-        L.or_sgd_step_s.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, P, C.c_int64, C.POINTER(SgdHP),
-                                    C.c_uint64, C.c_uint64]
-        L.or_adam_step_s.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, P, P, C.c_int64, C.POINTER(AdamHP),
-                                     C.c_float, C.c_uint64, C.c_uint64]
-        L.or_reduce_sum16.argtypes = [C.c_int, C.c_int, P, P, C.c_int64]
-        L.or_bytes_per_param.restype = C.c_int
-        L.or_bytes_per_param.argtypes = [C.c_int, C.c_int]
-        L.or_fpenv_clear()
-    return _lib
+        build()
+        _lib = _declare(C.CDLL(_LIB))
+        _lib_omp = _declare(C.CDLL(_LIB_OMP))
+    return _lib_omp if _parallel else _lib
+
+
+def _declare(L):
+    L.or_fpenv_clear.restype = C.c_uint
+    L.or_fpenv_ok.restype = C.c_int
+    L.or_rne16.restype = C.c_uint16
+    L.or_rne16.argtypes = [C.c_int, C.c_uint32]
+    L.or_widen16.restype = C.c_uint32
+    L.or_widen16.argtypes = [C.c_int, C.c_uint16]
+    P = C.c_void_p
+    L.or_split.argtypes = [C.c_int, P, P, P, C.c_int64]
+    L.or_reconstruct.argtypes = [C.c_int, P, P, P, C.c_int64]
+    L.or_cast16.argtypes = [C.c_int, P, P, C.c_int64]
+    L.or_widen.argtypes = [C.c_int, P, P, C.c_int64]
+    L.or_sgd_step.argtypes = [C.c_int, C.c_int, P, P, P, P, C.c_int64, C.POINTER(SgdHP)]
+    L.or_adam_step.argtypes = [C.c_int, C.c_int, P, P, P, P, P, C.c_int64,
+                               C.POINTER(AdamHP), C.c_float]
+    L.or_sgd_step_master.argtypes = [C.c_int, P, P, P, C.c_int64, C.POINTER(SgdHP)]
+    L.or_adam_step_master.argtypes = [C.c_int, P, P, P, P, C.c_int64, C.POINTER(AdamHP),
+                                      C.c_float]
+    L.or_sumsq.restype = C.c_double
+    L.or_sumsq.argtypes = [C.c_int, P, C.c_int64, C.c_double]
+    L.or_clip_coef.restype = C.c_float
+    L.or_clip_coef.argtypes = [C.c_double, C.c_double]
+    L.or_rtz16.restype = C.c_uint16
+    L.or_rtz16.argtypes = [C.c_int, C.c_uint32]
+    L.or_sr16.restype = C.c_uint16
+    L.or_sr16.argtypes = [C.c_uint32, C.c_uint32]
+    L.or_mix64.restype = C.c_uint64
+    L.or_mix64.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+    L.or_split_s.argtypes = [C.c_int, C.c_int, P, P, P, C.c_int64, C.c_uint64, C.c_uint64]
+    L.or_reconstruct_s.argtypes = [C.c_int, C.c_int, P, P, P, C.c_int64]
+    L.or_sgd_step_s.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, P, C.c_int64, C.POINTER(SgdHP),
+                                C.c_uint64, C.c_uint64]
+    L.or_adam_step_s.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, P, P, C.c_int64, C.POINTER(AdamHP),
+                                 C.c_float, C.c_uint64, C.c_uint64]
+    L.or_reduce_sum16.argtypes = [C.c_int, C.c_int, P, P, C.c_int64]
+    L.or_bytes_per_param.restype = C.c_int
+    L.or_bytes_per_param.argtypes = [C.c_int, C.c_int]
+    L.or_threads.restype = C.c_int
+    L.or_threads.argtypes = [C.c_int]
+    L.or_fpenv_clear()
+    return L
 
 
 def _ptr(a):

@@ -29,6 +29,28 @@
 #include <xmmintrin.h>
 #endif
 
+/* Element loops are independent (the method is elementwise), so the all-core baseline build
+ * (gcc -fopenmp: liboracle_omp.so, bench.py's cpu_baseline "threads_all") splits them across
+ * threads with no other change; the plain build ignores the annotation.  Both builds are
+ * bit-identical (tests/test_oracle_omp.py). */
+#ifdef _OPENMP
+#include <omp.h>
+#define OR_PARALLEL_FOR _Pragma("omp parallel for schedule(static)")
+#else
+#define OR_PARALLEL_FOR
+#endif
+
+/* Threads of the parallel build (1 in the plain build). */
+int or_threads(int set) {
+#ifdef _OPENMP
+    if (set > 0) omp_set_num_threads(set);
+    return omp_get_max_threads();
+#else
+    (void)set;
+    return 1;
+#endif
+}
+
 /* Format codes of THIS oracle (independent of the CUDA library's enum). */
 #define OR_FP16 0
 #define OR_BF16 1
@@ -166,11 +188,13 @@ static uint32_t reconstruct1(int fmt, uint16_t h, int16_t r) {
 
 void or_split(int fmt, const float* w, uint16_t* value, int16_t* resid, int64_t n) {
     int64_t i;
+    OR_PARALLEL_FOR
     for (i = 0; i < n; i++) split1(fmt, f2u(w[i]), &value[i], &resid[i]);
 }
 
 void or_reconstruct(int fmt, const uint16_t* value, const int16_t* resid, float* w, int64_t n) {
     int64_t i;
+    OR_PARALLEL_FOR
     for (i = 0; i < n; i++) w[i] = u2f(reconstruct1(fmt, value[i], resid[i]));
 }
 
@@ -286,6 +310,7 @@ void or_sgd_step(int vfmt, int gfmt, uint16_t* value, int16_t* resid, const void
                  float* buf, int64_t n, const or_sgd_hp* hp) {
     int64_t i;
     float gs = (float)hp->grad_scale;
+    OR_PARALLEL_FOR
     for (i = 0; i < n; i++) {
         float g = clamp_grad(load_grad(gfmt, grad, i) * gs, hp->clip_value);
         float w = u2f(reconstruct1(vfmt, value[i], resid[i]));
@@ -302,6 +327,7 @@ void or_adam_step(int vfmt, int gfmt, uint16_t* value, int16_t* resid, const voi
     int64_t i;
     float gs = (float)hp->grad_scale;
     adam_scalars c = adam_derive(hp);
+    OR_PARALLEL_FOR
     for (i = 0; i < n; i++) {
         float g = clamp_grad(load_grad(gfmt, grad, i) * gs, hp->clip_value);
         float w;
@@ -318,6 +344,7 @@ void or_sgd_step_master(int gfmt, float* w, const void* grad, float* buf, int64_
                         const or_sgd_hp* hp) {
     int64_t i;
     float gs = (float)hp->grad_scale;
+    OR_PARALLEL_FOR
     for (i = 0; i < n; i++) {
         float g = clamp_grad(load_grad(gfmt, grad, i) * gs, hp->clip_value);
         w[i] = sgd_update(w[i], g, buf ? &buf[i] : 0, hp);
@@ -329,6 +356,7 @@ void or_adam_step_master(int gfmt, float* w, const void* grad, float* m, float* 
     int64_t i;
     float gs = (float)hp->grad_scale;
     adam_scalars c = adam_derive(hp);
+    OR_PARALLEL_FOR
     for (i = 0; i < n; i++) {
         float g = clamp_grad(load_grad(gfmt, grad, i) * gs, hp->clip_value);
         if (clip_coef >= 0.0f || clip_coef != clip_coef) g = g * clip_coef;
@@ -468,6 +496,7 @@ static uint32_t draw(int scheme, uint64_t seed, uint64_t stream, int64_t i) {
 void or_split_s(int scheme, int fmt, const float* w, uint16_t* value, void* resid, int64_t n, uint64_t seed,
                 uint64_t stream) {
     int64_t i;
+    OR_PARALLEL_FOR
     for (i = 0; i < n; i++) {
         uint16_t h; int32_t r;
         split_s(scheme, fmt, f2u(w[i]), draw(scheme, seed, stream, i), &h, &r);
@@ -478,6 +507,7 @@ void or_split_s(int scheme, int fmt, const float* w, uint16_t* value, void* resi
 
 void or_reconstruct_s(int scheme, int fmt, const uint16_t* value, const void* resid, float* w, int64_t n) {
     int64_t i;
+    OR_PARALLEL_FOR
     for (i = 0; i < n; i++) w[i] = u2f(reconstruct_s(scheme, fmt, value[i], load_resid(scheme, resid, i)));
 }
 
@@ -487,6 +517,7 @@ void or_sgd_step_s(int scheme, int vfmt, int gfmt, uint16_t* value, void* resid,
                    int64_t n, const or_sgd_hp* hp, uint64_t seed, uint64_t stream) {
     int64_t i;
     float gs = (float)hp->grad_scale;
+    OR_PARALLEL_FOR
     for (i = 0; i < n; i++) {
         float g = clamp_grad(load_grad(gfmt, grad, i) * gs, hp->clip_value);
         float w = u2f(reconstruct_s(scheme, vfmt, value[i], load_resid(scheme, resid, i)));
@@ -503,6 +534,7 @@ void or_adam_step_s(int scheme, int vfmt, int gfmt, uint16_t* value, void* resid
     int64_t i;
     float gs = (float)hp->grad_scale;
     adam_scalars c = adam_derive(hp);
+    OR_PARALLEL_FOR
     for (i = 0; i < n; i++) {
         float g = clamp_grad(load_grad(gfmt, grad, i) * gs, hp->clip_value);
         float w;

@@ -25,7 +25,8 @@ MPO_MAX_HP_GROUPS = 16
 SYMBOLS = ("mpo_split", "mpo_reconstruct", "mpo_sgd_step", "mpo_adam_step", "mpo_norm_ws_doubles",
            "mpo_fused_backward_hook_step", "mpo_sharded_step", "mpo_last_error", "mpo_build_exact",
            "mpo_launch_count", "mpo_selfcheck_fastmath", "mpo_nvls_sharded_step", "mpo_nvls_alloc_local",
-           "mpo_nvls_free_local", "mpo_p2p_sharded_step")
+           "mpo_nvls_free_local", "mpo_p2p_sharded_step", "mpo_grad_sumsq", "mpo_sharded_step_grouped",
+           "mpo_comm_check")
 
 
 class MpoError(RuntimeError):
@@ -45,7 +46,7 @@ class SgdHP(C.Structure):
     _fields_ = [("lr", C.c_double), ("momentum", C.c_double), ("dampening", C.c_double),
                 ("weight_decay", C.c_double), ("grad_scale", C.c_double), ("nesterov", C.c_int32),
                 ("first_step", C.c_int32), ("seed", C.c_uint64), ("clip_value", C.c_double),
-                ("skip_nonfinite", C.c_int32), ("_pad2", C.c_int32)]
+                ("skip_nonfinite", C.c_int32), ("norm_ready", C.c_int32)]
 
 
 class AdamHP(C.Structure):
@@ -53,7 +54,12 @@ class AdamHP(C.Structure):
     _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
                 ("weight_decay", C.c_double), ("grad_scale", C.c_double), ("max_grad_norm", C.c_double),
                 ("adamw", C.c_int32), ("_pad", C.c_int32), ("step", C.c_int64), ("seed", C.c_uint64),
-                ("clip_value", C.c_double), ("skip_nonfinite", C.c_int32), ("_pad2", C.c_int32)]
+                ("clip_value", C.c_double), ("skip_nonfinite", C.c_int32), ("norm_ready", C.c_int32)]
+
+
+class Segment(C.Structure):
+    """mpo_segment"""
+    _fields_ = [("start", C.c_int64), ("hp", C.c_int32), ("sr_stream", C.c_int32)]
 
 
 _libs: dict = {}
@@ -67,8 +73,12 @@ def _declare(L):
     L.mpo_adam_step.argtypes = [D, D, C.POINTER(Tensor), I32, C.POINTER(AdamHP), I32, P, P]
     L.mpo_fused_backward_hook_step.argtypes = [D, D, D, C.POINTER(Tensor), P, P, P]
     L.mpo_sharded_step.argtypes = [D, C.c_size_t, I32, I32, D, P, P, P, P, P, I64, P, P, P]
+    L.mpo_sharded_step_grouped.argtypes = [D, C.c_size_t, I32, I32, D, P, P, P, P, P, I64, C.POINTER(Segment), I32,
+                                           P, I32, P, P]
+    L.mpo_grad_sumsq.argtypes = [D, C.POINTER(Tensor), I32, C.POINTER(C.c_double), I32, P, I32, P]
+    L.mpo_comm_check.argtypes = [C.c_size_t]
     for f in ("mpo_split", "mpo_reconstruct", "mpo_sgd_step", "mpo_adam_step", "mpo_fused_backward_hook_step",
-              "mpo_sharded_step"):
+              "mpo_sharded_step", "mpo_sharded_step_grouped", "mpo_grad_sumsq", "mpo_comm_check"):
         getattr(L, f).restype = C.c_int
     L.mpo_last_error.restype = C.c_char_p
     L.mpo_last_error.argtypes = []

@@ -13,7 +13,7 @@ from typing import Optional, Sequence
 import torch
 
 from . import _lib
-from ._lib import MPO_ADAM, MPO_BF16, MPO_FP16, MPO_FP32, MPO_SGD, AdamHP, MpoError, SgdHP, Tensor
+from ._lib import MPO_ADAM, MPO_BF16, MPO_FP16, MPO_FP32, MPO_SGD, AdamHP, MpoError, Segment, SgdHP, Tensor
 
 _DT = {torch.float16: MPO_FP16, torch.bfloat16: MPO_BF16, torch.float32: MPO_FP32}
 _VALUE_VIEW = {torch.float16, torch.bfloat16}
@@ -87,11 +87,12 @@ class SgdParams:
     seed: int = 0
     clip_value: float = 0.0
     skip_nonfinite: bool = False
+    norm_ready: bool = False
 
     def c(self) -> SgdHP:
         return SgdHP(self.lr, self.momentum, self.dampening, self.weight_decay, self.grad_scale,
                      int(self.nesterov), int(self.first_step), int(self.seed), float(self.clip_value),
-                     int(self.skip_nonfinite), 0)
+                     int(self.skip_nonfinite), int(self.norm_ready))
 
 
 @dataclass
@@ -108,11 +109,12 @@ class AdamParams:
     seed: int = 0
     clip_value: float = 0.0
     skip_nonfinite: bool = False
+    norm_ready: bool = False
 
     def c(self) -> AdamHP:
         return AdamHP(self.lr, self.beta1, self.beta2, self.eps, self.weight_decay, self.grad_scale,
                       self.max_grad_norm, int(self.adamw), 0, int(self.step), int(self.seed),
-                      float(self.clip_value), int(self.skip_nonfinite), 0)
+                      float(self.clip_value), int(self.skip_nonfinite), int(self.norm_ready))
 
 
 def _hp_array(hps, kind):
@@ -255,15 +257,47 @@ def mpo_fused_backward_hook_step(kind: int, vdt: int, gdt: int, one: Tensor, hp,
 def mpo_sharded_step(kind: int, comm_ptr: int, rank: int, world: int, value_flat: torch.Tensor,
                      grad_flat: torch.Tensor, resid_shard: torch.Tensor, m_shard: Optional[torch.Tensor],
                      v_shard: Optional[torch.Tensor], hp, norm_ws: Optional[torch.Tensor] = None, stream=None,
-                     exact: bool = False, scheme: str = "rne"):
-    """Data-parallel sharded step: RS(grad) -> shard update -> AG(value) (BASELINE north_star (c))."""
+                     exact: bool = False, scheme: str = "rne", segments=None):
+    """Data-parallel sharded step: RS(grad) -> shard update -> AG(value) (BASELINE north_star (c)).
+
+    ``hp``: one hyper-parameter set, or a list of groups together with ``segments``, a list of
+    (start in the shard, group index, sr_stream) pieces partitioning this rank's shard
+    (mpo_sharded_step_grouped)."""
     if grad_flat.dtype != value_flat.dtype or grad_flat.numel() != value_flat.numel():
         raise MpoError(_lib.MPO_EINVAL, "grad_flat must match value_flat in dtype and size")
     L = _lib_of(exact)
-    chp = hp.c() if hasattr(hp, "c") else hp
-    _lib.check(L, L.mpo_sharded_step(kind, comm_ptr, rank, world, format_code(value_flat.dtype, scheme), _ptr(value_flat),
-                                     _ptr(grad_flat), _ptr(resid_shard), _ptr(m_shard), _ptr(v_shard),
-                                     value_flat.numel(), C.byref(chp), _ptr(norm_ws), _stream(stream)))
+    vdt = format_code(value_flat.dtype, scheme)
+    if segments is None and not isinstance(hp, (list, tuple)):
+        chp = hp.c() if hasattr(hp, "c") else hp
+        _lib.check(L, L.mpo_sharded_step(kind, comm_ptr, rank, world, vdt, _ptr(value_flat), _ptr(grad_flat),
+                                         _ptr(resid_shard), _ptr(m_shard), _ptr(v_shard), value_flat.numel(),
+                                         C.byref(chp), _ptr(norm_ws), _stream(stream)))
+        return
+    hps = list(hp) if isinstance(hp, (list, tuple)) else [hp]
+    segments = segments if segments is not None else [(0, 0, rank)]
+    arr, nhp = _hp_array(hps, AdamHP if kind == MPO_ADAM else SgdHP)
+    seg = (Segment * len(segments))(*[Segment(int(a), int(h), int(s)) for a, h, s in segments])
+    _lib.check(L, L.mpo_sharded_step_grouped(kind, comm_ptr, rank, world, vdt, _ptr(value_flat), _ptr(grad_flat),
+                                             _ptr(resid_shard), _ptr(m_shard), _ptr(v_shard), value_flat.numel(),
+                                             seg, len(segments), C.cast(arr, C.c_void_p), nhp, _ptr(norm_ws),
+                                             _stream(stream)))
+
+
+def mpo_grad_sumsq(table: TensorTable, grad_scales, norm_ws: torch.Tensor, accumulate: bool = False, stream=None,
+                   exact: bool = False):
+    """S = sum (f32(g) * grad_scale[group])^2 over a table into norm_ws[0] (``accumulate``: added to it);
+    the shared pre-pass of a step spanning several tables (include/mpo.h norm_ready)."""
+    gs = (C.c_double * len(grad_scales))(*[float(x) for x in grad_scales])
+    L = _lib_of(exact)
+    _check_ws(norm_ws, exact)
+    _lib.check(L, L.mpo_grad_sumsq(table.gdt, table.arr, table.nt, gs, len(grad_scales), _ptr(norm_ws),
+                                   int(bool(accumulate)), _stream(stream)))
+
+
+def mpo_comm_check(comm_ptr: int, exact: bool = False):
+    """Raises MpoError(MPO_ENCCL) if the NCCL communicator failed asynchronously (never blocks)."""
+    L = _lib_of(exact)
+    _lib.check(L, L.mpo_comm_check(comm_ptr))
 
 
 def mpo_selfcheck_fastmath(pairs: int = 1 << 30, seed: int = 0xB0B, exact: bool = False, stream=None):

@@ -7,6 +7,7 @@
 
 #include <mutex>
 #include <unordered_map>
+#include <vector>
 
 #define MPO_ABI_TU
 #include "mpo_kernels.cuh"
@@ -183,6 +184,8 @@ mpo_status check_adam_hp(const mpo_adam_hp* hp, int32_t nhp) {
             return fail(MPO_EINVAL, "adam group " + std::to_string(i) + ": clip_value and max_grad_norm are exclusive");
         if ((h.skip_nonfinite != 0) != (hp[0].skip_nonfinite != 0))
             return fail(MPO_EINVAL, "adam group " + std::to_string(i) + ": skip_nonfinite differs from group 0");
+        if ((h.norm_ready != 0) != (hp[0].norm_ready != 0))
+            return fail(MPO_EINVAL, "adam group " + std::to_string(i) + ": norm_ready differs from group 0");
     }
     return MPO_OK;
 }
@@ -200,6 +203,8 @@ mpo_status check_sgd_hp(const mpo_sgd_hp* hp, int32_t nhp) {
             return fail(MPO_EINVAL, "sgd group " + std::to_string(i) + ": clip_value must be finite and >= 0");
         if ((h.skip_nonfinite != 0) != (hp[0].skip_nonfinite != 0))
             return fail(MPO_EINVAL, "sgd group " + std::to_string(i) + ": skip_nonfinite differs from group 0");
+        if ((h.norm_ready != 0) != (hp[0].norm_ready != 0))
+            return fail(MPO_EINVAL, "sgd group " + std::to_string(i) + ": norm_ready differs from group 0");
     }
     return MPO_OK;
 }
@@ -264,7 +269,7 @@ mpo_status launch_sumsq(const mpo_tensor* t, int lo, int hi, const HP<float>& gs
 
 // Sum of squares of the scaled grads of the whole table into norm_ws[0] (partials in norm_ws[1..]).
 mpo_status table_sumsq(mpo_dtype gdt, const mpo_tensor* t, int nt, const float* gs_of_group, int nhp,
-                       double* norm_ws, cudaStream_t s, double* accum = nullptr) {
+                       double* norm_ws, cudaStream_t s, double* accum = nullptr, int add_out = 0) {
     HP<float> gsc;
     for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) gsc.g[i] = i < nhp ? gs_of_group[i] : 1.0f;
     int64_t tiles = 0;
@@ -288,7 +293,7 @@ mpo_status table_sumsq(mpo_dtype gdt, const mpo_tensor* t, int nt, const float* 
         nparts += nb;
         if (nt == 0) break;
     }
-    sumsq_final_kernel<<<1, kThreads, 0, s>>>(partial, nparts, norm_ws, accum);
+    sumsq_final_kernel<<<1, kThreads, 0, s>>>(partial, nparts, norm_ws, accum, add_out);
     ++g_launches;
     return check_launch("sumsq_final_kernel");
 }
@@ -408,12 +413,13 @@ static mpo_status sgd_common(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t, 
     HP<SgdK> k;
     for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) k.g[i] = derive_sgd(hp[i < nhp ? i : 0]);
     const int skip = hp[0].skip_nonfinite != 0;
-    if (skip && !sumsq_ready) {
+    if (skip && !sumsq_ready && !hp[0].norm_ready) {
         float gs[MPO_MAX_HP_GROUPS];
         for (int i = 0; i < nhp; ++i) gs[i] = k.g[i].gs;
         mpo_status st = prepass(gdt, t, nt, gs, nhp, norm_ws, s, accum);
         if (st != MPO_OK) return st;
     }
+    if (skip && !norm_ws) return fail(MPO_EINVAL, "skip_nonfinite needs a norm workspace");
     return dispatch_sgd(vdt, gdt, t, nt, k, one_hp, skip ? norm_ws : nullptr, skip, s);
 }
 
@@ -435,12 +441,13 @@ static mpo_status adam_common(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t,
     const double max_norm = hp[0].max_grad_norm;
     const int skip = hp[0].skip_nonfinite != 0;
     const bool need = max_norm > 0.0 || skip;
-    if (need && !sumsq_ready) {
+    if (need && !sumsq_ready && !hp[0].norm_ready) {
         float gs[MPO_MAX_HP_GROUPS];
         for (int i = 0; i < nhp; ++i) gs[i] = k.g[i].gs;
         mpo_status st = prepass(gdt, t, nt, gs, nhp, norm_ws, s, accum);
         if (st != MPO_OK) return st;
     }
+    if (need && !norm_ws) return fail(MPO_EINVAL, "clipping / skip_nonfinite need a norm workspace");
     return dispatch_adam(vdt, gdt, t, nt, k, one_hp, need ? norm_ws : nullptr, max_norm > 0.0 ? max_norm : 0.0, skip, s);
 }
 
@@ -469,23 +476,69 @@ MPO_API mpo_status mpo_fused_backward_hook_step(mpo_optim kind, mpo_dtype vdt, m
         if ((st = check_adam_hp(h, 1)) != MPO_OK) return st;
         if (h->max_grad_norm > 0.0)
             return fail(MPO_EINVAL, "global-norm clipping is impossible in the fused backward hook (P:93, P:186)");
+        if (h->norm_ready) return fail(MPO_EINVAL, "norm_ready is for multi-tensor calls only");
         if ((st = check_table(&x, 1, 1, true, nullptr)) != MPO_OK) return st;
         return adam_common(vdt, gdt, &x, 1, h, 1, norm_ws, true, s, false, accum);
     }
     if (kind == MPO_SGD) {
         const mpo_sgd_hp* h = static_cast<const mpo_sgd_hp*>(hp);
         if ((st = check_sgd_hp(h, 1)) != MPO_OK) return st;
+        if (h->norm_ready) return fail(MPO_EINVAL, "norm_ready is for multi-tensor calls only");
         if ((st = check_table(&x, 1, 1, false, h)) != MPO_OK) return st;
         return sgd_common(vdt, gdt, &x, 1, h, 1, norm_ws, true, s, false, accum);
     }
     return fail(MPO_EINVAL, "unknown optimizer kind");
 }
 
-MPO_API mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t rank, int32_t world, mpo_dtype vdt,
-                                    void* value_flat, void* grad_flat, void* resid_shard, float* m_shard,
-                                    float* v_shard, int64_t n_total, const void* hp, double* norm_ws,
-                                    mpo_stream stream) {
+// Asynchronous error of a communicator (ncclInProgress = still initialising: healthy).
+static mpo_status comm_status(ncclComm_t comm) {
+    ncclResult_t async = ncclSuccess;
+    const ncclResult_t r = ncclCommGetAsyncError(comm, &async);
+    if (r != ncclSuccess) return fail(MPO_ENCCL, std::string("ncclCommGetAsyncError: ") + ncclGetErrorString(r));
+    if (async != ncclSuccess && async != ncclInProgress) {
+        const char* last = ncclGetLastError(comm);
+        return fail(MPO_ENCCL, std::string("communicator failed asynchronously: ") + ncclGetErrorString(async) +
+                                   (last && *last ? std::string(" (") + last + ")" : std::string()));
+    }
+    return MPO_OK;
+}
+
+MPO_API mpo_status mpo_comm_check(uintptr_t nccl_comm) {
     g_err.clear();
+    if (!nccl_comm) return fail(MPO_EINVAL, "NULL NCCL communicator");
+    return comm_status(reinterpret_cast<ncclComm_t>(nccl_comm));
+}
+
+MPO_API mpo_status mpo_grad_sumsq(mpo_dtype gdt, const mpo_tensor* t, int32_t nt, const double* grad_scale,
+                                  int32_t nhp, double* norm_ws, int32_t accumulate, mpo_stream stream) {
+    g_err.clear();
+    if (gdt != MPO_FP16 && gdt != MPO_BF16 && gdt != MPO_FP32)
+        return fail(MPO_EDTYPE, "grad dtype must be MPO_FP16, MPO_BF16 or MPO_FP32");
+    if (!grad_scale || nhp < 1 || nhp > MPO_MAX_HP_GROUPS) return fail(MPO_EINVAL, "grad_scale group count out of range");
+    if (!norm_ws) return fail(MPO_EINVAL, "NULL norm workspace");
+    if (nt < 0 || (nt > 0 && !t)) return fail(MPO_EINVAL, "bad tensor table");
+    float gs[MPO_MAX_HP_GROUPS];
+    for (int i = 0; i < nhp; ++i) {
+        if (!std::isfinite(grad_scale[i])) return fail(MPO_EINVAL, "non-finite grad_scale (group " + std::to_string(i) + ")");
+        gs[i] = float(grad_scale[i]);
+    }
+    for (int i = 0; i < nt; ++i) {
+        const std::string who = "tensor " + std::to_string(i) + ": ";
+        if (t[i].n < 0) return fail(MPO_EINVAL, who + "negative size");
+        if (t[i].hp < 0 || t[i].hp >= nhp) return fail(MPO_EINVAL, who + "hyper-parameter group index out of range");
+        if (t[i].n == 0) continue;
+        if (!t[i].grad) return fail(MPO_EINVAL, who + "NULL gradient");
+        if (!aligned16(t[i].grad)) return fail(MPO_EALIGN, who + "gradient not 16-byte aligned");
+    }
+    return table_sumsq(gdt, t, nt, gs, nhp, norm_ws, static_cast<cudaStream_t>(stream), nullptr, accumulate != 0);
+}
+
+// The sharded step over the pieces (segments) of this rank's shard: RS -> [sumsq + AllReduce] ->
+// one multi-tensor step over the pieces -> AG.
+static mpo_status sharded_common(mpo_optim kind, uintptr_t nccl_comm, int32_t rank, int32_t world, mpo_dtype vdt,
+                                 void* value_flat, void* grad_flat, void* resid_shard, float* m_shard, float* v_shard,
+                                 int64_t n_total, const mpo_segment* seg, int32_t nseg, const void* hp, int32_t nhp,
+                                 double* norm_ws, cudaStream_t s) {
     mpo_status st;
     if (!nccl_comm) return fail(MPO_EINVAL, "NULL NCCL communicator");
     if (world < 1 || rank < 0 || rank >= world) return fail(MPO_EINVAL, "bad rank / world");
@@ -495,58 +548,102 @@ MPO_API mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t
     const mpo_dtype gdt = mpo_dtype(is_value_format(vdt) ? base_of(vdt) : vdt);
     if ((st = check_dtypes(vdt, gdt)) != MPO_OK) return st;
     if (kind != MPO_SGD && kind != MPO_ADAM) return fail(MPO_EINVAL, "unknown optimizer kind");
-    if (n_total == 0) return MPO_OK;
-    if (!value_flat || !grad_flat) return fail(MPO_EINVAL, "NULL flat buffer");
-    if (!aligned16(value_flat) || !aligned16(grad_flat)) return fail(MPO_EALIGN, "flat buffer not 16-byte aligned");
-    ncclComm_t comm = reinterpret_cast<ncclComm_t>(nccl_comm);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int64_t shard = n_total / world;
-    mpo_tensor x;
-    x.value = static_cast<uint16_t*>(value_flat) + rank * shard;
-    x.resid = resid_shard;
-    x.grad = static_cast<uint16_t*>(grad_flat) + rank * shard;
-    x.m = m_shard;
-    x.v = v_shard;
-    x.n = shard;
-    x.hp = 0;
-    x.sr_stream = rank;   // distinct stochastic-rounding streams per shard
     if (kind == MPO_ADAM) {
         const mpo_adam_hp* h = static_cast<const mpo_adam_hp*>(hp);
-        if ((st = check_adam_hp(h, 1)) != MPO_OK) return st;
-        if ((st = check_table(&x, 1, 1, true, nullptr)) != MPO_OK) return st;
-        if ((h->max_grad_norm > 0.0 || h->skip_nonfinite) && !norm_ws)
+        if ((st = check_adam_hp(h, nhp)) != MPO_OK) return st;
+        if (h[0].norm_ready) return fail(MPO_EINVAL, "norm_ready is for multi-tensor calls only");
+        if ((h[0].max_grad_norm > 0.0 || h[0].skip_nonfinite) && !norm_ws)
             return fail(MPO_EINVAL, "clipping / skip_nonfinite need a norm workspace");
     } else {
         const mpo_sgd_hp* h = static_cast<const mpo_sgd_hp*>(hp);
-        if ((st = check_sgd_hp(h, 1)) != MPO_OK) return st;
-        if ((st = check_table(&x, 1, 1, false, h)) != MPO_OK) return st;
-        if (h->skip_nonfinite && !norm_ws) return fail(MPO_EINVAL, "skip_nonfinite needs a norm workspace");
+        if ((st = check_sgd_hp(h, nhp)) != MPO_OK) return st;
+        if (h[0].norm_ready) return fail(MPO_EINVAL, "norm_ready is for multi-tensor calls only");
+        if (h[0].skip_nonfinite && !norm_ws) return fail(MPO_EINVAL, "skip_nonfinite needs a norm workspace");
     }
+    if (n_total == 0) return MPO_OK;
+    if (!value_flat || !grad_flat) return fail(MPO_EINVAL, "NULL flat buffer");
+    if (!aligned16(value_flat) || !aligned16(grad_flat)) return fail(MPO_EALIGN, "flat buffer not 16-byte aligned");
+    const int64_t shard = n_total / world;
+    // the pieces of this rank's shard, as a table (each piece 16-B aligned in every array)
+    if (!seg || nseg < 1) return fail(MPO_EINVAL, "need at least one segment");
+    if (!resid_shard) return fail(MPO_EINVAL, "NULL residual shard");
+    const int64_t gran = resid_bytes(vdt) == 1 ? 16 : 8;
+    std::vector<mpo_tensor> tab(static_cast<size_t>(nseg));
+    for (int i = 0; i < nseg; ++i) {
+        const int64_t a = seg[i].start, b = i + 1 < nseg ? seg[i + 1].start : shard;
+        const std::string who = "segment " + std::to_string(i) + ": ";
+        if ((i == 0 && a != 0) || a < 0 || b <= a || b > shard)
+            return fail(MPO_EINVAL, who + "starts must begin at 0 and increase strictly inside the shard");
+        if (a % gran != 0)
+            return fail(MPO_EINVAL, who + "start must be a multiple of " + std::to_string(gran) + " elements");
+        mpo_tensor& x = tab[size_t(i)];
+        x.value = static_cast<uint16_t*>(value_flat) + rank * shard + a;
+        x.resid = static_cast<unsigned char*>(resid_shard) + a * resid_bytes(vdt);
+        x.grad = static_cast<uint16_t*>(grad_flat) + rank * shard + a;
+        x.m = m_shard ? m_shard + a : nullptr;
+        x.v = v_shard ? v_shard + a : nullptr;
+        x.n = b - a;
+        x.hp = seg[i].hp;
+        x.sr_stream = seg[i].sr_stream;
+    }
+    if (kind == MPO_ADAM) {
+        if ((st = check_table(tab.data(), nseg, nhp, true, nullptr)) != MPO_OK) return st;
+    } else {
+        if ((st = check_table(tab.data(), nseg, nhp, false, static_cast<const mpo_sgd_hp*>(hp))) != MPO_OK) return st;
+    }
+    ncclComm_t comm = reinterpret_cast<ncclComm_t>(nccl_comm);
+    // a communicator that already failed asynchronously is reported instead of hanging
+    if ((st = comm_status(comm)) != MPO_OK) return st;
+    void* grad_shard = static_cast<uint16_t*>(grad_flat) + rank * shard;
     // 1. reduce-scatter of the 16-bit gradients (sum), in place: shard `rank` of grad_flat
     //    (world 1: the reduction of one rank is the identity and the in-place shard is the buffer)
     if (world > 1)
-        MPO_NCCL(ncclReduceScatter(grad_flat, const_cast<void*>(x.grad), size_t(shard), nccl_dtype(vdt), ncclSum, comm, s));
-    // 2. residual-compensated update of this rank's shard
+        MPO_NCCL(ncclReduceScatter(grad_flat, grad_shard, size_t(shard), nccl_dtype(vdt), ncclSum, comm, s));
+    // 2. residual-compensated update of this rank's pieces
     //    (clipping / found-inf: the shard's sum of squares, all-reduced so every rank agrees)
     const bool need = kind == MPO_ADAM ? (static_cast<const mpo_adam_hp*>(hp)->max_grad_norm > 0.0 ||
                                           static_cast<const mpo_adam_hp*>(hp)->skip_nonfinite != 0)
                                        : static_cast<const mpo_sgd_hp*>(hp)->skip_nonfinite != 0;
     if (need) {
-        const float gs = float(kind == MPO_ADAM ? static_cast<const mpo_adam_hp*>(hp)->grad_scale
-                                                : static_cast<const mpo_sgd_hp*>(hp)->grad_scale);
-        if ((st = prepass(gdt, &x, 1, &gs, 1, norm_ws, s)) != MPO_OK) return st;
+        float gs[MPO_MAX_HP_GROUPS];
+        for (int i = 0; i < nhp; ++i)
+            gs[i] = float(kind == MPO_ADAM ? static_cast<const mpo_adam_hp*>(hp)[i].grad_scale
+                                           : static_cast<const mpo_sgd_hp*>(hp)[i].grad_scale);
+        if ((st = prepass(gdt, tab.data(), nseg, gs, nhp, norm_ws, s)) != MPO_OK) return st;
         if (world > 1) MPO_NCCL(ncclAllReduce(norm_ws, norm_ws, 1, ncclFloat64, ncclSum, comm, s));
     }
     if (kind == MPO_ADAM) {
         const mpo_adam_hp* h = static_cast<const mpo_adam_hp*>(hp);
-        if ((st = adam_common(vdt, gdt, &x, 1, h, 1, norm_ws, true, s, true)) != MPO_OK) return st;
+        if ((st = adam_common(vdt, gdt, tab.data(), nseg, h, nhp, norm_ws, false, s, true)) != MPO_OK) return st;
     } else {
         const mpo_sgd_hp* h = static_cast<const mpo_sgd_hp*>(hp);
-        if ((st = sgd_common(vdt, gdt, &x, 1, h, 1, norm_ws, true, s, true)) != MPO_OK) return st;
+        if ((st = sgd_common(vdt, gdt, tab.data(), nseg, h, nhp, norm_ws, false, s, true)) != MPO_OK) return st;
     }
     // 3. all-gather of the 16-bit values only (residual and state never move)
-    if (world > 1) MPO_NCCL(ncclAllGather(x.value, value_flat, size_t(shard), nccl_dtype(vdt), comm, s));
+    if (world > 1)
+        MPO_NCCL(ncclAllGather(static_cast<uint16_t*>(value_flat) + rank * shard, value_flat, size_t(shard),
+                               nccl_dtype(vdt), comm, s));
     return MPO_OK;
+}
+
+MPO_API mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t rank, int32_t world, mpo_dtype vdt,
+                                    void* value_flat, void* grad_flat, void* resid_shard, float* m_shard,
+                                    float* v_shard, int64_t n_total, const void* hp, double* norm_ws,
+                                    mpo_stream stream) {
+    g_err.clear();
+    const mpo_segment one{0, 0, rank};   // the shard's stochastic-rounding stream is its rank
+    return sharded_common(kind, nccl_comm, rank, world, vdt, value_flat, grad_flat, resid_shard, m_shard, v_shard,
+                          n_total, &one, 1, hp, 1, norm_ws, static_cast<cudaStream_t>(stream));
+}
+
+MPO_API mpo_status mpo_sharded_step_grouped(mpo_optim kind, uintptr_t nccl_comm, int32_t rank, int32_t world,
+                                            mpo_dtype vdt, void* value_flat, void* grad_flat, void* resid_shard,
+                                            float* m_shard, float* v_shard, int64_t n_total, const mpo_segment* seg,
+                                            int32_t nseg, const void* hp, int32_t nhp, double* norm_ws,
+                                            mpo_stream stream) {
+    g_err.clear();
+    return sharded_common(kind, nccl_comm, rank, world, vdt, value_flat, grad_flat, resid_shard, m_shard, v_shard,
+                          n_total, seg, nseg, hp, nhp, norm_ws, static_cast<cudaStream_t>(stream));
 }
 
 

@@ -455,15 +455,17 @@ __global__ void __launch_bounds__(kThreads) sumsq_kernel(const __grid_constant__
     if (threadIdx.x == 0) partial[blockIdx.x] = acc;
 }
 
-// Sums nparts partials (fixed order) into out[0].
+// Sums nparts partials (fixed order) into out[0] (add_out: out[0] += the sum, mpo_grad_sumsq's
+// accumulation over several tables of one step).
 __global__ void __launch_bounds__(kThreads) sumsq_final_kernel(const double* __restrict__ partial, int nparts,
-                                                               double* __restrict__ out, double* __restrict__ accum) {
+                                                               double* __restrict__ out, double* __restrict__ accum,
+                                                               int add_out) {
     __shared__ double sh[32];
     double acc = 0.0;
     for (int i = threadIdx.x; i < nparts; i += blockDim.x) acc += partial[i];
     acc = block_sum(acc, sh);
     if (threadIdx.x == 0) {
-        out[0] = acc;
+        out[0] = add_out ? out[0] + acc : acc;
         if (accum) accum[0] += acc;   // hook mode: found-inf over a whole backward
     }
 }
@@ -790,6 +792,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+#ifdef MPO_BULK_ST
+// 1-D bulk copy shared -> global (async proxy, bulk-group completion), the store side of the
+// A/B "MPO_BULK_ST": each consumer warp writes its outputs over its inputs in the stage and one
+// lane streams them out as four bulk copies instead of 6 x 128-bit STG per thread.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+#endif
+
 template <int G>
 struct GradBytes {
     static constexpr int v = G == kFP32 ? 4 : 2;
@@ -981,6 +997,45 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
 #else
         if (full_unit) process_unit<SF, G, Op, CLIP>(hv, rv, gu, mm, vv, c, coef, stream_of(T), base + el, ho, ro);
 #endif
+#if defined(MPO_BULK_ST)
+        {
+            // outputs over this thread's own inputs in the stage, then one lane of the warp
+            // streams the warp's contiguous 256-element slice out with bulk copies
+            unsigned char* st = ring + size_t(s) * SB;
+            const bool wm = Op::writes_m(c);
+            if (full_unit) {
+                *reinterpret_cast<uint4*>(st + el * 2) = ho;
+                if constexpr (RB == 2) *reinterpret_cast<uint4*>(st + OFF_R + el * 2) = ro.v;
+                else *reinterpret_cast<uint2*>(st + OFF_R + el) = make_uint2(ro.v.x, ro.v.y);
+                if (wm) {
+                    *reinterpret_cast<float4*>(st + OFF_M + el * 4) = make_float4(mm[0], mm[1], mm[2], mm[3]);
+                    *reinterpret_cast<float4*>(st + OFF_M + el * 4 + 16) = make_float4(mm[4], mm[5], mm[6], mm[7]);
+                }
+                if constexpr (Op::kHasV) {
+                    *reinterpret_cast<float4*>(st + OFF_V + el * 4) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+                    *reinterpret_cast<float4*>(st + OFF_V + el * 4 + 16) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+                }
+            }
+            fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the bulk copies
+            __syncwarp();
+            if (lane == 0) {
+                const int64_t w0 = int64_t(warp) * 32 * kUnitEl;            // warp slice start in the tile
+                const int64_t nw = nvec - w0 < 32 * kUnitEl ? (nvec - w0 > 0 ? nvec - w0 : 0) : 32 * kUnitEl;
+                if (nw > 0) {
+                    const int64_t g0 = base + w0;
+                    bulk_s2g(static_cast<uint16_t*>(T.value) + g0, st + w0 * 2, uint32_t(nw * 2));
+                    bulk_s2g(static_cast<unsigned char*>(T.resid) + g0 * RB, st + OFF_R + w0 * RB, uint32_t(nw * RB));
+                    if (wm) bulk_s2g(T.m + g0, st + OFF_M + w0 * 4, uint32_t(nw * 4));
+                    if constexpr (Op::kHasV) bulk_s2g(T.v + g0, st + OFF_V + w0 * 4, uint32_t(nw * 4));
+                    bulk_commit();
+                    bulk_wait_read0();      // the stage's smem has been read: it may be refilled
+                }
+                mbar_arrive(&empty[s]);
+            }
+            if (!full_unit && nvec < nvalid && el <= nvec && nvec < el + kUnitEl)
+                process_tail<SF, G, Op, CLIP>(T, base + nvec, base + nvalid, c, coef);
+        }
+#else
 #ifndef MPO_RELEASE_EARLY
         // release after the arithmetic has consumed the registers (the proxy fence then waits on
         // nothing still pending from this stage)
@@ -993,11 +1048,15 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
         } else if (nvec < nvalid && el <= nvec && nvec < el + kUnitEl) {
             process_tail<SF, G, Op, CLIP>(T, base + nvec, base + nvalid, c, coef);
         }
+#endif
         if (++s == stages) {
             s = 0;
             ph ^= 1u;
         }
     }
+#if defined(MPO_BULK_ST)
+    if (lane == 0) bulk_wait0();   // every bulk store of this warp complete before the CTA exits
+#endif
 }
 
 #ifdef MPO_ABI_TU

@@ -53,6 +53,13 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         self._hooks = []
         self._tables = {}
         self._norm_ws = None
+        # hook mode: the ctypes table row and group of each parameter, kept OUT of self.state so
+        # state_dict() stays plain tensors and ints (picklable)
+        self._rows = {}
+        # skip_nonfinite: the step counts a skipped update must not advance are rolled back once its
+        # found-inf flag has reached the host (deferred, no synchronisation in step())
+        self._skip_check = None
+        self._hook_S = None
         idx = 0
         for group in self.param_groups:
             for p in group["params"]:
@@ -94,6 +101,93 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                                                scheme=self.scheme))
         return out
 
+    # -- checkpoint / resume ---------------------------------------------------------------
+    def state_dict(self):
+        """torch-style state dict: per parameter its residual (int16 / int8, the paper's extra bits,
+        P:82 "Extra bits are stored by the optimizer"), fp32 m / v, the int step count and the
+        stochastic-rounding stream index; plus the param groups and an "mpo" entry (storage scheme,
+        seed, gradient surgery).  The 16-bit values themselves are the parameters (model.state_dict()).
+        Tensors are referenced, not copied (torch.save serialises them)."""
+        self._resolve_skips()
+        sd = super().state_dict()
+        sd["mpo"] = {"format": 1, "kind": "adam" if self._kind == MPO_ADAM else "sgd", "scheme": self.scheme,
+                     "seed": self.seed, "clip_value": self.clip_value, "skip_nonfinite": self.skip_nonfinite,
+                     "max_grad_norm": getattr(self, "max_grad_norm", 0.0)}
+        return sd
+
+    def load_state_dict(self, state_dict):
+        """Restore a state_dict() of the same parameter layout.  Unlike torch's base class (which
+        casts floating state to the parameter's dtype), residual / m / v keep their own dtypes and
+        are copied INTO the existing device buffers (shape and dtype checked), so the cached
+        multi-tensor tables and hook rows stay valid; they are rebuilt anyway."""
+        meta = state_dict.get("mpo")
+        if meta is None:
+            raise MpoError(1, "not a residual-optimizer state dict (no 'mpo' entry)")
+        kind = "adam" if self._kind == MPO_ADAM else "sgd"
+        if meta.get("kind") != kind or meta.get("scheme") != self.scheme:
+            raise MpoError(3, f"state dict of a {meta.get('kind')}/{meta.get('scheme')} optimizer, this one is "
+                              f"{kind}/{self.scheme}")
+        saved = state_dict["param_groups"]
+        if len(saved) != len(self.param_groups) or any(len(a["params"]) != len(b["params"])
+                                                       for a, b in zip(saved, self.param_groups)):
+            raise MpoError(1, "state dict has a different parameter group layout")
+        self._resolve_skips()
+        id_map = {old: p for a, b in zip(saved, self.param_groups) for old, p in zip(a["params"], b["params"])}
+        with torch.no_grad():
+            for k, st in state_dict["state"].items():
+                p = id_map[k]
+                cur = self.state[p]
+                for key in ("resid", "m", "v"):
+                    src, dst = st.get(key), cur.get(key)
+                    if (src is None) != (dst is None):
+                        raise MpoError(1, f"parameter {k}: '{key}' present in only one of state dict / optimizer")
+                    if src is None:
+                        continue
+                    if src.dtype != dst.dtype or tuple(src.shape) != tuple(dst.shape):
+                        raise MpoError(3, f"parameter {k}: '{key}' is {src.dtype}{tuple(src.shape)}, "
+                                          f"expected {dst.dtype}{tuple(dst.shape)}")
+                    dst.copy_(src)
+                cur["step"] = int(st["step"])
+                cur["index"] = int(st["index"])
+        for g, a in zip(self.param_groups, saved):
+            for key, val in a.items():
+                if key != "params":
+                    g[key] = val
+        self.seed = int(meta["seed"])
+        self.clip_value = float(meta["clip_value"])
+        self.skip_nonfinite = bool(meta["skip_nonfinite"])
+        if hasattr(self, "max_grad_norm"):
+            self.max_grad_norm = float(meta.get("max_grad_norm", 0.0))
+        self._tables.clear()
+        if self._hooks:
+            self._build_rows()
+            self._hp_c = {}
+
+    # -- loss scaling: step counts of skipped updates (deferred) -----------------------------
+    def _queue_skip_check(self, params, dev_S):
+        """Queue a device->host copy of the step's S (non-blocking) to learn later whether the
+        update was skipped; params' step counts are then rolled back (torch's GradScaler does not
+        step the optimizer, so its bias corrections never count a skipped step)."""
+        host = torch.empty(dev_S.numel(), dtype=torch.float64, pin_memory=True)
+        host.copy_(dev_S, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._skip_check = (params, host, ev)
+
+    def _resolve_skips(self):
+        chk, self._skip_check = self._skip_check, None
+        if chk is None:
+            return
+        params, host, ev = chk
+        ev.synchronize()
+        import math
+        bad = [not math.isfinite(x) for x in host.tolist()]
+        if len(bad) == 1:
+            bad = bad * len(params)
+        for p, b in zip(params, bad):
+            if b:
+                self.state[p]["step"] -= 1
+
     # -- multi-tensor step -----------------------------------------------------------------
     def _table_for(self, params):
         key = tuple(id(p) for p in params)
@@ -115,12 +209,14 @@ class _ResidualOptimizer(torch.optim.Optimizer):
     def step(self, closure=None):
         if closure is not None:
             raise MpoError(1, "closure optimizers are not supported (the step is fused, P:194)")
+        self._resolve_skips()
         params = [p for g in self.param_groups for p in g["params"] if p.grad is not None]
         if not params:
             return None
         by_dtype = {}
         for p in params:
             by_dtype.setdefault((p.dtype, p.grad.dtype), []).append(p)
+        launches = []
         for plist in by_dtype.values():
             tab = self._table_for(plist)
             # hyper-parameter groups: one per (param group, step)
@@ -133,9 +229,24 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                 raise MpoError(1, "more than 16 distinct (group, step) pairs in one step")
             for i, h in enumerate(hp_index):
                 tab.arr[i].hp = h
-            hps = [self._hp(self.param_groups[gi], stp) for (gi, stp) in keys]
+            launches.append((tab, [self._hp(self.param_groups[gi], stp) for (gi, stp) in keys]))
+        need_norm = self._needs_norm()
+        if need_norm and len(launches) > 1:
+            # one S over every table of the step (global-norm clipping is over ALL gradients, R9;
+            # the found-inf skip is all-or-nothing): shared pre-pass, then norm_ready launches
+            ws = self._ws(params[0].device)
+            for i, (tab, hps) in enumerate(launches):
+                api.mpo_grad_sumsq(tab, [h.grad_scale for h in hps], ws, accumulate=i > 0, exact=self.exact)
+                for h in hps:
+                    h.norm_ready = True
+        for tab, hps in launches:
             self._launch(tab, hps)
+        if self.skip_nonfinite:
+            self._queue_skip_check(params, self._ws(params[0].device)[:1])
         return None
+
+    def _needs_norm(self):
+        return self.skip_nonfinite or getattr(self, "max_grad_norm", 0.0) > 0
 
     # -- hook mode ---------------------------------------------------------------------------
     def install_backward_hooks(self, batch_below: int = 1 << 16, flush_elems: int = 1 << 22):
@@ -155,6 +266,17 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         self._pending_elems = 0
         self._flush_queued = False
         self._hp_c, self._codes = {}, {}
+        self._build_rows()
+        if self.skip_nonfinite:
+            n = sum(len(g["params"]) for g in self.param_groups)
+            self._hook_S = torch.zeros(n, dtype=torch.float64, device=self.param_groups[0]["params"][0].device)
+        for group in self.param_groups:
+            for p in group["params"]:
+                self._hooks.append(p.register_post_accumulate_grad_hook(_weak_hook(self)))
+        return list(self._hooks)
+
+    def _build_rows(self):
+        self._rows = {}
         for gi, group in enumerate(self.param_groups):
             for p in group["params"]:
                 st = self.state[p]
@@ -165,10 +287,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                 row.v = st["v"].data_ptr() if st.get("v") is not None else None
                 row.n = p.numel()
                 row.sr_stream = st["index"]
-                st["row"] = row
-                st["group"] = gi
-                self._hooks.append(p.register_post_accumulate_grad_hook(_weak_hook(self)))
-        return list(self._hooks)
+                self._rows[p] = (row, gi)
 
     def remove_backward_hooks(self):
         for h in self._hooks:
@@ -176,6 +295,8 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         self._hooks = []
 
     def _hook(self, p: torch.Tensor):
+        if self._skip_check is not None:
+            self._resolve_skips()          # the previous backward's skipped parameters
         st = self.state[p]
         g = p.grad
         st["step"] += 1
@@ -189,27 +310,39 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             if self._pending_elems >= self._flush_elems:
                 self._flush_pending(final=False)
             return
-        row = st["row"]
+        row, group = self._rows[p]
         row.grad = g.data_ptr()
         # host cost per hook matters when backward is short: the ctypes hyper-parameters are built
         # once per (group, step) and shared by the group's parameters; format codes are cached
-        key = (st["group"], st["step"])
+        key = (group, st["step"])
         hp = self._hp_c.get(key)
         if hp is None:
             if len(self._hp_c) > 64:
                 self._hp_c.clear()
-            hp = self._hp_c[key] = self._hp(self.param_groups[st["group"]], st["step"]).c()
+            hp = self._hp_c[key] = self._hp(self.param_groups[group], st["step"]).c()
         codes = self._codes.get((p.dtype, g.dtype))
         if codes is None:
             codes = self._codes[(p.dtype, g.dtype)] = (api.format_code(p.dtype, self.scheme), api.dtype_code(g.dtype))
         api.mpo_fused_backward_hook_step(self._kind, codes[0], codes[1], row, hp, exact=self.exact,
                                          norm_ws=self._ws(p.device) if self.skip_nonfinite else None)
+        if self.skip_nonfinite:
+            # this parameter's S (norm_ws[0] of its call) for the step-count rollback of a skip
+            self._hook_S[st["index"]].copy_(self._norm_ws[0])
+            if not self._flush_queued:
+                torch.autograd.Variable._execution_engine.queue_callback(self._flush_pending)
+                self._flush_queued = True
         p.grad = None   # freed now; stream order makes the block's reuse safe
 
     def _flush_pending(self, final: bool = True):
         """One multi-tensor launch over the batched small parameters of this backward."""
         if final:
             self._flush_queued = False
+            if self._hook_S is not None:
+                # end of backward: learn (later, without a sync) which parameters were skipped
+                params = [p for g in self.param_groups for p in g["params"]]
+                order = sorted(range(len(params)), key=lambda i: self.state[params[i]]["index"])
+                self._queue_skip_check([params[i] for i in order], self._hook_S)
+                self._hook_S.zero_()
         if not self._pending:
             return
         pending, self._pending, self._pending_elems = self._pending, [], 0
@@ -221,8 +354,8 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                 ps = [p for p, _ in items]
                 sts = [self.state[p] for p in ps]
                 keys, hp_index = {}, []
-                for s_ in sts:
-                    hp_index.append(keys.setdefault((s_["group"], s_["step"]), len(keys)))
+                for p_, s_ in zip(ps, sts):
+                    hp_index.append(keys.setdefault((self._rows[p_][1], s_["step"]), len(keys)))
                 tab = api.TensorTable([p.data for p in ps], [s_["resid"] for s_ in sts], [g for _, g in items],
                                       [s_.get("m") for s_ in sts], [s_.get("v") for s_ in sts], hp_index,
                                       scheme=self.scheme, sr_streams=[s_["index"] for s_ in sts])
@@ -242,6 +375,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         """skip_nonfinite: whether a non-finite scaled gradient was seen -- by the last step() (which
         then updated nothing), or by any hook of the backward passes since the last reset (hook
         mode skips only the offending parameters).  Synchronises with the device."""
+        self._resolve_skips()
         if self._norm_ws is None:
             return False
         ws = self._norm_ws

@@ -29,15 +29,17 @@ ALIGN = 8   # elements: 16 B for 16-bit data, so every parameter view is 16-byte
 class ShardLayout:
     sizes: List[int]
     world: int
+    align: int = ALIGN      # 16 for the int8-residual (X8) formats: every piece 16-B aligned
 
     def __post_init__(self):
         if self.world < 1:
             raise ValueError("world must be >= 1")
+        a = self.align
         offs, o = [], 0
         for n in self.sizes:
             offs.append(o)
-            o += (n + ALIGN - 1) // ALIGN * ALIGN
-        q = ALIGN * self.world
+            o += (n + a - 1) // a * a
+        q = a * self.world
         self.offsets = offs
         self.used = o
         self.total = (o + q - 1) // q * q
@@ -48,6 +50,22 @@ class ShardLayout:
 
     def views(self, flat: torch.Tensor, shapes: Sequence[torch.Size]):
         return [flat[o:o + n].view(s) for o, n, s in zip(self.offsets, self.sizes, shapes)]
+
+    def segments(self, rank: int, hp_index: Sequence[int]):
+        """mpo_segment table of ``rank``'s shard for per-parameter hyper-parameter groups: runs of
+        consecutive parameter pieces with the same group become one segment (padding goes with the
+        preceding piece), starting at 0; segment k draws stochastic-rounding numbers from stream
+        rank + world*k (one segment: stream = rank, as mpo_sharded_step)."""
+        segs = []
+        for i, _, start, _ in self.owner_slices(rank):
+            h = int(hp_index[i])
+            if not segs:
+                segs.append([0, h])
+            elif segs[-1][1] != h:
+                segs.append([start, h])
+        if not segs:
+            segs = [[0, 0]]
+        return [(a, h, rank + self.world * k) for k, (a, h) in enumerate(segs)]
 
     def owner_slices(self, rank: int):
         """(param index, start within param, start within shard, length) of the parameter pieces
@@ -112,7 +130,7 @@ class ShardedResidualOptimizer:
 
     def __init__(self, params, kind: str = "adam", fmt: Optional[torch.dtype] = None, group=None,
                  hp=None, exact: bool = False, comm_ptr: Optional[int] = None, scheme: str = "rne",
-                 seed: int = 0, transport: str = "nccl"):
+                 seed: int = 0, transport: str = "nccl", hp_index: Optional[Sequence[int]] = None):
         import torch.distributed as dist
         if transport not in ("nccl", "p2p"):
             raise MpoError(1, "transport must be 'nccl' or 'p2p'")
@@ -129,7 +147,8 @@ class ShardedResidualOptimizer:
         vdt = fmt if self.params[0].dtype == torch.float32 else self.params[0].dtype
         if vdt not in (torch.float16, torch.bfloat16):
             raise MpoError(3, "fmt must be torch.float16 or torch.bfloat16")
-        self.layout = L = ShardLayout([p.numel() for p in self.params], self.world)
+        self.layout = L = ShardLayout([p.numel() for p in self.params], self.world,
+                                      align=2 * ALIGN if scheme == "x8" else ALIGN)
         lo, hi = L.shard_range(self.rank)
         # fp32 source of the flat buffer (transient), split once on the device
         src = torch.zeros(L.total, dtype=torch.float32, device=dev)
@@ -169,9 +188,21 @@ class ShardedResidualOptimizer:
             p.grad = gg
         self.hp = hp if hp is not None else (api.AdamParams(lr=1e-3) if self.kind == MPO_ADAM
                                              else api.SgdParams(lr=1e-2))
+        # per-parameter hyper-parameter groups (e.g. no weight decay on 1-D tensors): hp is then a
+        # list and hp_index names each parameter's group; the shard's pieces form the segment table
+        # of mpo_sharded_step_grouped
+        self.hps = list(self.hp) if isinstance(self.hp, (list, tuple)) else [self.hp]
+        if hp_index is not None and len(hp_index) != len(self.params):
+            raise MpoError(1, "hp_index needs one group index per parameter")
+        if any(not 0 <= int(h) < len(self.hps) for h in (hp_index or [])):
+            raise MpoError(1, "hp_index out of range")
+        self.segments = L.segments(self.rank, hp_index) if hp_index is not None else None
+        if len(self.hps) > 1 and self.segments is None:
+            raise MpoError(1, "several hyper-parameter groups need hp_index")
         self.step_count = 0
-        if transport == "p2p" and getattr(self.hp, "max_grad_norm", 0.0) > 0:
-            raise MpoError(1, "the P2P fused step has no norm pre-pass: use transport='nccl' for max_grad_norm")
+        if transport == "p2p" and (getattr(self.hps[0], "max_grad_norm", 0.0) > 0 or len(self.hps) > 1):
+            raise MpoError(1, "the P2P fused step has no norm pre-pass and one hyper-parameter group: use "
+                              "transport='nccl' for max_grad_norm / hp groups")
         self.comm = None if transport == "p2p" else (comm_ptr if comm_ptr is not None else nccl_comm_ptr(group))
 
     def zero_grad(self):
@@ -180,12 +211,13 @@ class ShardedResidualOptimizer:
     @torch.no_grad()
     def step(self):
         self.step_count += 1
-        hp = self.hp
-        if self.kind == MPO_ADAM:
-            hp.step = self.step_count
-        else:
-            hp.first_step = self.step_count == 1
-        hp.seed = api.step_seed(self.seed, self.step_count)
+        for hp in self.hps:
+            if self.kind == MPO_ADAM:
+                hp.step = self.step_count
+            else:
+                hp.first_step = self.step_count == 1
+            hp.seed = api.step_seed(self.seed, self.step_count)
+        hp = self.hps[0]
         if self.transport == "p2p":
             # every rank's gradients are complete before any rank reads them, and every rank's
             # new values are in place before any rank reads its replica again
@@ -195,9 +227,17 @@ class ShardedResidualOptimizer:
                                      scheme=self.scheme)
             self._hv.barrier(channel=0)
             return
+        need_ws = getattr(hp, "max_grad_norm", 0.0) > 0 or getattr(hp, "skip_nonfinite", False)
         api.mpo_sharded_step(self.kind, self.comm, self.rank, self.world, self.value, self.grad, self.resid, self.m,
-                             self.v, hp, norm_ws=self.norm_ws if getattr(hp, "max_grad_norm", 0.0) > 0 else None,
-                             exact=self.exact, scheme=self.scheme)
+                             self.v, self.hps if self.segments is not None else hp,
+                             norm_ws=self.norm_ws if need_ws else None, exact=self.exact, scheme=self.scheme,
+                             segments=self.segments)
+
+    def check_comm(self):
+        """Raises MpoError(MPO_ENCCL) if the NCCL communicator failed asynchronously (never blocks;
+        the sharded step also checks before issuing its collectives)."""
+        if self.comm is not None:
+            api.mpo_comm_check(self.comm, exact=self.exact)
 
     def persistent_bytes(self) -> int:
         b = self.value.numel() * 2 + self.grad.numel() * 2 + self.resid.numel() * self.resid.element_size()
@@ -357,12 +397,15 @@ class BucketedShardedOptimizer:
         ev.record(torch.cuda.current_stream())
         self.side.wait_event(ev)
         with torch.cuda.stream(self.side):
+            # each bucket draws its stochastic-rounding numbers from its own stream (rank + world*b):
+            # one shared stream would repeat the same draws in every bucket of a step
             api.mpo_sharded_step(self.kind, self.comm, self.rank, self.world, self.value[o:o + length],
                                  self.grad[o:o + length], self.resid[po:po + k],
                                  None if self.m is None else self.m[po:po + k],
-                                 None if self.v is None else self.v[po:po + k], hp,
+                                 None if self.v is None else self.v[po:po + k], [hp],
                                  norm_ws=self.norm_ws if getattr(hp, "skip_nonfinite", False) else None,
-                                 exact=self.exact, scheme=self.scheme, stream=self.side)
+                                 exact=self.exact, scheme=self.scheme, stream=self.side,
+                                 segments=[(0, 0, self.rank + self.world * b)])
             self.grad[o:o + length].zero_()       # ready for the next backward's accumulation
         if all(x == 0 for x in self._pending):  # backward done: re-arm the bucket counters
             self._pending = [len(idx) for _, _, idx in L.buckets]

@@ -166,3 +166,46 @@ def test_cpu_tensors_are_rejected():
     with pytest.raises(MpoError, match="CUDA"):
         mpo_split(torch.zeros(8), torch.bfloat16, value=torch.zeros(8, dtype=torch.bfloat16),
                   resid=torch.zeros(8, dtype=torch.int16))
+
+
+def test_grouped_sharded_and_sumsq_validation(libs):
+    """mpo_sharded_step_grouped's segment table, mpo_grad_sumsq and mpo_comm_check validate their
+    arguments before touching the device or the communicator (no GPU needed)."""
+    _lib, L, _ = libs
+    hp = (_lib.AdamHP * 2)(_lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1, 0),
+                           _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.1, 1.0, 0.0, 1, 0, 1, 0))
+
+    def grouped(segs, nhp=2, n=64, world=2, vdt=_lib.MPO_BF16):
+        arr = (_lib.Segment * len(segs))(*[_lib.Segment(*s) for s in segs])
+        return _status(L, L.mpo_sharded_step_grouped(_lib.MPO_ADAM, 1, 0, world, vdt, 16, 32, 48, 64, 80, n, arr,
+                                                      len(segs), C.cast(hp, C.c_void_p), nhp, None, None))
+    rc, msg = grouped([(8, 0, 0)])
+    assert rc == _lib.MPO_EINVAL and "segment 0" in msg                  # must start at 0
+    rc, msg = grouped([(0, 0, 0), (4, 1, 1)])
+    assert rc == _lib.MPO_EINVAL and "multiple of 8" in msg              # 16-B alignment of the pieces
+    rc, msg = grouped([(0, 0, 0), (8, 1, 1)], vdt=49)                    # MPO_BF16_X8: int8 residuals
+    assert rc == _lib.MPO_EINVAL and "multiple of 16" in msg
+    rc, msg = grouped([(0, 0, 0), (32, 1, 1)])
+    assert rc == _lib.MPO_EINVAL and "segment 1" in msg                  # beyond the 32-element shard
+    rc, msg = grouped([(0, 2, 0)])
+    assert rc == _lib.MPO_EINVAL and "group index" in msg
+    rc, msg = grouped([(0, 0, 0)], nhp=17)
+    assert rc == _lib.MPO_EINVAL
+    # mpo_grad_sumsq
+    tab = (_lib.Tensor * 1)(_lib.Tensor(0, 0, 48, 0, 0, 8, 0, 0))
+    gs = (C.c_double * 1)(1.0)
+    assert L.mpo_grad_sumsq(9, tab, 1, gs, 1, 16, 0, None) == _lib.MPO_EDTYPE
+    assert L.mpo_grad_sumsq(_lib.MPO_BF16, tab, 1, gs, 1, None, 0, None) == _lib.MPO_EINVAL
+    tab[0].grad = 50
+    rc, msg = _status(L, L.mpo_grad_sumsq(_lib.MPO_BF16, tab, 1, gs, 1, 16, 0, None))
+    assert rc == _lib.MPO_EALIGN and "tensor 0" in msg
+    nan = (C.c_double * 1)(float("nan"))
+    assert L.mpo_grad_sumsq(_lib.MPO_BF16, tab, 1, nan, 1, 16, 0, None) == _lib.MPO_EINVAL
+    # communicator check: NULL refused (a live communicator is exercised by the GPU tests)
+    assert L.mpo_comm_check(0) == _lib.MPO_EINVAL
+    # norm_ready is for multi-tensor calls only
+    one = _lib.Tensor(16, 32, 48, 64, 80, 8, 0, 0)
+    ready = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1, 0, 0.0, 0, 1)
+    rc, msg = _status(L, L.mpo_fused_backward_hook_step(_lib.MPO_ADAM, _lib.MPO_BF16, _lib.MPO_BF16, C.byref(one),
+                                                        C.byref(ready), None, None))
+    assert rc == _lib.MPO_EINVAL and "norm_ready" in msg

@@ -211,6 +211,43 @@ def test_sharded_world1_equals_unsharded(mpo, nccl1, kind, clip):
         assert torch.equal(a.data.view(torch.int16), b.data.view(torch.int16))
 
 
+@pytest.mark.parametrize("clip", [False, True])
+def test_sharded_grouped_world1_equals_param_groups(mpo, nccl1, clip):
+    """Per-parameter hyper-parameter groups in the sharded step (mpo_sharded_step_grouped: the
+    shard's pieces as a segment table; P:19 unchanged hyper-parameters, e.g. no decay on 1-D
+    tensors) == ResidualAdamW with the same two param groups, bitwise at world 1; the
+    communicator reports healthy (mpo_comm_check)."""
+    torch.manual_seed(4)
+    shapes = [(33, 17), (4096,), (5,), (128, 64), (1000,)]
+    src = [torch.randn(s, device="cuda") * 0.02 for s in shapes]
+    pa = [nn.Parameter(t.clone()) for t in src]
+    pb = [nn.Parameter(t.clone()) for t in src]
+    decay = [len(s) == 2 for s in shapes]
+    mg = 0.05 if clip else None
+    ref = mpo.ResidualAdamW([{"params": [p for p, d in zip(pa, decay) if d], "weight_decay": 0.1},
+                             {"params": [p for p, d in zip(pa, decay) if not d], "weight_decay": 0.0}],
+                            lr=1e-3, fmt=torch.bfloat16, max_grad_norm=mg)
+    hps = [mpo.AdamParams(lr=1e-3, weight_decay=0.1, max_grad_norm=mg or 0.0),
+           mpo.AdamParams(lr=1e-3, weight_decay=0.0, max_grad_norm=mg or 0.0)]
+    sh = mpo.ShardedResidualOptimizer(pb, kind="adam", fmt=torch.bfloat16, hp=hps,
+                                      hp_index=[0 if d else 1 for d in decay])
+    assert len(sh.segments) > 1
+    for t in range(3):
+        grads = [torch.randn(s, device="cuda").to(torch.bfloat16) * 1e-2 for s in shapes]
+        if clip:   # exact-sum construction (P8)
+            grads = [(torch.sign(g) * 2.0 ** -7 + (g == 0) * 2.0 ** -7).to(torch.bfloat16) for g in grads]
+        for p, g in zip(pa, grads):
+            p.grad = g.clone()
+        sh.zero_grad()
+        for p, g in zip(pb, grads):
+            p.grad.copy_(g)
+        ref.step()
+        sh.step()
+        sh.check_comm()
+    for a, b in zip(pa, pb):
+        assert torch.equal(a.data.view(torch.int16), b.data.view(torch.int16))
+
+
 @pytest.mark.parametrize("kind", ["adam", "sgd"])
 def test_sharded_p2p_transport_world1_equals_nccl(mpo, nccl1, kind):
     """transport='p2p' (torch symmetric memory + mpo_p2p_sharded_step between symmetric-memory
@@ -464,6 +501,7 @@ def test_p2p_fused_sharded_step_emulated_peers(mpo, orc, world, kind, fmt, schem
     w = synth.weights(n, 0.02, 7)
     for k in range(world):                       # special values in every shard (slow unit paths)
         w[k * S:k * S + 36] = synth.edge_f32() * np.float32(1e-3)
+        w[k * S + 36:k * S + 72] = synth.edge_f32()      # unscaled: overflow, Inf, NaN, max-finite
     h, r = orc.split_s(scheme, fmt, w, seed=3, stream=0)
     gs = [synth.grads(n, 1e-2, fmt, 0xC0FFEE, k) for k in range(world)]
     if world > 1:                                # a non-finite gradient on one rank only

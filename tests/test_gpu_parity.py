@@ -26,6 +26,32 @@ pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "split_examples.txt")
 
 
+_FMA_STATS = []
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _fma_stats_report():
+    """Writes the FMA build's literal-bar counts (see _check_fma_tolerance) to
+    $MPO_STATS_DIR/fma_strict_bar.json when set, and bounds their total: the literal bar fails
+    only where R12's cancellation bound applies (asserted per element in _check_fma_tolerance): measured
+    on B200 (round 2) 3.6e-4 of the elements miss the literal 1e-6 relative bar and 3e-8 the 1-ulp16
+    bar (max 14 ulp16, at |w_new| << |u|); the bounds below keep a margin of ~3x."""
+    yield
+    if not _FMA_STATS:
+        return
+    import json
+    tot = {k: sum(s[k] for s in _FMA_STATS) for k in ("finite", "outside_strict_bar", "outside_1e-6_rel",
+                                                       "outside_1_ulp16", "bitwise_differing_values")}
+    tot["max_ulp16"] = max(s["max_ulp16"] for s in _FMA_STATS)
+    out = os.environ.get("MPO_STATS_DIR")
+    if out:
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, "fma_strict_bar.json"), "w") as fh:
+            json.dump({"total": tot, "per_check": _FMA_STATS}, fh, indent=1)
+    assert tot["outside_1e-6_rel"] <= 1e-3 * tot["finite"], tot
+    assert tot["outside_1_ulp16"] <= 1e-7 * tot["finite"], tot
+
+
 @pytest.fixture(scope="module")
 def mpo():
     if not torch.cuda.is_available():
@@ -182,6 +208,16 @@ def _check_fma_tolerance(fmt, pre, gpu, orc_, g32, uscale=None):
     assert ok.all(), (int((~ok).sum()), np.abs(wo[~ok])[:8], err[~ok][:8], bound[~ok][:8])
     well = fin & (err <= 1e-6 * np.abs(wo)) & (err <= 1e-6 * (np.abs(w0) + np.abs(wo)))
     assert ulp16_dist(hg[well], ho[well], fmt).max(initial=0) <= 1
+    # BASELINE.json's literal bar, "<= 1 ulp of the 16-bit value AND <= 1e-6 relative on the fp32
+    # weight", counted over ALL finite elements (reported: DESIGN.md R12 quotes the counts; every
+    # element outside it is a cancellation case that met the R12 bound asserted above)
+    d16 = ulp16_dist(hg[fin], ho[fin], fmt)
+    strict = (d16 <= 1) & (err[fin] <= 1e-6 * np.abs(wo[fin]))
+    _FMA_STATS.append({"test": os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], "fmt": fmt,
+                       "finite": int(fin.sum()), "outside_strict_bar": int((~strict).sum()),
+                       "outside_1e-6_rel": int((err[fin] > 1e-6 * np.abs(wo[fin])).sum()),
+                       "outside_1_ulp16": int((d16 > 1).sum()), "max_ulp16": int(d16.max(initial=0)),
+                       "bitwise_differing_values": int((hg[fin] != ho[fin]).sum())})
     g = np.abs(np.asarray(g32, dtype=np.float64))
     if mg is not None:
         f = np.isfinite(mo)
@@ -223,6 +259,8 @@ def test_multi_tensor_ragged_bit_exact(mpo, orc, fmt, gfmt, kind):
         w = synth.weights(n, 0.05, 0xC0FFEE + i)
         if n > 40:
             w[:36] = synth.edge_f32() * np.float32(1e-3)
+        if n > 80:
+            w[36:72] = synth.edge_f32()      # unscaled: overflow, Inf, NaN, max-finite
         h, r = orc.split(fmt, w)
         hs.append(h); rs.append(r)
         gs.append(synth.grads(n, 1e-2, gf, 0xC0FFEE, i))

@@ -167,13 +167,22 @@ def test_p7_first_adam_step_moves_by_lr(orc, fmt):
 
 
 # ---------------------------------------------------------------------------------- P10 --
-@pytest.mark.parametrize("kind", ["adamw", "adam_l2", "sgd_m", "sgd_nesterov", "sgd_damp_wd"])
+@pytest.mark.parametrize("kind", ["adamw", "adam_l2", "sgd_m", "sgd_nesterov", "sgd_damp_wd",
+                                  "adam_b1_0", "adam_b1_03", "adamw_b1_05"])
 def test_p10_matches_torch_optim(orc, kind):
     import torch
     n, T = 8192, 30
     w0 = synth.weights(n, 0.02, 0xC0FFEE)
     p = torch.nn.Parameter(torch.from_numpy(w0.copy()))
-    if kind == "adamw":
+    # beta1 <= 0.5 (lerp weight 1-beta1 >= 0.5) drives the oracle's upper lerp branch (reading R6,
+    # torch's lerp switches formula at weight 0.5): pinned here against torch.optim too
+    upper = {"adam_b1_0": (0.0, 0.999, False), "adam_b1_03": (0.3, 0.99, False), "adamw_b1_05": (0.5, 0.95, True)}
+    if kind in upper:
+        b1, b2, aw = upper[kind]
+        hp = dict(lr=1e-3, beta1=b1, beta2=b2, eps=1e-8, weight_decay=0.05, adamw=aw)
+        cls = torch.optim.AdamW if aw else torch.optim.Adam
+        opt = cls([p], lr=1e-3, betas=(b1, b2), eps=1e-8, weight_decay=0.05, foreach=False, fused=False)
+    elif kind == "adamw":
         hp = dict(lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, adamw=True)
         opt = torch.optim.AdamW([p], lr=1e-3, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1,
                                 foreach=False, fused=False)
@@ -242,18 +251,90 @@ def test_clip_coef_closed_forms(orc):
     assert orc.clip_coef(float("inf"), 1.0) == 0.0
 
 
-def test_clip_applied_in_step(orc):
-    n = 1024
-    w0 = synth.weights(n)
-    g = synth.grads(n, 1e-2, "fp32", 1, 1)
-    c = orc.clip_coef(orc.sumsq("fp32", g), 0.01)
-    assert c < 1.0
-    a = w0.copy(); b = w0.copy()
-    m1 = np.zeros(n, np.float32); v1 = np.zeros(n, np.float32)
-    m2 = np.zeros(n, np.float32); v2 = np.zeros(n, np.float32)
-    orc.adam_step_master("fp32", a, g, m1, v1, lr=1e-3, clip_coef=c)
-    orc.adam_step_master("fp32", b, (g * f32(c)).astype(np.float32), m2, v2, lr=1e-3)
-    assert np.array_equal(a, b) and np.array_equal(m1, m2)
+@pytest.mark.parametrize("adamw", [False, True])
+def test_clipped_step_matches_torch_clip_grad_norm_and_adam(orc, adamw):
+    """Global-norm clipping (R9) pinned against library routines: loss-scaled 16-bit
+    gradients of several tensors are unscaled (grad_scale), clipped with
+    torch.nn.utils.clip_grad_norm_ over ALL tensors and stepped with torch.optim.Adam/AdamW on an
+    fp32 master; the oracle computes S = sum (g*gs)^2 over the tensors, coef = clip_coef(S), and
+    steps each tensor with it.  eps is of the order of the clipped gradients, so the trajectory
+    depends on coef (Adam alone is nearly scale-invariant); some steps are unclipped (norm below
+    max_norm).  A coefficient computed on unscaled grads, per tensor instead of globally, applied
+    before the scale or skipped would leave the tolerance."""
+    import torch
+    sizes, T, gs = [1000, 37, 2048], 12, 1.0 / 1024.0
+    lr, b1, b2, eps, wd, max_norm = 1e-3, 0.9, 0.95, 1e-3, 0.1, 0.05
+    ws = [synth.weights(n, 0.02, 0xB0B + i) for i, n in enumerate(sizes)]
+    ps = [torch.nn.Parameter(torch.from_numpy(w.copy())) for w in ws]
+    cls = torch.optim.AdamW if adamw else torch.optim.Adam
+    opt = cls(ps, lr=lr, betas=(b1, b2), eps=eps, weight_decay=wd, foreach=False, fused=False)
+    ms = [np.zeros(n, np.float32) for n in sizes]
+    vs = [np.zeros(n, np.float32) for n in sizes]
+    wmax = [np.abs(w).astype(np.float64) for w in ws]
+    clipped = 0
+    for t in range(1, T + 1):
+        sig = (2e-3 if t % 3 else 2e-4) * 1024.0      # every third step: norm < max_norm, coef = 1
+        g16 = [synth.grads(n, sig, "fp16", 2023, 100 * t + i) for i, n in enumerate(sizes)]
+        for p, g in zip(ps, g16):   # torch: unscale (fp32), then clip over all tensors, then step
+            p.grad = torch.from_numpy(orc.widen("fp16", g) * np.float32(gs))
+        torch.nn.utils.clip_grad_norm_(ps, max_norm, foreach=False)
+        opt.step()
+        S = sum(orc.sumsq("fp16", g, grad_scale=gs) for g in g16)
+        coef = orc.clip_coef(S, max_norm)
+        clipped += coef < 1.0
+        for i in range(len(sizes)):
+            orc.adam_step_master("fp16", ws[i], g16[i], ms[i], vs[i], lr=lr, beta1=b1, beta2=b2, eps=eps,
+                                 weight_decay=wd, adamw=adamw, grad_scale=gs, step=t, clip_coef=coef)
+            wmax[i] = np.maximum(wmax[i], np.abs(ws[i]))
+    assert 0 < clipped < T
+    for i in range(len(sizes)):
+        ref = ps[i].detach().numpy().astype(np.float64)
+        err = np.abs(ws[i].astype(np.float64) - ref)
+        assert (err <= 2 * T * _ulp32(wmax[i])).all(), err.max()
+    # the same run with the coefficient left out is far outside that tolerance (the test bites)
+    w_noclip = ws[0].copy() * 0 + synth.weights(sizes[0], 0.02, 0xB0B)
+    m0 = np.zeros(sizes[0], np.float32); v0 = np.zeros(sizes[0], np.float32)
+    for t in range(1, T + 1):
+        sig = (2e-3 if t % 3 else 2e-4) * 1024.0
+        g = synth.grads(sizes[0], sig, "fp16", 2023, 100 * t)
+        orc.adam_step_master("fp16", w_noclip, g, m0, v0, lr=lr, beta1=b1, beta2=b2, eps=eps, weight_decay=wd,
+                             adamw=adamw, grad_scale=gs, step=t)
+    ref = ps[0].detach().numpy().astype(np.float64)
+    assert np.abs(w_noclip.astype(np.float64) - ref).max() > 100 * 2 * T * _ulp32(wmax[0]).max()
+
+
+def test_adam_lerp_closed_forms(orc):
+    """The first-moment update m <- lerp(m, g, 1-beta1) (R6) against its closed forms, both
+    branches: beta1 = 0 gives m_new = g EXACTLY (the upper formula g - (g-m)*0; the lower one,
+    m + 1*(g-m), would round g-m); beta1 = 0.5 on dyadic inputs is exact (m+g)/2; and for random
+    inputs and beta1 in {0.9, 0.64, 0.5, 0.3, 0.1} m_new lies within 2 binary32 ulps (of the
+    operands' scale) of the exact lerp computed in fp64.  Observed through Adam's m output on an fp32 master."""
+    n = 1 << 14
+    m0 = synth.normal_f32(n, 1e-2, 9, 1)
+    g = synth.normal_f32(n, 1e-2, 9, 2)
+    w = np.zeros(n, np.float32)
+    m = m0.copy(); v = np.zeros(n, np.float32)
+    orc.adam_step_master("fp32", w, g, m, v, lr=1e-3, beta1=0.0, step=2)
+    assert np.array_equal(m.view(np.uint32), g.view(np.uint32))
+    # the lower formula would not be exact here (the test distinguishes the branches)
+    low = (m0 + (g - m0)).astype(np.float32)
+    assert np.count_nonzero(low != g) > n // 4
+    md = (np.round(m0 * 2 ** 12) / 2 ** 12).astype(np.float32)
+    gd = (np.round(g * 2 ** 12) / 2 ** 12).astype(np.float32)
+    m = md.copy(); v = np.zeros(n, np.float32)
+    orc.adam_step_master("fp32", w.copy(), gd, m, v, lr=1e-3, beta1=0.5, step=2)
+    assert np.array_equal(m, ((md.astype(np.float64) + gd.astype(np.float64)) / 2).astype(np.float32))
+    for b1 in (0.9, 0.64, 0.5, 0.3, 0.1):
+        wgt = np.float64(np.float32(1.0 - b1))          # the float lerp weight both sides use (R7)
+        m = m0.copy(); v = np.zeros(n, np.float32)
+        orc.adam_step_master("fp32", w.copy(), g, m, v, lr=1e-3, beta1=b1, step=2)
+        exact = m0.astype(np.float64) + wgt * (g.astype(np.float64) - m0.astype(np.float64))
+        # three roundings (g - m, the product, the sum): within 2 ulps of the operands' scale
+        scale = np.maximum(np.abs(m0), np.abs(g))
+        assert (np.abs(m.astype(np.float64) - exact) <= 2 * _ulp32(scale)).all(), b1
+        # a branch with the weight's complement (the classic slip) is far outside
+        wrong = m0.astype(np.float64) + (1 - wgt) * (g.astype(np.float64) - m0.astype(np.float64))
+        assert np.median(np.abs(wrong - exact) / _ulp32(scale)) > 1000 or b1 == 0.5
 
 
 # ----------------------------------------------------------------------------------- P9 --

@@ -58,7 +58,37 @@ def _rank_grads(rank, n, fmt):
     return q
 
 
-def _worker(rank, world, port, kind, clip, out_dir):
+HP_INDEX = [0, 1, 1, 0, 1, 0]          # e.g. decay on matrices only, none on 1-D tensors
+GROUP_WD = (0.1, 0.0)
+
+
+def test_layout_segments():
+    """The segment table of mpo_sharded_step_grouped: it partitions each rank's shard from 0, every
+    start is a multiple of the alignment (16-B aligned pieces), every parameter piece lies inside
+    one segment of its own group, and the stochastic-rounding streams are distinct per rank and
+    segment (one segment: stream = rank, like mpo_sharded_step)."""
+    for align in (8, 16):
+        for world in (1, 2, 3, 8):
+            L = ShardLayout(SIZES, world, align=align)
+            assert all(o % align == 0 for o in L.offsets) and L.total % (align * world) == 0
+            streams = set()
+            for r in range(world):
+                segs = L.segments(r, HP_INDEX)
+                starts = [a for a, _, _ in segs]
+                assert starts[0] == 0 and all(a < b for a, b in zip(starts, starts[1:])) and starts[-1] < L.shard
+                assert all(a % align == 0 for a in starts)
+                ends = starts[1:] + [L.shard]
+                for i, _, b, n in L.owner_slices(r):
+                    k = max(j for j, a in enumerate(starts) if a <= b)
+                    assert b + n <= ends[k] and segs[k][1] == HP_INDEX[i]
+                for k, (_, _, st) in enumerate(segs):
+                    assert st == r + world * k
+                    streams.add(st)
+            assert len(streams) == sum(len(L.segments(r, HP_INDEX)) for r in range(world))
+            assert L.segments(0, [0] * len(SIZES)) == [(0, 0, 0)]
+
+
+def _worker(rank, world, port, kind, clip, out_dir, groups=False):
     import oracle
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -90,7 +120,17 @@ def _worker(rank, world, port, kind, clip, out_dir):
             ss = torch.tensor([oracle.sumsq(fmt, g16, 1.0 / world)], dtype=torch.float64)
             dist.all_reduce(ss)
             coef = oracle.clip_coef(float(ss[0]), 0.01)
-        if kind == "adam":
+        if kind == "adam" and groups:
+            # per-parameter groups: each segment of the shard with its own hyper-parameters
+            segs = L.segments(rank, HP_INDEX)
+            ends = [a for a, _, _ in segs[1:]] + [L.shard]
+            for (a, hgrp, _), b in zip(segs, ends):
+                sl = slice(a, b)
+                hh, rr, mm, vv = hs[sl].copy(), rs[sl].copy(), m[sl].copy(), v[sl].copy()
+                oracle.adam_step(fmt, fmt, hh, rr, g16[sl].copy(), mm, vv, lr=1e-3, weight_decay=GROUP_WD[hgrp],
+                                 grad_scale=1.0 / world, step=1, clip_coef=coef)
+                hs[sl], rs[sl] = hh, rr
+        elif kind == "adam":
             oracle.adam_step(fmt, fmt, hs, rs, g16, m, v, lr=1e-3, weight_decay=0.1, grad_scale=1.0 / world,
                              step=1, clip_coef=coef)
         else:
@@ -106,10 +146,11 @@ def _worker(rank, world, port, kind, clip, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,clip", [("adam", False), ("adam", True), ("sgd", False)])
-def test_sharded_equals_unsharded_world2(tmp_path, orc, kind, clip):
+@pytest.mark.parametrize("kind,clip,groups", [("adam", False, False), ("adam", True, False), ("sgd", False, False),
+                                              ("adam", True, True)])
+def test_sharded_equals_unsharded_world2(tmp_path, orc, kind, clip, groups):
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), kind, clip, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), kind, clip, str(tmp_path), groups), nprocs=world, join=True)
     fmt = "bf16"
     L = ShardLayout(SIZES, world)
     w = np.zeros(L.total, np.float32)
@@ -125,8 +166,16 @@ def test_sharded_equals_unsharded_world2(tmp_path, orc, kind, clip):
         coef = orc.clip_coef(orc.sumsq(fmt, g16, 1.0 / world), 0.01) if clip else None
         if clip:
             assert coef < 1.0
-        orc.adam_step(fmt, fmt, h, r, g16, m, v, lr=1e-3, weight_decay=0.1, grad_scale=1.0 / world, step=1,
-                      clip_coef=coef)
+        if groups:   # unsharded reference: every parameter stepped with its own group
+            for i, (o, n) in enumerate(zip(L.offsets, SIZES)):
+                sl = slice(o, o + n)
+                hh, rr, mm, vv = h[sl].copy(), r[sl].copy(), m[sl].copy(), v[sl].copy()
+                orc.adam_step(fmt, fmt, hh, rr, g16[sl].copy(), mm, vv, lr=1e-3, weight_decay=GROUP_WD[HP_INDEX[i]],
+                              grad_scale=1.0 / world, step=1, clip_coef=coef)
+                h[sl], r[sl] = hh, rr
+        else:
+            orc.adam_step(fmt, fmt, h, r, g16, m, v, lr=1e-3, weight_decay=0.1, grad_scale=1.0 / world, step=1,
+                          clip_coef=coef)
     else:
         orc.sgd_step(fmt, fmt, h, r, g16, m, lr=0.1, momentum=0.9, grad_scale=1.0 / world, first_step=True)
     for rank in range(world):
