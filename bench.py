@@ -688,7 +688,7 @@ def flat1m_secondary(hbm_peak, steps=100, warmup=10):
     return res
 
 
-def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
+def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024, modes=("hook", "two_phase", "amp_fp32_master")):
     """BASELINE configs[2]: GPT-2 small (HF GPT2LMHeadModel, random init, tied lm_head, 124 439 808
     params / 148 tensors) in bf16 + int16 residual, AdamW (lr 6e-4, betas (0.9, 0.95), wd 0.1)
     fused into backward through post-accumulate-grad hooks, on synthetic tokens
@@ -729,10 +729,12 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
         model = GPT2LMHeadModel(GPT2Config()).to(dev)
         P = sum(p.numel() for p in model.parameters())
         hp = dict(lr=6e-4, betas=(0.9, 0.95), weight_decay=0.1)
-        if mode in ("hook", "two_phase"):
+        if mode in ("hook", "hook_python", "two_phase"):
             opt = mpo.ResidualAdamW(model.parameters(), fmt=torch.bfloat16, **hp)   # splits fp32 init on the GPU
             if mode == "hook":
-                opt.install_backward_hooks()
+                opt.install_backward_hooks()                 # native (C++) hooks
+            elif mode == "hook_python":
+                opt.install_backward_hooks(native=False)     # the same logic as Python hooks (A/B)
 
             def step(rec=None):
                 loss = loss_of(model)
@@ -816,7 +818,7 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024):
                "peak_bytes_per_param": peak / P, "peak_gb": peak / 1e9, "loss": float(loss.detach()), "leftover_bytes_excluded": base}
         del model, opt, step, loss
         return res
-    for mode in ("hook", "two_phase", "amp_fp32_master"):
+    for mode in modes:
         try:
             out[mode] = run(mode)
         except Exception as ex:   # recorded, not hidden
@@ -985,7 +987,8 @@ def main():
         except Exception as ex:
             line["secondary"]["gpt2_hook_mode"] = {"error": f"{type(ex).__name__}: {ex}"}
         try:   # small activations (B=1, T=128): gradients are a large share of the peak
-            line["secondary"]["gpt2_hook_mode_b1_t128"] = hook_mode_secondary(batch=1, seq=128)
+            line["secondary"]["gpt2_hook_mode_b1_t128"] = hook_mode_secondary(
+                steps=20, batch=1, seq=128, modes=("hook", "two_phase", "amp_fp32_master", "hook_python"))
         except Exception as ex:
             line["secondary"]["gpt2_hook_mode_b1_t128"] = {"error": f"{type(ex).__name__}: {ex}"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -103,8 +103,56 @@ def _stale(out: str) -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
+HOOKS_SRC = os.path.join(CSRC, "mpo_hooks.cpp")
+
+
+def hooks_path() -> str:
+    import sysconfig
+    return os.path.join(LIBDIR, "mpo_hooks" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_hooks(force: bool = False) -> str:
+    """The native post-accumulate-grad hook module (csrc/mpo_hooks.cpp: autograd plumbing that
+    calls the C ABI; no kernels), compiled with g++ against the installed torch -- in-tree, so it
+    travels with the repository like the CUDA libraries."""
+    import sysconfig
+    import torch
+    from torch.utils import cpp_extension as ce
+    out = hooks_path()
+    deps = [HOOKS_SRC, os.path.join(INCLUDE, "mpo.h"), __file__]
+    if not force and os.path.exists(out) and all(os.path.getmtime(d) <= os.path.getmtime(out) for d in deps):
+        return out
+    inc = ce.include_paths(device_type="cuda") + [sysconfig.get_paths()["include"], INCLUDE]
+    libs = ce.library_paths(device_type="cuda")
+    abi = int(torch._C._GLIBCXX_USE_CXX11_ABI)
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-fvisibility=hidden", "-w",
+           f"-D_GLIBCXX_USE_CXX11_ABI={abi}", "-DTORCH_EXTENSION_NAME=mpo_hooks", "-DTORCH_API_INCLUDE_EXTENSION_H",
+           *[f"-I{d}" for d in inc], HOOKS_SRC, *[f"-L{d}" for d in libs],
+           "-lc10", "-lc10_cuda", "-ltorch", "-ltorch_cpu", "-ltorch_python", "-lcudart",
+           *[f"-Wl,-rpath,{d}" for d in libs], "-o", out + f".tmp{os.getpid()}"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("g++ failed building the native hook module")
+    os.replace(out + f".tmp{os.getpid()}", out)
+    return out
+
+
+def load_hooks():
+    """Import the native hook module from lib/ (ImportError if it was not built)."""
+    import importlib.util
+    path = hooks_path()
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python -m paper_2309_12381_b200._build`")
+    import torch  # noqa: F401  (the module links against torch's libraries)
+    spec = importlib.util.spec_from_file_location("mpo_hooks", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
 def build(force: bool = False, verbose: bool = False):
-    """Compile both libraries if a source is newer than the output."""
+    """Compile both libraries (and the native hook module) if a source is newer than the output."""
     os.makedirs(LIBDIR, exist_ok=True)
     outs = []
     for exact in (False, True):
@@ -116,6 +164,7 @@ def build(force: bool = False, verbose: bool = False):
             if verbose:
                 sys.stderr.write(log)
         outs.append(out)
+    outs.append(build_hooks(force))
     return outs
 
 

@@ -97,13 +97,15 @@ def _declare(L):
     L.mpo_p2p_sharded_step.restype = C.c_int
 
 
-def load(exact: bool = False):
-    """Load libmpo.so (FMA build) or libmpo_exact.so (-fmad=false build)."""
+def load(exact: bool = True):
+    """Load libmpo_exact.so (-fmad=false: bit-exact to the CPU oracle; the default of every entry
+    point) or libmpo.so (exact=False: FMA contraction, within DESIGN.md R12's tolerance; measured
+    0.5-1 % faster on the step, profiles/r02_ab_bulkst_exact.log)."""
     key = bool(exact)
     if key not in _libs:
         path = _build.lib_path(exact)
         override = os.environ.get("MPO_LIB_OVERRIDE")   # A/B experiments only (scripts/ab_variants.py)
-        if override and not exact:
+        if override:
             path = override
         if not os.path.exists(path):
             raise ImportError(f"{path} is missing: build it with `python -m paper_2309_12381_b200._build` "

@@ -189,7 +189,7 @@ class TensorTable:
 # Entry points (same names as the C ABI)
 # ------------------------------------------------------------------------------------------
 def mpo_split(w: torch.Tensor, fmt: torch.dtype, value: Optional[torch.Tensor] = None,
-              resid: Optional[torch.Tensor] = None, stream=None, exact: bool = False, scheme: str = "rne",
+              resid: Optional[torch.Tensor] = None, stream=None, exact: bool = True, scheme: str = "rne",
               seed: int = 0, sr_stream: int = 0):
     """fp32 -> (16-bit value, residual) under a storage scheme."""
     if w.dtype != torch.float32:
@@ -207,7 +207,7 @@ def mpo_split(w: torch.Tensor, fmt: torch.dtype, value: Optional[torch.Tensor] =
 
 
 def mpo_reconstruct(value: torch.Tensor, resid: torch.Tensor, out: Optional[torch.Tensor] = None,
-                    stream=None, exact: bool = False, scheme: str = "rne") -> torch.Tensor:
+                    stream=None, exact: bool = True, scheme: str = "rne") -> torch.Tensor:
     """(16-bit value, residual) -> fp32."""
     if out is None:
         out = torch.empty(value.shape, dtype=torch.float32, device=value.device)
@@ -226,7 +226,7 @@ def _check_ws(norm_ws, exact):
         raise MpoError(_lib.MPO_EINVAL, "norm_ws must be a float64 tensor of norm_ws_doubles() entries")
 
 
-def mpo_sgd_step(table: TensorTable, hps, norm_ws: Optional[torch.Tensor] = None, stream=None, exact: bool = False):
+def mpo_sgd_step(table: TensorTable, hps, norm_ws: Optional[torch.Tensor] = None, stream=None, exact: bool = True):
     """Residual-compensated SGD(-momentum) step over a table; skip_nonfinite needs norm_ws."""
     arr, nhp = _hp_array(hps, SgdHP)
     L = _lib_of(exact)
@@ -235,7 +235,7 @@ def mpo_sgd_step(table: TensorTable, hps, norm_ws: Optional[torch.Tensor] = None
 
 
 def mpo_adam_step(table: TensorTable, hps, norm_ws: Optional[torch.Tensor] = None, stream=None,
-                  exact: bool = False):
+                  exact: bool = True):
     """Residual-compensated Adam/AdamW step over a table; clipping needs norm_ws."""
     arr, nhp = _hp_array(hps, AdamHP)
     L = _lib_of(exact)
@@ -245,7 +245,7 @@ def mpo_adam_step(table: TensorTable, hps, norm_ws: Optional[torch.Tensor] = Non
 
 
 def mpo_fused_backward_hook_step(kind: int, vdt: int, gdt: int, one: Tensor, hp, stream=None,
-                                 exact: bool = False, norm_ws: Optional[torch.Tensor] = None):
+                                 exact: bool = True, norm_ws: Optional[torch.Tensor] = None):
     """One parameter's step from its post-accumulate-grad hook.  ``one`` is an
     mpo_tensor row, ``hp`` an SgdHP / AdamHP struct (kept by the caller); norm_ws is needed for
     skip_nonfinite (its last entry accumulates the sums of squares over the backward)."""
@@ -257,7 +257,7 @@ def mpo_fused_backward_hook_step(kind: int, vdt: int, gdt: int, one: Tensor, hp,
 def mpo_sharded_step(kind: int, comm_ptr: int, rank: int, world: int, value_flat: torch.Tensor,
                      grad_flat: torch.Tensor, resid_shard: torch.Tensor, m_shard: Optional[torch.Tensor],
                      v_shard: Optional[torch.Tensor], hp, norm_ws: Optional[torch.Tensor] = None, stream=None,
-                     exact: bool = False, scheme: str = "rne", segments=None):
+                     exact: bool = True, scheme: str = "rne", segments=None):
     """Data-parallel sharded step: RS(grad) -> shard update -> AG(value) (BASELINE north_star (c)).
 
     ``hp``: one hyper-parameter set, or a list of groups together with ``segments``, a list of
@@ -284,7 +284,7 @@ def mpo_sharded_step(kind: int, comm_ptr: int, rank: int, world: int, value_flat
 
 
 def mpo_grad_sumsq(table: TensorTable, grad_scales, norm_ws: torch.Tensor, accumulate: bool = False, stream=None,
-                   exact: bool = False):
+                   exact: bool = True):
     """S = sum (f32(g) * grad_scale[group])^2 over a table into norm_ws[0] (``accumulate``: added to it);
     the shared pre-pass of a step spanning several tables (include/mpo.h norm_ready)."""
     gs = (C.c_double * len(grad_scales))(*[float(x) for x in grad_scales])
@@ -294,13 +294,13 @@ def mpo_grad_sumsq(table: TensorTable, grad_scales, norm_ws: torch.Tensor, accum
                                    int(bool(accumulate)), _stream(stream)))
 
 
-def mpo_comm_check(comm_ptr: int, exact: bool = False):
+def mpo_comm_check(comm_ptr: int, exact: bool = True):
     """Raises MpoError(MPO_ENCCL) if the NCCL communicator failed asynchronously (never blocks)."""
     L = _lib_of(exact)
     _lib.check(L, L.mpo_comm_check(comm_ptr))
 
 
-def mpo_selfcheck_fastmath(pairs: int = 1 << 30, seed: int = 0xB0B, exact: bool = False, stream=None):
+def mpo_selfcheck_fastmath(pairs: int = 1 << 30, seed: int = 0xB0B, exact: bool = True, stream=None):
     """Fast sqrt/div sequences vs IEEE sqrtf and `/` on the device (diagnostic; see include/mpo.h).
     Returns (sqrt mismatches, div mismatches, sqrt fast-path count, div fast-path count)."""
     counts = torch.zeros(4, dtype=torch.int64, device="cuda")
@@ -311,7 +311,7 @@ def mpo_selfcheck_fastmath(pairs: int = 1 << 30, seed: int = 0xB0B, exact: bool 
 
 def mpo_p2p_sharded_step(kind: int, rank: int, world: int, value_peers: Sequence[int], grad_peers: Sequence[int],
                          resid_shard: torch.Tensor, m_shard: Optional[torch.Tensor], v_shard: Optional[torch.Tensor],
-                         n_total: int, hp, value_dtype: torch.dtype, stream=None, exact: bool = False,
+                         n_total: int, hp, value_dtype: torch.dtype, stream=None, exact: bool = True,
                          scheme: str = "rne"):
     """The sharded step fused with its collectives over NVLink peer memory (include/mpo.h): one
     kernel reads every rank's gradient shard (P2P), updates, and writes the new values into every
@@ -330,7 +330,7 @@ def mpo_p2p_sharded_step(kind: int, rank: int, world: int, value_peers: Sequence
 
 def mpo_nvls_sharded_step(kind: int, rank: int, world: int, vdt: int, value_mc: int, value_uc: int, grad_mc: int,
                           resid_shard: torch.Tensor, m_shard: Optional[torch.Tensor], v_shard: Optional[torch.Tensor],
-                          n_total: int, hp, stream=None, exact: bool = False):
+                          n_total: int, hp, stream=None, exact: bool = True):
     """The sharded step fused with its collectives over NVLink SHARP (include/mpo.h): multicast
     addresses are raw device addresses (ints) of a multicast object every rank bound."""
     L = _lib_of(exact)
@@ -343,7 +343,7 @@ class NvlsLocalBuffer:
     """A single-device multicast object bound to fresh memory (world-1 NVLS runs and tests):
     ``uc`` / ``mc`` are the unicast / multicast device addresses of the same bytes."""
 
-    def __init__(self, nbytes: int, exact: bool = False):
+    def __init__(self, nbytes: int, exact: bool = True):
         self._L = _lib_of(exact)
         uc, mc, sz = C.c_void_p(), C.c_void_p(), C.c_int64()
         _lib.check(self._L, self._L.mpo_nvls_alloc_local(nbytes, C.byref(uc), C.byref(mc), C.byref(sz)))
@@ -355,11 +355,11 @@ class NvlsLocalBuffer:
             self.uc = self.mc = None
 
 
-def norm_ws_doubles(exact: bool = False) -> int:
+def norm_ws_doubles(exact: bool = True) -> int:
     return int(_lib_of(exact).mpo_norm_ws_doubles())
 
 
-def launch_count(exact: bool = False) -> int:
+def launch_count(exact: bool = True) -> int:
     return int(_lib_of(exact).mpo_launch_count())
 
 

@@ -26,6 +26,36 @@ from ._lib import MPO_ADAM, MPO_SGD, MPO_MAX_HP_GROUPS, MpoError, Tensor
 _16 = (torch.float16, torch.bfloat16)
 
 
+class _GroupDict(dict):
+    """A param group that pushes hyper-parameter changes (e.g. an LR scheduler's
+    ``group["lr"] = ...``) to the native hooks, which build each call's struct without Python."""
+
+    def __init__(self, d, on_change):
+        super().__init__(d)
+        self._on_change = on_change
+
+    def __setitem__(self, k, v):
+        super().__setitem__(k, v)
+        self._on_change()
+
+    def update(self, *a, **kw):
+        super().update(*a, **kw)
+        self._on_change()
+
+
+def _native_finalize(ns, mod, params):
+    """The optimizer is gone: disarm the native state (its hooks then do nothing) and take the
+    hooks off the parameters that are still alive."""
+    ns.disarm()
+    for ref in params:
+        p = ref()
+        if p is not None:
+            try:
+                mod.uninstall(p)
+            except Exception:
+                pass
+
+
 def _weak_hook(opt):
     """A post-accumulate-grad hook that refers to its optimizer weakly: the tensor's hook table is
     held from C++, where Python's cycle collector cannot see it, so a strong reference would keep
@@ -60,6 +90,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         # found-inf flag has reached the host (deferred, no synchronisation in step())
         self._skip_check = None
         self._hook_S = None
+        self._native = None          # native (C++) hook state, see install_backward_hooks
         idx = 0
         for group in self.param_groups:
             for p in group["params"]:
@@ -109,7 +140,9 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         seed, gradient surgery).  The 16-bit values themselves are the parameters (model.state_dict()).
         Tensors are referenced, not copied (torch.save serialises them)."""
         self._resolve_skips()
+        self._pull_native_steps()
         sd = super().state_dict()
+        sd["param_groups"] = [{k: v for k, v in g.items()} for g in sd["param_groups"]]
         sd["mpo"] = {"format": 1, "kind": "adam" if self._kind == MPO_ADAM else "sgd", "scheme": self.scheme,
                      "seed": self.seed, "clip_value": self.clip_value, "skip_nonfinite": self.skip_nonfinite,
                      "max_grad_norm": getattr(self, "max_grad_norm", 0.0)}
@@ -162,6 +195,11 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         if self._hooks:
             self._build_rows()
             self._hp_c = {}
+        if self._native is not None:
+            self._native.resolve()
+            self._push_native_steps()
+            for gi in range(len(self.param_groups)):
+                self._push_group(gi)
 
     # -- loss scaling: step counts of skipped updates (deferred) -----------------------------
     def _queue_skip_check(self, params, dev_S):
@@ -213,6 +251,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         params = [p for g in self.param_groups for p in g["params"] if p.grad is not None]
         if not params:
             return None
+        self._pull_native_steps()            # a multi-tensor step between native-hook backwards
         by_dtype = {}
         for p in params:
             by_dtype.setdefault((p.dtype, p.grad.dtype), []).append(p)
@@ -243,13 +282,16 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             self._launch(tab, hps)
         if self.skip_nonfinite:
             self._queue_skip_check(params, self._ws(params[0].device)[:1])
+        if self._native is not None:
+            self._resolve_skips()
+            self._push_native_steps()
         return None
 
     def _needs_norm(self):
         return self.skip_nonfinite or getattr(self, "max_grad_norm", 0.0) > 0
 
     # -- hook mode ---------------------------------------------------------------------------
-    def install_backward_hooks(self, batch_below: int = 1 << 16, flush_elems: int = 1 << 22):
+    def install_backward_hooks(self, batch_below: int = 1 << 16, flush_elems: int = 1 << 22, native: bool = True):
         """Step each parameter inside backward, as soon as its gradient is accumulated, then free
         the gradient.  Returns the hook handles.
 
@@ -258,10 +300,18 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         ends, then stepped by one multi-tensor launch (bounded transient memory, far fewer
         launches).  ``batch_below=0`` steps every parameter individually; batching is off with
         ``skip_nonfinite`` (whose hook-mode skip is per parameter).  The hooks hold the optimizer
-        weakly: keep a reference to it for as long as training runs."""
+        weakly: keep a reference to it for as long as training runs.
+
+        ``native=True`` (default): the hooks are C++ (csrc/mpo_hooks.cpp, autograd plumbing that
+        calls the same C ABI): no Python runs per parameter, which keeps the hook mode's host cost
+        per backward near the two-phase step's (P:104-111 report +3-4 % time).  ``native=False``:
+        the same logic as Python hooks (A/B and reference)."""
         self._check_hook_mode()
         self._batch_below = 0 if self.skip_nonfinite else int(batch_below)
         self._flush_elems = int(flush_elems)
+        if native:
+            self._install_native()
+            return []
         self._pending = []
         self._pending_elems = 0
         self._flush_queued = False
@@ -289,10 +339,68 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                 row.sr_stream = st["index"]
                 self._rows[p] = (row, gi)
 
+    def _params_by_index(self):
+        ps = [p for g in self.param_groups for p in g["params"]]
+        return sorted(ps, key=lambda p: self.state[p]["index"])
+
+    def _install_native(self):
+        from . import _build, _lib
+        if self._native is not None:
+            raise MpoError(1, "native backward hooks are already installed")
+        mod = _build.load_hooks()
+        L = _lib.load(self.exact)
+        fn = lambda name: C.cast(getattr(L, name), C.c_void_p).value
+        params = self._params_by_index()
+        dev = params[0].device
+        ws = self._ws(dev) if self.skip_nonfinite else None
+        bufs = (None, None)
+        if self.skip_nonfinite:
+            bufs = (torch.zeros(len(params), dtype=torch.float64, device=dev),
+                    torch.zeros(len(params), dtype=torch.float64, pin_memory=True))
+        ns = mod.HookState(self._kind, self.seed & 0xFFFFFFFFFFFFFFFF, self._batch_below, self._flush_elems,
+                           fn("mpo_fused_backward_hook_step"), fn("mpo_adam_step"), fn("mpo_sgd_step"),
+                           fn("mpo_last_error"), 0 if ws is None else ws.data_ptr(),
+                           0 if bufs[0] is None else bufs[0].data_ptr(), 0 if bufs[1] is None else bufs[1].data_ptr())
+        gi_of = {id(p): gi for gi, g in enumerate(self.param_groups) for p in g["params"]}
+        for p in params:
+            st = self.state[p]
+            ns.add_param(p.data.data_ptr(), st["resid"].data_ptr(), 0 if st.get("m") is None else st["m"].data_ptr(),
+                         0 if st.get("v") is None else st["v"].data_ptr(), p.numel(), st["index"], gi_of[id(p)],
+                         api.format_code(p.dtype, self.scheme), st["step"])
+        self._native, self._native_mod, self._native_bufs = ns, mod, bufs
+        for gi in range(len(self.param_groups)):
+            self.param_groups[gi] = _GroupDict(self.param_groups[gi], lambda gi=gi: self._push_group(gi))
+            self._push_group(gi)
+        for i, p in enumerate(params):
+            mod.install(ns, p, i)
+        self._native_fin = weakref.finalize(self, _native_finalize, ns, mod, [weakref.ref(p) for p in params])
+
+    def _push_group(self, gi):
+        if self._native is not None:
+            self._native.set_group(gi, bytes(self._hp(self.param_groups[gi], 1).c()))
+
+    def _pull_native_steps(self):
+        if self._native is not None:
+            for p, stp in zip(self._params_by_index(), self._native.steps()):
+                self.state[p]["step"] = int(stp)
+
+    def _push_native_steps(self):
+        if self._native is not None:
+            self._native.set_steps([int(self.state[p]["step"]) for p in self._params_by_index()])
+
+    def native_hook_calls(self) -> int:
+        """Library calls the native hooks made so far (per-parameter steps + batched flushes)."""
+        return 0 if self._native is None else int(self._native.calls())
+
     def remove_backward_hooks(self):
         for h in self._hooks:
             h.remove()
         self._hooks = []
+        if self._native is not None:
+            self._pull_native_steps()
+            self._native_fin()                       # disarm + uninstall
+            self._native = None
+            self.param_groups[:] = [dict(g) for g in self.param_groups]
 
     def _hook(self, p: torch.Tensor):
         if self._skip_check is not None:
@@ -376,6 +484,8 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         then updated nothing), or by any hook of the backward passes since the last reset (hook
         mode skips only the offending parameters).  Synchronises with the device."""
         self._resolve_skips()
+        if self._native is not None:
+            self._native.resolve()
         if self._norm_ws is None:
             return False
         ws = self._norm_ws
@@ -402,7 +512,7 @@ class ResidualSGD(_ResidualOptimizer):
 
     def __init__(self, params: Iterable, lr: float, momentum: float = 0.0, dampening: float = 0.0,
                  weight_decay: float = 0.0, nesterov: bool = False, grad_scale: float = 1.0,
-                 fmt: Optional[torch.dtype] = None, exact: bool = False, scheme: str = "rne", seed: int = 0,
+                 fmt: Optional[torch.dtype] = None, exact: bool = True, scheme: str = "rne", seed: int = 0,
                  clip_value: float = 0.0, skip_nonfinite: bool = False):
         defaults = dict(lr=lr, momentum=momentum, dampening=dampening, weight_decay=weight_decay,
                         nesterov=nesterov, grad_scale=grad_scale)
@@ -431,7 +541,7 @@ class ResidualAdamW(_ResidualOptimizer):
 
     def __init__(self, params: Iterable, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
                  weight_decay: float = 0.0, adamw: bool = True, grad_scale: float = 1.0,
-                 max_grad_norm: Optional[float] = None, fmt: Optional[torch.dtype] = None, exact: bool = False,
+                 max_grad_norm: Optional[float] = None, fmt: Optional[torch.dtype] = None, exact: bool = True,
                  scheme: str = "rne", seed: int = 0, clip_value: float = 0.0, skip_nonfinite: bool = False):
         defaults = dict(lr=lr, betas=tuple(betas), eps=eps, weight_decay=weight_decay, adamw=adamw,
                         grad_scale=grad_scale)

@@ -129,7 +129,7 @@ class ShardedResidualOptimizer:
     global-norm clipping)."""
 
     def __init__(self, params, kind: str = "adam", fmt: Optional[torch.dtype] = None, group=None,
-                 hp=None, exact: bool = False, comm_ptr: Optional[int] = None, scheme: str = "rne",
+                 hp=None, exact: bool = True, comm_ptr: Optional[int] = None, scheme: str = "rne",
                  seed: int = 0, transport: str = "nccl", hp_index: Optional[Sequence[int]] = None):
         import torch.distributed as dist
         if transport not in ("nccl", "p2p"):
@@ -318,7 +318,7 @@ class BucketedShardedOptimizer:
     Global-norm clipping is impossible here; the per-bucket found-inf skip is available."""
 
     def __init__(self, params, kind: str = "adam", fmt: Optional[torch.dtype] = None, group=None, hp=None,
-                 bucket_elems: int = 1 << 22, exact: bool = False, comm_ptr: Optional[int] = None,
+                 bucket_elems: int = 1 << 22, exact: bool = True, comm_ptr: Optional[int] = None,
                  scheme: str = "rne", seed: int = 0):
         import torch.distributed as dist
         self.params = [p for p in params]

@@ -64,12 +64,14 @@ def _pair(fmt, kind, mpo, **kw):
 @pytest.mark.parametrize("fmt", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("kind", ["adam", "sgd"])
 @pytest.mark.parametrize("batch_below", [0, 1 << 16, 1 << 30])
-def test_hook_mode_equals_two_phase(mpo, fmt, kind, batch_below):
+@pytest.mark.parametrize("native", [True, False])
+def test_hook_mode_equals_two_phase(mpo, fmt, kind, batch_below, native):
     """Per-parameter launches (batch_below=0), small parameters batched into one launch at the end
-    of backward (default), and everything batched: all bitwise equal to the two-phase step."""
+    of backward (default), and everything batched: all bitwise equal to the two-phase step, with
+    the native (C++) hooks and with the Python hooks."""
     kw = dict(lr=1e-3, weight_decay=0.1) if kind == "adam" else dict(lr=0.1, momentum=0.9, weight_decay=1e-4)
     a, b, oa, ob = _pair(fmt, kind, mpo, **kw)
-    ob.install_backward_hooks(batch_below=batch_below)
+    ob.install_backward_hooks(batch_below=batch_below, native=native)
     gen = torch.Generator(device="cuda").manual_seed(1)
     for step in range(4):
         idx = torch.randint(0, 257, (4, 33), device="cuda", generator=gen)
@@ -91,6 +93,32 @@ def test_hook_mode_equals_two_phase(mpo, fmt, kind, batch_below):
         for k in ("m", "v"):
             if sa.get(k) is not None:
                 assert torch.equal(sa[k], sb[k]), (na, k)
+
+
+def test_native_hooks_follow_lr_changes_and_uninstall(mpo):
+    """An LR schedule that writes param_groups[i]["lr"] between backwards reaches the native hooks
+    (their group structs are pushed on assignment); the steps equal the two-phase optimizer's;
+    remove_backward_hooks() leaves ordinary gradient accumulation and keeps the step counts."""
+    a, b, oa, ob = _pair(torch.bfloat16, "adam", mpo, lr=1e-3, weight_decay=0.1)
+    ob.install_backward_hooks()
+    sa = torch.optim.lr_scheduler.StepLR(oa, step_size=1, gamma=0.5)
+    sb = torch.optim.lr_scheduler.StepLR(ob, step_size=1, gamma=0.5)
+    gen = torch.Generator(device="cuda").manual_seed(2)
+    for step in range(3):
+        idx = torch.randint(0, 257, (4, 33), device="cuda", generator=gen)
+        _loss(a, idx).backward()
+        oa.step()
+        for p in a.parameters():
+            p.grad = None
+        _loss(b, idx).backward()
+        sa.step(); sb.step()
+    assert ob.native_hook_calls() > 0
+    for pa, pb in zip(a.parameters(), b.parameters()):
+        assert torch.equal(pa.view(torch.int16), pb.view(torch.int16))
+    ob.remove_backward_hooks()
+    assert all(st["step"] == 3 for st in ob.state_dict()["state"].values())
+    _loss(b, idx).backward()
+    assert all(p.grad is not None for p in b.parameters())
 
 
 def test_hook_mode_refuses_clipping(mpo):
