@@ -40,8 +40,8 @@
  *     a tensor table name the offending table index).  NaN/Inf in gradients is NOT an error:
  *     it propagates into the weights (training-divergence signal left to the caller).
  *
- * Two builds of the same sources are shipped: libmpo_exact.so (-fmad=false, bit-exact to the CPU
- * oracle for every entry point; the build the Python binding, the optimizers and bench.py use by
+ * Two builds of the same sources are shipped: libmpo_exact.so (-fmad=false, bit-exact to the
+ * CPU oracle for every entry point; the build the Python binding, the optimizers and bench.py use by
  * default) and libmpo.so (FMA contraction; within DESIGN.md R12's tolerance, 0.5-1 % faster).
  */
 #ifndef MPO_H
