@@ -711,7 +711,16 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024, modes=("hook", "tw
         (a @ a).float().sum().backward()
         torch.nn.functional.linear(a, a).float().sum().backward()
         del a
+    # ... and the ones the autograd engine's device thread creates for this model's shapes (its own
+    # cuBLAS / cuBLASLt handle, 1 MiB Lt workspace): one throwaway fwd+bwd of the same model, so
+    # that no mode is charged for them (round 1 charged 1 MiB = 0.008 B/param to the first mode)
+    torch.manual_seed(0)
+    warm = GPT2LMHeadModel(GPT2Config()).to(dev).to(torch.bfloat16)
+    logits = warm(idx[:, :-1]).logits
+    torch.nn.functional.cross_entropy(logits.float().reshape(-1, logits.shape[-1]), idx[:, 1:].reshape(-1)).backward()
+    del warm, logits
     torch.cuda.synchronize()
+    torch.cuda.empty_cache()
 
     def loss_of(model):
         logits = model(idx[:, :-1]).logits

@@ -54,14 +54,15 @@ struct Param {
     mpo_tensor row;   // value / resid / m / v / n / sr_stream; grad filled per call
     int group = 0;
     int vdt = 0;      // storage format code of the value
-    int64_t step = 0;
+    int64_t* step = nullptr;   // this parameter's count in the optimizer's shared int64 buffer
 };
 
 class HookState : public std::enable_shared_from_this<HookState> {
    public:
-    HookState(int kind, uint64_t seed, int64_t batch_below, int64_t flush_elems, int64_t hook_fn, int64_t adam_fn,
-              int64_t sgd_fn, int64_t err_fn, int64_t norm_ws, int64_t hook_S, int64_t host_S)
+    HookState(int kind, uint64_t seed, int64_t batch_below, int64_t flush_elems, int64_t steps, int64_t hook_fn,
+              int64_t adam_fn, int64_t sgd_fn, int64_t err_fn, int64_t norm_ws, int64_t hook_S, int64_t host_S)
         : kind_(kind), seed_(seed), batch_below_(batch_below), flush_elems_(flush_elems),
+          steps_(reinterpret_cast<int64_t*>(steps)),
           hook_fn_(reinterpret_cast<HookFn>(hook_fn)), adam_fn_(reinterpret_cast<AdamFn>(adam_fn)),
           sgd_fn_(reinterpret_cast<SgdFn>(sgd_fn)), err_fn_(reinterpret_cast<ErrFn>(err_fn)),
           norm_ws_(reinterpret_cast<double*>(norm_ws)), hook_S_(reinterpret_cast<double*>(hook_S)),
@@ -73,8 +74,9 @@ class HookState : public std::enable_shared_from_this<HookState> {
         if (ev_) cudaEventDestroy(ev_);
     }
 
-    int add_param(int64_t value, int64_t resid, int64_t m, int64_t v, int64_t n, int32_t sr_stream, int group, int vdt,
-                  int64_t step) {
+    // sr_stream = the parameter's index: its slot in the step-count buffer and in hook_S
+    int add_param(int64_t value, int64_t resid, int64_t m, int64_t v, int64_t n, int32_t sr_stream, int group,
+                  int vdt) {
         Param p;
         std::memset(&p.row, 0, sizeof(p.row));
         p.row.value = reinterpret_cast<void*>(value);
@@ -85,7 +87,7 @@ class HookState : public std::enable_shared_from_this<HookState> {
         p.row.sr_stream = sr_stream;
         p.group = group;
         p.vdt = vdt;
-        p.step = step;
+        p.step = steps_ + sr_stream;
         params_.push_back(p);
         return int(params_.size()) - 1;
     }
@@ -99,16 +101,6 @@ class HookState : public std::enable_shared_from_this<HookState> {
         groups_[size_t(gi)] = bytes;
     }
 
-    std::vector<int64_t> steps() {
-        resolve();
-        std::vector<int64_t> s;
-        for (const Param& p : params_) s.push_back(p.step);
-        return s;
-    }
-    void set_steps(const std::vector<int64_t>& s) {
-        if (s.size() != params_.size()) throw std::runtime_error("mpo hook: step count list size mismatch");
-        for (size_t i = 0; i < s.size(); ++i) params_[i].step = s[i];
-    }
     void disarm() { alive_ = false; }
     int64_t calls() const { return calls_; }
 
@@ -119,7 +111,7 @@ class HookState : public std::enable_shared_from_this<HookState> {
         check_pending_ = false;
         if (cudaEventSynchronize(ev_) != cudaSuccess) throw std::runtime_error("mpo hook: cudaEventSynchronize failed");
         for (size_t i = 0; i < params_.size(); ++i)
-            if (!std::isfinite(host_S_[i])) params_[i].step -= 1;
+            if (!std::isfinite(host_S_[i])) *params_[i].step -= 1;
     }
 
     void on_grad(int idx, const at::Tensor& t) {
@@ -128,7 +120,7 @@ class HookState : public std::enable_shared_from_this<HookState> {
         if (!g.defined()) return;
         if (check_pending_) resolve();
         Param& p = params_[size_t(idx)];
-        p.step += 1;
+        *p.step += 1;
         if (!g.is_cuda() || !g.is_contiguous()) throw std::runtime_error("mpo hook: gradient must be a contiguous CUDA tensor");
         if (p.row.n < batch_below_) {
             // small parameters (biases, norms): held until one multi-tensor launch at the end of
@@ -182,15 +174,15 @@ class HookState : public std::enable_shared_from_this<HookState> {
     mpo_adam_hp adam_hp(const Param& p) const {
         mpo_adam_hp hp;
         std::memcpy(&hp, groups_.at(size_t(p.group)).data(), sizeof(hp));
-        hp.step = p.step;
-        hp.seed = step_seed(seed_, p.step);
+        hp.step = *p.step;
+        hp.seed = step_seed(seed_, *p.step);
         return hp;
     }
     mpo_sgd_hp sgd_hp(const Param& p) const {
         mpo_sgd_hp hp;
         std::memcpy(&hp, groups_.at(size_t(p.group)).data(), sizeof(hp));
-        hp.first_step = p.step == 1;
-        hp.seed = step_seed(seed_, p.step);
+        hp.first_step = *p.step == 1;
+        hp.seed = step_seed(seed_, *p.step);
         return hp;
     }
 
@@ -219,7 +211,7 @@ class HookState : public std::enable_shared_from_this<HookState> {
             std::vector<mpo_sgd_hp> shp;
             for (size_t k : kv.second) {
                 const Param& p = params_[size_t(pending[k].first)];
-                auto key = std::make_pair(p.group, p.step);
+                auto key = std::make_pair(p.group, *p.step);
                 auto it = keys.find(key);
                 int h;
                 if (it == keys.end()) {
@@ -251,6 +243,7 @@ class HookState : public std::enable_shared_from_this<HookState> {
     int kind_;
     uint64_t seed_;
     int64_t batch_below_, flush_elems_;
+    int64_t* steps_;
     HookFn hook_fn_;
     AdamFn adam_fn_;
     SgdFn sgd_fn_;
@@ -291,11 +284,9 @@ PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
     m.doc() = "native post-accumulate-grad hooks of the fused backward step (calls the libmpo C ABI)";
     py::class_<HookState, std::shared_ptr<HookState>>(m, "HookState")
         .def(py::init<int, uint64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
-                      int64_t>())
+                      int64_t, int64_t>())
         .def("add_param", &HookState::add_param)
         .def("set_group", [](HookState& s, int gi, py::bytes b) { s.set_group(gi, std::string(b)); })
-        .def("steps", &HookState::steps)
-        .def("set_steps", &HookState::set_steps)
         .def("resolve", &HookState::resolve)
         .def("disarm", &HookState::disarm)
         .def("calls", &HookState::calls);

@@ -2,6 +2,9 @@
 // the code being the C ABI's mpo_dtype value: base | scheme << 4; see mpo_device.cuh Fmt).
 #include "mpo_kernels.cuh"
 
+#include <cstdlib>
+#include <cstring>
+
 #ifndef MPO_SF
 #error "compile with -DMPO_SF=<storage format code>"
 #endif
@@ -75,15 +78,49 @@ mpo_status FormatOps<SF>::nvls(int kind, void* value_mc, const void* value_uc, c
 template <>
 mpo_status FormatOps<SF>::p2p(int kind, const Peers& peers, int world, int rank, void* resid, float* m, float* v,
                               int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak, cudaStream_t s) {
-    const int64_t grid = grid_for((n / kUnitEl + kThreads - 1) / kThreads, 8);
-    if (kind == MPO_ADAM)
-        p2p_step_kernel<SF, AdamOp><<<unsigned(grid), kThreads, 0, s>>>(peers, world, rank, resid, m, v, shard_base, n,
-                                                                         *ak);
+    static const bool lsu = [] {
+        const char* e = std::getenv("MPO_P2P_KERNEL");
+        return e && std::strcmp(e, "lsu") == 0;
+    }();
+    if (lsu) {   // per-thread 128-bit loads of every stream (A/B; round-1 kernel)
+        const int64_t grid = grid_for((n / kUnitEl + kThreads - 1) / kThreads, 8);
+        if (kind == MPO_ADAM)
+            p2p_step_kernel<SF, AdamOp><<<unsigned(grid), kThreads, 0, s>>>(peers, world, rank, resid, m, v, shard_base,
+                                                                             n, *ak);
+        else
+            p2p_step_kernel<SF, SgdOp><<<unsigned(grid), kThreads, 0, s>>>(peers, world, rank, resid, m, v, shard_base,
+                                                                            n, *sk);
+        ++g_launches;
+        return check_launch("p2p_step_kernel");
+    }
+    // bulk-copy pipeline: stages of [value | resid | world grads | m | v] in 113 KB per CTA
+    const bool adam = kind == MPO_ADAM;
+    const int sb = int(kP2PTileEl) * (2 + Fmt<SF>::rbytes + 2 * world + 4 + (adam ? 4 : 0));
+    int stages = (kP2PSmem - kBarBytes) / sb;
+    stages = stages > kMaxStages ? kMaxStages : stages;
+    if (stages < 2) return fail(MPO_EINVAL, "P2P step: too many ranks for the shared-memory stages");
+    const int smem = kBarBytes + stages * sb;
+    const int64_t tiles = (n + kP2PTileEl - 1) / kP2PTileEl;
+    const int64_t grid = grid_for(tiles, 2);
+    cudaError_t attr;
+    if (adam) {
+        static const cudaError_t a = cudaFuncSetAttribute(p2p_tma_kernel<SF, AdamOp>,
+                                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kP2PSmem);
+        attr = a;
+    } else {
+        static const cudaError_t a = cudaFuncSetAttribute(p2p_tma_kernel<SF, SgdOp>,
+                                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kP2PSmem);
+        attr = a;
+    }
+    if (attr != cudaSuccess) return fail(MPO_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr));
+    if (adam)
+        p2p_tma_kernel<SF, AdamOp><<<unsigned(grid), kP2PThreads, smem, s>>>(peers, world, rank, resid, m, v,
+                                                                             shard_base, n, *ak, stages);
     else
-        p2p_step_kernel<SF, SgdOp><<<unsigned(grid), kThreads, 0, s>>>(peers, world, rank, resid, m, v, shard_base, n,
-                                                                        *sk);
+        p2p_tma_kernel<SF, SgdOp><<<unsigned(grid), kP2PThreads, smem, s>>>(peers, world, rank, resid, m, v,
+                                                                            shard_base, n, *sk, stages);
     ++g_launches;
-    return check_launch("p2p_step_kernel");
+    return check_launch("p2p_tma_kernel");
 }
 
 }  // namespace mpo

@@ -1332,6 +1332,186 @@ __global__ void __launch_bounds__(kThreads) p2p_step_kernel(const __grid_constan
     asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
+// ---- the same fused P2P step on the bulk-copy pipeline (default; MPO_P2P_KERNEL=lsu selects the
+// kernel above).  One producer warp streams, per 2048-element tile of this rank's shard, the local
+// value replica / residual / m / v AND the 16-bit gradient slice of every rank (peer addresses)
+// into a shared-memory stage with 1-D bulk copies; 8 consumer warps sum the ranks' gradients from
+// the stage in rank order (R15), update, and store the new values into every replica (P2P
+// stores) and residual / m / v locally.  Tiles are half the step kernel's so that 8 ranks'
+// gradients still leave >= 2 stages in half an SM's shared memory (2 CTAs per SM).
+constexpr int kP2PCW = 8;
+constexpr int64_t kP2PTileEl = int64_t(kP2PCW) * 32 * kUnitEl;   // 2048 elements
+constexpr int kP2PThreads = (kP2PCW + 1) * 32;
+constexpr int kP2PSmem = 113 * 1024;                              // per CTA, 2 CTAs per SM
+
+// Ragged tail of the shard (X8's 16-element bulk granule): element by element, peers read directly.
+template <int SF, class Op>
+__device__ __noinline__ void p2p_tail(const Peers& P, int world, int rank, void* resid, float* m, float* v,
+                                      int64_t shard_base, int64_t lo, int64_t hi, const typename Op::K c) {
+    using FM = Fmt<SF>;
+    constexpr int B = FM::base;
+    const bool need_m = Op::reads_m(c), has_m = Op::writes_m(c);
+    for (int64_t i = lo; i < hi; ++i) {
+        float g = grad_f32_16<B>(P.g[0][shard_base + i]);
+        for (int k = 1; k < world; ++k) g = g + grad_f32_16<B>(P.g[k][shard_base + i]);
+        g = g * c.gs;
+        if (c.clip_on) g = clamp_grad(g, c.clipv);
+        int32_t code;
+        if constexpr (FM::rbytes == 1) code = static_cast<const int8_t*>(resid)[i];
+        else if constexpr (FM::scheme == kRTZ) code = static_cast<const uint16_t*>(resid)[i];
+        else code = static_cast<const int16_t*>(resid)[i];
+        float w = reconstruct1_s<SF>(P.v[rank][shard_base + i], code);
+        float mi = need_m ? m[i] : 0.0f;
+        float vi = 0.0f;
+        if constexpr (Op::kHasV) vi = v[i];
+        w = Op::apply(w, g, mi, vi, c);
+        uint32_t h;
+        split1_s<SF>(w, sr_draw(c.seed, uint32_t(rank), uint64_t(i)), h, code);
+        for (int k = 0; k < world; ++k) P.v[k][shard_base + i] = static_cast<uint16_t>(h);
+        if constexpr (FM::rbytes == 1) static_cast<int8_t*>(resid)[i] = static_cast<int8_t>(code);
+        else static_cast<int16_t*>(resid)[i] = static_cast<int16_t>(code);
+        if (has_m) m[i] = mi;
+        if constexpr (Op::kHasV) v[i] = vi;
+    }
+}
+
+template <int SF, class Op>
+__global__ void __launch_bounds__(kP2PThreads, 2) p2p_tma_kernel(const __grid_constant__ Peers P, int world, int rank,
+                                                                  void* resid, float* __restrict__ m,
+                                                                  float* __restrict__ v, int64_t shard_base, int64_t n,
+                                                                  const __grid_constant__ typename Op::K c, int stages) {
+    constexpr int B = Fmt<SF>::base;
+    constexpr int RB = Fmt<SF>::rbytes;
+    constexpr int64_t TE = kP2PTileEl;
+    constexpr uint32_t kGran = RB == 1 ? 16u : uint32_t(kUnitEl);
+    // stage layout: [value TE*2 | resid TE*RB | grads of rank 0..world-1, TE*2 each | m TE*4 | v TE*4]
+    const int OFF_R = int(TE) * 2, OFF_G = int(TE) * (2 + RB), OFF_M = OFF_G + int(TE) * 2 * world,
+              OFF_V = OFF_M + int(TE) * 4;
+    const int SB = OFF_V + (Op::kHasV ? int(TE) * 4 : 0);
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + kMaxStages;
+    unsigned char* ring = smem + kBarBytes;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool need_m = Op::reads_m(c), has_m = Op::writes_m(c);
+    const int64_t ntiles = (n + TE - 1) / TE;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kP2PCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kP2PCW) {
+        if (lane == 0) {
+            const uint64_t pol = load_policy();
+            int s = 0;
+            uint32_t ph = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int64_t base = tile * TE;
+                const int64_t nvalid = n - base < TE ? n - base : TE;
+                const uint32_t nvec = uint32_t(nvalid) & ~(kGran - 1u);
+                mbar_wait(&empty[s], ph ^ 1u);
+                uint32_t bytes = nvec * (2u + RB + 2u * uint32_t(world));
+                if (need_m) bytes += nvec * 4u;
+                if constexpr (Op::kHasV) bytes += nvec * 4u;
+                unsigned char* st = ring + size_t(s) * SB;
+                mbar_arrive_expect_tx(&full[s], bytes);
+                if (nvec) {
+                    bulk_g2s(st, P.v[rank] + shard_base + base, nvec * 2u, &full[s], pol);
+                    bulk_g2s(st + OFF_R, static_cast<const unsigned char*>(resid) + base * RB, nvec * RB, &full[s], pol);
+                    for (int k = 0; k < world; ++k)
+                        bulk_g2s(st + OFF_G + k * int(TE) * 2, P.g[k] + shard_base + base, nvec * 2u, &full[s], pol);
+                    if (need_m) bulk_g2s(st + OFF_M, m + base, nvec * 4u, &full[s], pol);
+                    if constexpr (Op::kHasV) bulk_g2s(st + OFF_V, v + base, nvec * 4u, &full[s], pol);
+                }
+                if (++s == stages) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+        return;
+    }
+    const int64_t el = int64_t(threadIdx.x) * kUnitEl;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t base = tile * TE;
+        const int64_t nvalid = n - base < TE ? n - base : TE;
+        const int64_t nvec = nvalid & ~int64_t(kGran - 1u);
+        const bool full_unit = el + kUnitEl <= nvec;
+        mbar_wait(&full[s], ph);
+        uint4 hv = make_uint4(0u, 0u, 0u, 0u);
+        ResidUnit<SF> rv;
+        rv.v = hv;
+        float gsum[8], mm[8], vv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) gsum[k] = mm[k] = vv[k] = 0.0f;
+        if (full_unit) {
+            const unsigned char* st = ring + size_t(s) * SB;
+            hv = *reinterpret_cast<const uint4*>(st + el * 2);
+            if constexpr (RB == 2) {
+                rv.v = *reinterpret_cast<const uint4*>(st + OFF_R + el * 2);
+            } else {
+                const uint2 r2 = *reinterpret_cast<const uint2*>(st + OFF_R + el);
+                rv.v = make_uint4(r2.x, r2.y, 0u, 0u);
+            }
+            // the ranks' gradients summed in fp32 in rank order (R15)
+            GradUnit<B> g0;
+            g0.a = *reinterpret_cast<const uint4*>(st + OFF_G + el * 2);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) gsum[i] = grad_at<B>(g0, i);
+            for (int k = 1; k < world; ++k) {
+                GradUnit<B> gx;
+                gx.a = *reinterpret_cast<const uint4*>(st + OFF_G + k * int(TE) * 2 + el * 2);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) gsum[i] = gsum[i] + grad_at<B>(gx, i);
+            }
+            if (need_m) {
+                const float4 a = *reinterpret_cast<const float4*>(st + OFF_M + el * 4);
+                const float4 b = *reinterpret_cast<const float4*>(st + OFF_M + el * 4 + 16);
+                mm[0] = a.x; mm[1] = a.y; mm[2] = a.z; mm[3] = a.w; mm[4] = b.x; mm[5] = b.y; mm[6] = b.z; mm[7] = b.w;
+            }
+            if constexpr (Op::kHasV) {
+                const float4 a = *reinterpret_cast<const float4*>(st + OFF_V + el * 4);
+                const float4 b = *reinterpret_cast<const float4*>(st + OFF_V + el * 4 + 16);
+                vv[0] = a.x; vv[1] = a.y; vv[2] = a.z; vv[3] = a.w; vv[4] = b.x; vv[5] = b.y; vv[6] = b.z; vv[7] = b.w;
+            }
+        }
+        uint4 ho;
+        ResidUnit<SF> ro;
+        if (full_unit) {
+            GradUnit<kFP32> gu;
+            gu.a = make_uint4(__float_as_uint(gsum[0]), __float_as_uint(gsum[1]), __float_as_uint(gsum[2]),
+                              __float_as_uint(gsum[3]));
+            gu.b = make_uint4(__float_as_uint(gsum[4]), __float_as_uint(gsum[5]), __float_as_uint(gsum[6]),
+                              __float_as_uint(gsum[7]));
+            // stochastic-rounding draws keyed like mpo_sharded_step: stream = rank, index in the shard
+            process_unit<SF, kFP32, Op, false>(hv, rv, gu, mm, vv, c, 1.0f, uint32_t(rank), base + el, ho, ro);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (full_unit) {
+            const int64_t e = base + el;
+            for (int k = 0; k < world; ++k) stv(P.v[k] + shard_base + e, ho);   // every rank's replica
+            st_resid<SF>(resid, e, ro);
+            if (has_m) stf8(m + e, mm);
+            if constexpr (Op::kHasV) stf8(v + e, vv);
+        } else if (nvec < nvalid && el <= nvec && nvec < el + kUnitEl) {
+            p2p_tail<SF, Op>(P, world, rank, resid, m, v, shard_base, base + nvec, base + nvalid, c);
+        }
+        if (++s == stages) {
+            s = 0;
+            ph ^= 1u;
+        }
+    }
+    // peer stores visible system-wide before the caller's cross-rank barrier
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
 // ------------------------------------------------------------------------------------------
 // Host launch templates
 // ------------------------------------------------------------------------------------------

@@ -91,6 +91,9 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         self._skip_check = None
         self._hook_S = None
         self._native = None          # native (C++) hook state, see install_backward_hooks
+        # per-parameter step counts, one int64 each: state[p]["step"] is a 0-dim view of this host
+        # buffer, which the native hooks update in place (one source of truth for both paths)
+        self._steps = torch.zeros(sum(len(g["params"]) for g in self.param_groups), dtype=torch.int64)
         idx = 0
         for group in self.param_groups:
             for p in group["params"]:
@@ -117,7 +120,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             st["resid"] = torch.zeros(p.shape, dtype=api.resid_dtype(self.scheme), device=p.device)
         else:
             raise MpoError(3, f"unsupported parameter dtype {p.dtype}")
-        st["step"] = 0
+        st["step"] = self._steps[idx]
         self._init_state(p, st)
 
     def _init_state(self, p, st):
@@ -143,6 +146,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         self._pull_native_steps()
         sd = super().state_dict()
         sd["param_groups"] = [{k: v for k, v in g.items()} for g in sd["param_groups"]]
+        sd["state"] = {k: {**st, "step": int(st["step"])} for k, st in sd["state"].items()}
         sd["mpo"] = {"format": 1, "kind": "adam" if self._kind == MPO_ADAM else "sgd", "scheme": self.scheme,
                      "seed": self.seed, "clip_value": self.clip_value, "skip_nonfinite": self.skip_nonfinite,
                      "max_grad_norm": getattr(self, "max_grad_norm", 0.0)}
@@ -180,7 +184,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                         raise MpoError(3, f"parameter {k}: '{key}' is {src.dtype}{tuple(src.shape)}, "
                                           f"expected {dst.dtype}{tuple(dst.shape)}")
                     dst.copy_(src)
-                cur["step"] = int(st["step"])
+                cur["step"].fill_(int(st["step"]))
                 cur["index"] = int(st["index"])
         for g, a in zip(self.param_groups, saved):
             for key, val in a.items():
@@ -262,7 +266,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             keys, hp_index = {}, []
             for p, gi in zip(plist, tab._group_of):
                 self.state[p]["step"] += 1
-                k = (gi, self.state[p]["step"])
+                k = (gi, int(self.state[p]["step"]))
                 hp_index.append(keys.setdefault(k, len(keys)))
             if len(keys) > MPO_MAX_HP_GROUPS:
                 raise MpoError(1, "more than 16 distinct (group, step) pairs in one step")
@@ -358,6 +362,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             bufs = (torch.zeros(len(params), dtype=torch.float64, device=dev),
                     torch.zeros(len(params), dtype=torch.float64, pin_memory=True))
         ns = mod.HookState(self._kind, self.seed & 0xFFFFFFFFFFFFFFFF, self._batch_below, self._flush_elems,
+                           self._steps.data_ptr(),
                            fn("mpo_fused_backward_hook_step"), fn("mpo_adam_step"), fn("mpo_sgd_step"),
                            fn("mpo_last_error"), 0 if ws is None else ws.data_ptr(),
                            0 if bufs[0] is None else bufs[0].data_ptr(), 0 if bufs[1] is None else bufs[1].data_ptr())
@@ -366,7 +371,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             st = self.state[p]
             ns.add_param(p.data.data_ptr(), st["resid"].data_ptr(), 0 if st.get("m") is None else st["m"].data_ptr(),
                          0 if st.get("v") is None else st["v"].data_ptr(), p.numel(), st["index"], gi_of[id(p)],
-                         api.format_code(p.dtype, self.scheme), st["step"])
+                         api.format_code(p.dtype, self.scheme))
         self._native, self._native_mod, self._native_bufs = ns, mod, bufs
         for gi in range(len(self.param_groups)):
             self.param_groups[gi] = _GroupDict(self.param_groups[gi], lambda gi=gi: self._push_group(gi))
@@ -380,13 +385,13 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             self._native.set_group(gi, bytes(self._hp(self.param_groups[gi], 1).c()))
 
     def _pull_native_steps(self):
+        """The native hooks count steps in place in self._steps; only a pending found-inf rollback
+        of the last backward has to be applied before the counts are read."""
         if self._native is not None:
-            for p, stp in zip(self._params_by_index(), self._native.steps()):
-                self.state[p]["step"] = int(stp)
+            self._native.resolve()
 
     def _push_native_steps(self):
-        if self._native is not None:
-            self._native.set_steps([int(self.state[p]["step"]) for p in self._params_by_index()])
+        pass
 
     def native_hook_calls(self) -> int:
         """Library calls the native hooks made so far (per-parameter steps + batched flushes)."""
@@ -422,12 +427,12 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         row.grad = g.data_ptr()
         # host cost per hook matters when backward is short: the ctypes hyper-parameters are built
         # once per (group, step) and shared by the group's parameters; format codes are cached
-        key = (group, st["step"])
+        key = (group, int(st["step"]))
         hp = self._hp_c.get(key)
         if hp is None:
             if len(self._hp_c) > 64:
                 self._hp_c.clear()
-            hp = self._hp_c[key] = self._hp(self.param_groups[group], st["step"]).c()
+            hp = self._hp_c[key] = self._hp(self.param_groups[group], key[1]).c()
         codes = self._codes.get((p.dtype, g.dtype))
         if codes is None:
             codes = self._codes[(p.dtype, g.dtype)] = (api.format_code(p.dtype, self.scheme), api.dtype_code(g.dtype))
@@ -463,7 +468,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                 sts = [self.state[p] for p in ps]
                 keys, hp_index = {}, []
                 for p_, s_ in zip(ps, sts):
-                    hp_index.append(keys.setdefault((self._rows[p_][1], s_["step"]), len(keys)))
+                    hp_index.append(keys.setdefault((self._rows[p_][1], int(s_["step"])), len(keys)))
                 tab = api.TensorTable([p.data for p in ps], [s_["resid"] for s_ in sts], [g for _, g in items],
                                       [s_.get("m") for s_ in sts], [s_.get("v") for s_ in sts], hp_index,
                                       scheme=self.scheme, sr_streams=[s_["index"] for s_ in sts])

@@ -1,0 +1,164 @@
+"""Multi-GPU parity of the three sharded transports (BASELINE north_star (c)),
+for a box with >= 2 GPUs.  Run one process per GPU:
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 --master-port 29511 \\
+        -m pytest tests/test_multigpu.py -q -p no:cacheprovider
+
+Skipped when WORLD_SIZE < 2 (the 1-GPU `pytest -m gpu` run).  On every rank, with gradients built so
+the cross-rank sum is exact in bf16 (multiples of 2^-12, |k| <= 16 per rank: reading R13 / R15 --
+NCCL's 16-bit per-hop sums, the P2P kernel's rank-order fp32 sum and NVLS's in-switch fp32 sum then
+all equal the exact sum):
+* mpo_sharded_step (NCCL reduce-scatter -> shard update -> all-gather) leaves every replica equal to
+  the oracle's unsharded step on the summed gradient, bit for bit (exact build), with per-parameter
+  hyper-parameter groups (mpo_sharded_step_grouped) and with global-norm clipping;
+* mpo_p2p_sharded_step over torch symmetric memory (real NVLink peers) == the NCCL result, bitwise;
+* mpo_nvls_sharded_step over the symmetric-memory multicast object (when the box exposes one)
+  == the NCCL result, bitwise;
+* the communicator reports healthy (mpo_comm_check).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+WORLD = int(os.environ.get("WORLD_SIZE", "1"))
+SIZES = [33 * 17, 4096, 5, 128 * 64, 1000, 3, 65536 + 8]
+
+
+@pytest.fixture(scope="module")
+def dist():
+    if WORLD < 2 or not torch.cuda.is_available():
+        pytest.skip("needs WORLD_SIZE >= 2 (launch with torch.distributed.run)")
+    import torch.distributed as d
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    d.init_process_group("nccl", device_id=torch.device("cuda", local))
+    yield d
+    d.destroy_process_group()
+
+
+def _setup(dist, fmt="bf16"):
+    from paper_2309_12381_b200 import ShardLayout
+    rank = dist.get_rank()
+    L = ShardLayout(SIZES, WORLD)
+    w = np.zeros(L.total, np.float32)
+    g = [np.zeros(L.total, np.float32) for _ in range(WORLD)]
+    for i, (o, n) in enumerate(zip(L.offsets, SIZES)):
+        w[o:o + n] = synth.weights(n, 0.02, 0xB0B + i)
+        for r in range(WORLD):
+            g[r][o:o + n] = synth.rng(77, r, i).integers(-16, 17, size=n).astype(np.float32) * np.float32(2.0 ** -12)
+    return L, rank, w, g
+
+
+def _oracle_step(orc, L, w, g, hp_of_param, clip):
+    fmt = "bf16"
+    h, r = orc.split(fmt, w)
+    gsum = synth.to16_bits(sum(g), fmt)
+    assert np.array_equal(orc.widen(fmt, gsum), sum(g).astype(np.float32))     # exact sum
+    m = np.zeros(L.total, np.float32)
+    v = np.zeros(L.total, np.float32)
+    coef = orc.clip_coef(orc.sumsq(fmt, gsum, 1.0 / WORLD), clip) if clip else None
+    for i, (o, n) in enumerate(zip(L.offsets, SIZES)):
+        sl = slice(o, o + n)
+        hh, rr, mm, vv = h[sl].copy(), r[sl].copy(), m[sl].copy(), v[sl].copy()
+        orc.adam_step(fmt, fmt, hh, rr, gsum[sl].copy(), mm, vv, lr=1e-3, weight_decay=hp_of_param(i),
+                      grad_scale=1.0 / WORLD, step=1, clip_coef=coef)
+        h[sl], r[sl] = hh, rr
+    return h, r
+
+
+def _dev(a, dt=torch.bfloat16):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int16).copy()).view(dt).cuda()
+
+
+@pytest.mark.parametrize("groups,clip", [(False, 0.0), (True, 0.0), (False, 0.01)])
+def test_nccl_sharded_step_equals_oracle(dist, orc, groups, clip):
+    import paper_2309_12381_b200 as mpo
+    from paper_2309_12381_b200._lib import MPO_ADAM
+    from paper_2309_12381_b200.sharded import nccl_comm_ptr
+    L, rank, w, g = _setup(dist)
+    wd = (lambda i: 0.1 if i % 2 == 0 else 0.0) if groups else (lambda i: 0.1)
+    h, r = orc.split("bf16", w)
+    value, grad = _dev(h), _dev(synth.to16_bits(g[rank], "bf16"))
+    lo, hi = L.shard_range(rank)
+    resid = torch.from_numpy(r[lo:hi].copy()).cuda()
+    m = torch.zeros(L.shard, device="cuda")
+    v = torch.zeros(L.shard, device="cuda")
+    ws = torch.zeros(mpo.norm_ws_doubles(), dtype=torch.float64, device="cuda")
+    comm = nccl_comm_ptr()
+    if groups:
+        hps = [mpo.AdamParams(lr=1e-3, weight_decay=0.1, grad_scale=1.0 / WORLD, max_grad_norm=clip),
+               mpo.AdamParams(lr=1e-3, weight_decay=0.0, grad_scale=1.0 / WORLD, max_grad_norm=clip)]
+        segs = L.segments(rank, [0 if i % 2 == 0 else 1 for i in range(len(SIZES))])
+        mpo.mpo_sharded_step(MPO_ADAM, comm, rank, WORLD, value, grad, resid, m, v, hps, norm_ws=ws if clip else None,
+                             segments=segs)
+    else:
+        hp = mpo.AdamParams(lr=1e-3, weight_decay=0.1, grad_scale=1.0 / WORLD, max_grad_norm=clip)
+        mpo.mpo_sharded_step(MPO_ADAM, comm, rank, WORLD, value, grad, resid, m, v, hp, norm_ws=ws if clip else None)
+    torch.cuda.synchronize()
+    mpo.mpo_comm_check(comm)
+    ho, ro = _oracle_step(orc, L, w, g, wd, clip)
+    assert np.array_equal(value.view(torch.int16).cpu().numpy().view(np.uint16), ho)
+    assert np.array_equal(resid.cpu().numpy(), ro[lo:hi])
+
+
+def _symm(n, dt):
+    import torch.distributed._symmetric_memory as symm
+    return symm.empty(n, dtype=dt, device="cuda")
+
+
+def test_p2p_and_nvls_equal_nccl(dist, orc):
+    """Real NVLink peers: the fused P2P kernel (and NVLS multicast when available) == NCCL."""
+    import paper_2309_12381_b200 as mpo
+    from paper_2309_12381_b200 import api
+    from paper_2309_12381_b200._lib import MPO_ADAM
+    from paper_2309_12381_b200.sharded import _peer_addrs, _rendezvous, nccl_comm_ptr
+    L, rank, w, g = _setup(dist)
+    h, r = orc.split("bf16", w)
+    lo, hi = L.shard_range(rank)
+    hp = mpo.AdamParams(lr=1e-3, weight_decay=0.1, grad_scale=1.0 / WORLD)
+    results = {}
+    # NCCL reference
+    value, grad = _dev(h), _dev(synth.to16_bits(g[rank], "bf16"))
+    resid = torch.from_numpy(r[lo:hi].copy()).cuda()
+    m, v = torch.zeros(L.shard, device="cuda"), torch.zeros(L.shard, device="cuda")
+    mpo.mpo_sharded_step(MPO_ADAM, nccl_comm_ptr(), rank, WORLD, value, grad, resid, m, v, hp)
+    torch.cuda.synchronize()
+    results["nccl"] = (value.view(torch.int16).cpu().numpy(), resid.cpu().numpy(), m.cpu().numpy(), v.cpu().numpy())
+    # P2P over symmetric memory
+    sv, sg = _symm(L.total, torch.bfloat16), _symm(L.total, torch.bfloat16)
+    sv.copy_(_dev(h))
+    sg.copy_(_dev(synth.to16_bits(g[rank], "bf16")))
+    hv, hg = _rendezvous(sv, None), _rendezvous(sg, None)
+    resid = torch.from_numpy(r[lo:hi].copy()).cuda()
+    m, v = torch.zeros(L.shard, device="cuda"), torch.zeros(L.shard, device="cuda")
+    hg.barrier(channel=0)
+    api.mpo_p2p_sharded_step(MPO_ADAM, rank, WORLD, _peer_addrs(hv, sv, rank), _peer_addrs(hg, sg, rank), resid, m, v,
+                             L.total, hp, torch.bfloat16)
+    hv.barrier(channel=0)
+    torch.cuda.synchronize()
+    results["p2p"] = (sv.view(torch.int16).cpu().numpy(), resid.cpu().numpy(), m.cpu().numpy(), v.cpu().numpy())
+    # NVLS (multicast object of the symmetric allocation), when the box provides it
+    mc_v, mc_g = int(getattr(hv, "multicast_ptr", 0) or 0), int(getattr(hg, "multicast_ptr", 0) or 0)
+    if mc_v and mc_g:
+        sv.copy_(_dev(h))
+        sg.copy_(_dev(synth.to16_bits(g[rank], "bf16")))
+        resid = torch.from_numpy(r[lo:hi].copy()).cuda()
+        m, v = torch.zeros(L.shard, device="cuda"), torch.zeros(L.shard, device="cuda")
+        off_v = sv.data_ptr() - int(hv.buffer_ptrs[rank])
+        off_g = sg.data_ptr() - int(hg.buffer_ptrs[rank])
+        hg.barrier(channel=0)
+        api.mpo_nvls_sharded_step(MPO_ADAM, rank, WORLD, api.format_code(torch.bfloat16), mc_v + off_v, sv.data_ptr(),
+                                  mc_g + off_g, resid, m, v, L.total, hp)
+        hv.barrier(channel=0)
+        torch.cuda.synchronize()
+        results["nvls"] = (sv.view(torch.int16).cpu().numpy(), resid.cpu().numpy(), m.cpu().numpy(), v.cpu().numpy())
+    ref = results["nccl"]
+    for name, res in results.items():
+        for a, b in zip(ref, res):
+            assert np.array_equal(np.asarray(a).view(np.uint8), np.asarray(b).view(np.uint8)), name
