@@ -674,11 +674,43 @@ def flat1m_secondary(hbm_peak, steps=100, warmup=10):
         pool[it[0] % sets].step()
         it[0] += 1
     ms_rot, _ = timed(rot, steps * 2, sets)
+    # device side only: the same `steps` launches (step counts 1..steps) captured in one CUDA graph
+    # and replayed, so the host's per-call cost (Python marshalling + validation + launch, ~10 us)
+    # drops out and what remains is the kernel's own launch-to-launch time
+    g_us = None
+    try:
+        s_ = torch.cuda.Stream()
+        graph = torch.cuda.CUDAGraph()
+        t0_ = wl.t
+        with torch.cuda.stream(s_):
+            wl.step()                                   # warm (first-call attribute setup) off-graph
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph, stream=s_):
+                for _ in range(steps):
+                    wl.step()
+        wl.t = t0_
+        graph.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(5):
+            graph.replay()
+        b.record()
+        torch.cuda.synchronize()
+        g_us = a.elapsed_time(b) / (5 * steps) * 1e3
+        del graph
+    except Exception as ex:   # recorded, not hidden
+        g_us = f"unavailable: {type(ex).__name__}: {ex}"[:200]
     res = {"config": f"BASELINE configs[0]: {wl.P} params, 1 tensor, fp16 + int16 residual, Adam, {steps} steps",
+           "cuda_graph_device_only": ({"us_per_step": g_us, "params_per_s": wl.P / (g_us * 1e-6),
+                                       "gbs": per / (g_us * 1e-6) / 1e9, "frac_of_measured_hbm":
+                                       per / (g_us * 1e-6) / 1e9 / hbm_peak}
+                                      if isinstance(g_us, float) else g_us),
            "bytes_per_param": bpp, "launches_per_step": launches / steps,
            "back_to_back_l2_resident": {"params_per_s": wl.P / (ms * 1e-3), "us_per_step": ms * 1e3,
                                         "gbs": per / (ms * 1e-3) / 1e9,
-                                        "note": "27 MB working set < L2: launch / L2-bound"},
+                                        "note": "27 MB working set < L2; bound by the host's per-call cost "
+                                                "(Python marshalling + C validation + launch), see cuda_graph"},
            "l2_flushed_rotating": {"params_per_s": wl.P / (ms_rot * 1e-3), "us_per_step": ms_rot * 1e3,
                                    "gbs": per / (ms_rot * 1e-3) / 1e9,
                                    "frac_of_measured_hbm": per / (ms_rot * 1e-3) / 1e9 / hbm_peak,

@@ -223,17 +223,18 @@ mpo_status check_table(const mpo_tensor* t, int32_t nt, int32_t nhp, bool adam, 
     if (nt < 0 || (nt > 0 && !t)) return fail(MPO_EINVAL, "bad tensor table");
     for (int i = 0; i < nt; ++i) {
         const mpo_tensor& x = t[i];
-        const std::string who = "tensor " + std::to_string(i) + ": ";
-        if (x.n < 0) return fail(MPO_EINVAL, who + "negative size");
-        if (x.hp < 0 || x.hp >= nhp) return fail(MPO_EINVAL, who + "hyper-parameter group index out of range");
-        if (x.sr_stream < 0 || x.sr_stream >= (1 << 27)) return fail(MPO_EINVAL, who + "sr_stream out of range");
+        // the message is built only on failure (this loop runs on every call, before the launch)
+        auto who = [i] { return "tensor " + std::to_string(i) + ": "; };
+        if (x.n < 0) return fail(MPO_EINVAL, who() + "negative size");
+        if (x.hp < 0 || x.hp >= nhp) return fail(MPO_EINVAL, who() + "hyper-parameter group index out of range");
+        if (x.sr_stream < 0 || x.sr_stream >= (1 << 27)) return fail(MPO_EINVAL, who() + "sr_stream out of range");
         if (x.n == 0) continue;
         const bool need_m = adam || (sgd && sgd[x.hp].momentum != 0.0);
         if (!x.value || !x.resid || !x.grad || (need_m && !x.m) || (adam && !x.v))
-            return fail(MPO_EINVAL, who + "NULL array");
+            return fail(MPO_EINVAL, who() + "NULL array");
         if (!aligned16(x.value) || !aligned16(x.resid) || !aligned16(x.grad) || (need_m && !aligned16(x.m)) ||
             (adam && !aligned16(x.v)))
-            return fail(MPO_EALIGN, who + "array base pointer not 16-byte aligned");
+            return fail(MPO_EALIGN, who() + "array base pointer not 16-byte aligned");
     }
     return MPO_OK;
 }
@@ -411,7 +412,7 @@ static mpo_status sgd_common(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t, 
                              int32_t nhp, double* norm_ws, bool one_hp, cudaStream_t s, bool sumsq_ready,
                              double* accum = nullptr) {
     HP<SgdK> k;
-    for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) k.g[i] = derive_sgd(hp[i < nhp ? i : 0]);
+    for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) k.g[i] = i < nhp ? derive_sgd(hp[i]) : k.g[0];
     const int skip = hp[0].skip_nonfinite != 0;
     if (skip && !sumsq_ready && !hp[0].norm_ready) {
         float gs[MPO_MAX_HP_GROUPS];
@@ -437,7 +438,7 @@ static mpo_status adam_common(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t,
                               int32_t nhp, double* norm_ws, bool one_hp, cudaStream_t s, bool sumsq_ready,
                               double* accum = nullptr) {
     HP<AdamK> k;
-    for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) k.g[i] = derive_adam(hp[i < nhp ? i : 0]);
+    for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) k.g[i] = i < nhp ? derive_adam(hp[i]) : k.g[0];
     const double max_norm = hp[0].max_grad_norm;
     const int skip = hp[0].skip_nonfinite != 0;
     const bool need = max_norm > 0.0 || skip;
