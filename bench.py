@@ -333,14 +333,29 @@ def multi_gpu_breakdown(wl, dist, steps, warmup, p2p=False):
     del rs_out, ag_out
     out["nccl_algo"] = os.environ.get("NCCL_ALGO", "auto (NCCL's choice; NCCL_DEBUG=INFO names it)")
     # the same step fused with its collectives over NVLink peer memory (mpo_p2p_sharded_step on
-    # torch symmetric memory, between symmetric-memory barriers), when the box provides it
-    # opt-in (--p2p): a symmetric-memory rendezvous that fails on some ranks only would hang the
-    # others, and the default run must always deliver its line
+    # torch symmetric memory, between symmetric-memory barriers) and over NVLS multicast, when the
+    # box provides them.  A symmetric-memory rendezvous that failed on some ranks only would hang
+    # the others, so every rank first checks what it can do locally (symmetric memory importable,
+    # peer access to every other local GPU) and the ranks agree (all_reduce MIN) before any
+    # rendezvous; --no-p2p skips it altogether
     if p2p and not wl.clip:
+        ok = 1
         try:
-            out["p2p_fused_step"] = _p2p_fused_timing(wl, dist, steps, warmup)
-        except Exception as ex:
-            out["p2p_fused_step"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+            import torch.distributed._symmetric_memory  # noqa: F401
+            me = torch.cuda.current_device()
+            ok = int(all(torch.cuda.can_device_access_peer(me, j) for j in range(torch.cuda.device_count())
+                         if j != me))
+        except Exception:
+            ok = 0
+        t = torch.tensor([ok], device="cuda", dtype=torch.int32)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if int(t.item()):
+            try:
+                out.update(_p2p_fused_timing(wl, dist, steps, warmup))
+            except Exception as ex:
+                out["p2p_fused_step"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+        else:
+            out["p2p_fused_step"] = {"skipped": "no symmetric memory / peer access on every rank"}
     return out
 
 
@@ -365,10 +380,37 @@ def _p2p_fused_timing(wl, dist, steps, warmup):
         hv.barrier(channel=0)
 
     ms, launches = timed(step, steps, warmup, dist)
-    res = {"ms_per_step": ms, "params_per_s": wl.P / (ms * 1e-3), "launches_per_step": launches / steps,
-           "nvlink_bytes_per_rank_per_step": 2 * 2 * L.shard * (N - 1),
-           "note": "one kernel per rank: P2P loads of every rank's grad shard (fp32 sum in rank order), "
-                   "update, P2P stores of the new values into every replica; + 2 symmetric-memory barriers"}
+    res = {"p2p_fused_step": {
+        "ms_per_step": ms, "params_per_s": wl.P / (ms * 1e-3), "launches_per_step": launches / steps,
+        "nvlink_bytes_per_rank_per_step": 2 * 2 * L.shard * (N - 1),
+        "nvlink_gbs_per_rank": 2 * 2 * L.shard * (N - 1) / (ms * 1e-3) / 1e9,
+        "note": "one kernel per rank: bulk copies of every rank's grad shard (fp32 sum in rank order), update, "
+                "P2P stores of the new values into every replica; + 2 symmetric-memory barriers"}}
+    # NVLS: the same buffers' multicast object, when every rank has one (all ranks agree first)
+    import torch
+    mc_v, mc_g = int(getattr(hv, "multicast_ptr", 0) or 0), int(getattr(hg, "multicast_ptr", 0) or 0)
+    t = torch.tensor([1 if (mc_v and mc_g and wl.scheme == "rne") else 0], device="cuda", dtype=torch.int32)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    if int(t.item()):
+        off_v, off_g = val.data_ptr() - int(hv.buffer_ptrs[r]), grd.data_ptr() - int(hg.buffer_ptrs[r])
+        vdt = api.format_code(wl.value.dtype)
+
+        def nvls():
+            wl.t += 1
+            hg.barrier(channel=0)
+            api.mpo_nvls_sharded_step(kind, r, N, vdt, mc_v + off_v, val.data_ptr(), mc_g + off_g, wl.resid, wl.m,
+                                      wl.v, L.total, wl.hp())
+            hv.barrier(channel=0)
+        try:
+            ms2, l2 = timed(nvls, steps, warmup, dist)
+            res["nvls_fused_step"] = {"ms_per_step": ms2, "params_per_s": wl.P / (ms2 * 1e-3),
+                                      "launches_per_step": l2 / steps,
+                                      "note": "multimem.ld_reduce of the grad shard (fp32 in-switch sum), update, "
+                                              "multimem.st of the values; + 2 symmetric-memory barriers"}
+        except Exception as ex:
+            res["nvls_fused_step"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+    else:
+        res["nvls_fused_step"] = {"skipped": "no multicast object on every rank (or a non-RNE scheme)"}
     del val, grd
     return res
 
@@ -917,8 +959,8 @@ def main():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=30)
-    ap.add_argument("--p2p", action="store_true",
-                    help="N>1 (or --mg-breakdown): also time the P2P fused sharded step on torch symmetric memory")
+    ap.add_argument("--no-p2p", action="store_true",
+                    help="N>1 (or --mg-breakdown): skip the P2P / NVLS fused sharded steps on torch symmetric memory")
     ap.add_argument("--mg-breakdown", action="store_true",
                     help="run the N>1 update/collective breakdown at world 1 too (code-path check)")
     args = ap.parse_args()
@@ -963,7 +1005,7 @@ def main():
                 import torch.distributed as tdist
                 wl.step(sharded=True)
                 dist = tdist
-            mg = multi_gpu_breakdown(wl, dist, args.steps, args.warmup, p2p=args.p2p)
+            mg = multi_gpu_breakdown(wl, dist, args.steps, args.warmup, p2p=not args.no_p2p)
             if world > 1:
                 # the step kernel's own launch time on the shard (the whole-step window also
                 # holds the NCCL collectives, reported with their NVLink fractions in multi_gpu)

@@ -57,6 +57,9 @@ if __name__ == "__main__":
         summ[wl] = {"kernel": st[0]["kernel"],
                     "dram_bytes_per_launch": sum(k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"] for k in st) / len(st),
                     "gpu_time_us_per_launch": sum(k["gpu__time_duration.sum"] for k in st) / len(st),
-                    "source": f"profiles/{tag}_ncu_full.json (ncu --set full, cache control all: cold L2 per replay)"}
+                    "source": (f"profiles/{tag}_ncu_full.json (ncu --set full, kernel replay, cache control all: "
+                               "cold L2 per replay)") if "smsp__issue_active.avg.pct_of_peak_sustained_active" in st[0]
+                    else (f"profiles/{tag}_ncu_full.json (ncu DRAM metrics only, application replay of the bench "
+                          "command, launch after the warm-up: no memory save/restore of the working set)")}
     with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as fh:
         json.dump(summ, fh, indent=1)
