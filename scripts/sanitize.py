@@ -46,5 +46,23 @@ for k in range(W2):
     api.mpo_p2p_sharded_step(MPO_ADAM, k, W2, [t.data_ptr() for t in reps], [t.data_ptr() for t in grads],
                              torch.zeros(S, dtype=torch.int16, device=dev), torch.zeros(S, device=dev),
                              torch.zeros(S, device=dev), n, mpo.AdamParams(lr=1e-3, step=1), torch.bfloat16)
+# round 2: the P2P step with an int8-residual format (16-element bulk granule + 8-element tail)
+# and SGD; a step spanning two gradient dtypes (mpo_grad_sumsq + norm_ready); the Python hooks
+from paper_2309_12381_b200._lib import MPO_SGD  # noqa: E402
+for k in range(W2):
+    S = n // W2
+    api.mpo_p2p_sharded_step(MPO_SGD, k, W2, [t.data_ptr() for t in reps], [t.data_ptr() for t in grads],
+                             torch.zeros(S, dtype=torch.int8, device=dev), torch.zeros(S, device=dev), None, n,
+                             mpo.SgdParams(lr=0.1, momentum=0.9), torch.bfloat16, scheme="x8")
+ps = [torch.nn.Parameter(torch.randn(m, device=dev) * 0.02) for m in (4100, 77)]
+o2 = mpo.ResidualAdamW(ps, lr=1e-3, fmt=torch.float16, max_grad_norm=0.05)
+ps[0].grad = (torch.randn(4100, device=dev) * 1e-2).to(torch.float16)
+ps[1].grad_dtype = None
+ps[1].grad = torch.randn(77, device=dev) * 1e-2
+o2.step()
+model2 = torch.nn.Sequential(torch.nn.Linear(32, 40), torch.nn.Linear(40, 8)).cuda()
+o3 = mpo.ResidualSGD(model2.parameters(), lr=0.1, momentum=0.9, fmt=torch.float16)
+o3.install_backward_hooks(native=False, batch_below=0)
+model2(torch.randn(4, 32, device=dev, dtype=torch.float16)).float().sum().backward()
 torch.cuda.synchronize()
 print("sanitize run ok")
