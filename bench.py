@@ -349,14 +349,57 @@ def multi_gpu_breakdown(wl, dist, steps, warmup, p2p=False):
             ok = 0
         t = torch.tensor([ok], device="cuda", dtype=torch.int32)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        if int(t.item()):
+        if not int(t.item()):
+            out["p2p_fused_step"] = {"skipped": "no symmetric memory / peer access on every rank"}
+        elif N > 1 or os.environ.get("MPO_BENCH_FUSED_CHILD") == "1":   # (the env: exercise it at N=1)
+            # in child processes (one per rank, their own process group): a device fault in a fused
+            # kernel on hardware this code has never run on then costs the child, not this line
+            out.update(_fused_in_children(wl, steps, warmup))
+        else:
             try:
                 out.update(_p2p_fused_timing(wl, dist, steps, warmup))
             except Exception as ex:
                 out["p2p_fused_step"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
-        else:
-            out["p2p_fused_step"] = {"skipped": "no symmetric memory / peer access on every rank"}
     return out
+
+
+def _fused_in_children(wl, steps, warmup, timeout_s=900):
+    """Every rank runs `bench.py --fused-child` (same workload, a fresh process group on
+    MASTER_PORT + 101) and reads its JSON line; an error or a timeout is reported, not raised."""
+    import torch
+    torch.cuda.empty_cache()                 # the children need the memory this process cached
+    env = dict(os.environ)
+    env["MASTER_PORT"] = str(int(os.environ.get("MASTER_PORT", "29500")) + 101)
+    env.pop("TORCHELASTIC_USE_AGENT_STORE", None)   # the child group hosts its own store
+    cmd = [sys.executable, os.path.abspath(__file__), "--fused-child", "--workload", wl.name, "--steps", str(steps),
+           "--warmup", str(warmup)]
+    try:
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout_s)
+        lines = [line for line in r.stdout.splitlines() if line.startswith("{")]
+        if lines:
+            return json.loads(lines[-1])
+        return {"p2p_fused_step": {"error": f"child rc={r.returncode}: {r.stderr[-300:]}"}}
+    except subprocess.TimeoutExpired:
+        return {"p2p_fused_step": {"error": f"child timed out after {timeout_s} s"}}
+
+
+def fused_child(args):
+    """--fused-child (started by _fused_in_children on every rank): the P2P and NVLS fused sharded
+    steps on this workload, one JSON line with their timings."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device(f"cuda:{local}"))
+    try:
+        wl = Workload(args.workload, world, rank)
+        res = _p2p_fused_timing(wl, dist, args.steps, args.warmup)
+    except Exception as ex:
+        res = {"p2p_fused_step": {"error": f"{type(ex).__name__}: {ex}"[:300]}}
+    emit(res)
+    dist.destroy_process_group()
 
 
 def _p2p_fused_timing(wl, dist, steps, warmup):
@@ -985,10 +1028,13 @@ def main():
                     help="N>1 (or --mg-breakdown): skip the P2P / NVLS fused sharded steps on torch symmetric memory")
     ap.add_argument("--mg-breakdown", action="store_true",
                     help="run the N>1 update/collective breakdown at world 1 too (code-path check)")
+    ap.add_argument("--fused-child", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)
+    if args.fused_child:
+        return fused_child(args)
 
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -428,6 +428,44 @@ def test_bucketed_hook_sharding_equals_two_phase(mpo, nccl1, kind):
     bk.remove_hooks()
 
 
+def test_bucketed_sr_streams_per_bucket(mpo, orc, nccl1):
+    """Stochastic rounding in the bucketed hook x sharding path: bucket b of rank r draws from stream
+    r + world*b (R18), so no two buckets of a step repeat the same draws.  World 1, fp16 SR,
+    Adam; the gradient of every parameter is a known constant (loss = sum(p * C_p)), so the oracle
+    can step each bucket of the flat buffers with its own stream: bit-exact."""
+    from paper_2309_12381_b200 import api
+    torch.manual_seed(12)
+    shapes = [(40, 24), (24,), (24, 48), (48,), (300,)]
+    ps = [nn.Parameter(torch.randn(s, device="cuda") * 0.05) for s in shapes]
+    w0 = [p.detach().clone() for p in ps]
+    C = [(torch.randn(s, device="cuda") * 1e-2).to(torch.float16) for s in shapes]
+    hp = mpo.AdamParams(lr=1e-3, weight_decay=0.0)
+    bk = mpo.BucketedShardedOptimizer(ps, kind="adam", fmt=torch.float16, hp=hp, bucket_elems=1024, scheme="sr",
+                                      seed=5, exact=True)
+    L = bk.layout
+    assert len(L.buckets) > 1
+    sum(((p * c).float().sum() for p, c in zip(ps, C))).backward()
+    bk.wait()
+    torch.cuda.synchronize()
+    # oracle: the same flat fp32 source split with stream 0, then each bucket stepped with stream b
+    src = np.zeros(L.total, np.float32)
+    g = np.zeros(L.total, np.uint16)
+    for w, c, o in zip(w0, C, L.offsets):
+        src[o:o + w.numel()] = w.reshape(-1).cpu().numpy()
+        g[o:o + c.numel()] = c.reshape(-1).view(torch.int16).cpu().numpy().view(np.uint16)
+    h, r = orc.split_s("sr", "fp16", src, seed=api.step_seed(5, 0), stream=0)
+    for b, (o, length, _) in enumerate(L.buckets):
+        sl = slice(o, o + length)
+        hh, rr = h[sl].copy(), r[sl].copy()
+        m = np.zeros(length, np.float32); v = np.zeros(length, np.float32)
+        orc.adam_step_s("sr", "fp16", "fp16", hh, rr, g[sl].copy(), m, v, lr=1e-3, weight_decay=0.0, step=1,
+                        seed=api.step_seed(5, 1), stream=b)
+        assert np.array_equal(bk.value[sl].view(torch.int16).cpu().numpy().view(np.uint16), hh), b
+        po = L.part_offsets[b]
+        assert np.array_equal(bk.resid[po:po + length].cpu().numpy(), rr), b
+    bk.remove_hooks()
+
+
 def _cudart():
     import ctypes
     import glob
