@@ -15,6 +15,7 @@ Everything numeric runs in libmpo (api.py marshals arguments only).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import weakref
 from typing import Iterable, Optional
 
@@ -201,7 +202,6 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             self._hp_c = {}
         if self._native is not None:
             self._native.resolve()
-            self._push_native_steps()
             for gi in range(len(self.param_groups)):
                 self._push_group(gi)
 
@@ -222,7 +222,6 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             return
         params, host, ev = chk
         ev.synchronize()
-        import math
         bad = [not math.isfinite(x) for x in host.tolist()]
         if len(bad) == 1:
             bad = bad * len(params)
@@ -286,9 +285,6 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             self._launch(tab, hps)
         if self.skip_nonfinite:
             self._queue_skip_check(params, self._ws(params[0].device)[:1])
-        if self._native is not None:
-            self._resolve_skips()
-            self._push_native_steps()
         return None
 
     def _needs_norm(self):
@@ -390,8 +386,6 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         if self._native is not None:
             self._native.resolve()
 
-    def _push_native_steps(self):
-        pass
 
     def native_hook_calls(self) -> int:
         """Library calls the native hooks made so far (per-parameter steps + batched flushes)."""

@@ -121,6 +121,39 @@ def test_native_hooks_follow_lr_changes_and_uninstall(mpo):
     assert all(p.grad is not None for p in b.parameters())
 
 
+@pytest.mark.parametrize("kind", ["adam", "sgd"])
+def test_native_hooks_param_groups(mpo, kind):
+    """Two param groups with different hyper-parameters (no decay on 1-D tensors, a different lr):
+    the native hooks pick each parameter's group struct; == two-phase bitwise; installing twice is
+    refused."""
+    torch.manual_seed(3)
+    a, b = TinyLM().cuda(), TinyLM().cuda()
+    b.load_state_dict(a.state_dict())
+
+    def groups(m):
+        dec = [p for p in m.parameters() if p.dim() > 1]
+        nod = [p for p in m.parameters() if p.dim() <= 1]
+        if kind == "adam":
+            return [{"params": dec, "weight_decay": 0.1}, {"params": nod, "weight_decay": 0.0, "lr": 3e-3}]
+        return [{"params": dec, "weight_decay": 1e-4}, {"params": nod, "weight_decay": 0.0, "lr": 0.2}]
+    mk = (lambda m: mpo.ResidualAdamW(groups(m), lr=1e-3, fmt=torch.bfloat16)) if kind == "adam" else \
+        (lambda m: mpo.ResidualSGD(groups(m), lr=0.1, momentum=0.9, fmt=torch.bfloat16))
+    oa, ob = mk(a), mk(b)
+    ob.install_backward_hooks()
+    with pytest.raises(mpo.MpoError):
+        ob.install_backward_hooks()
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    for _ in range(3):
+        idx = torch.randint(0, 257, (4, 33), device="cuda", generator=gen)
+        _loss(a, idx).backward()
+        oa.step()
+        for p in a.parameters():
+            p.grad = None
+        _loss(b, idx).backward()
+    for pa, pb in zip(a.parameters(), b.parameters()):
+        assert torch.equal(pa.view(torch.int16), pb.view(torch.int16))
+
+
 def test_hook_mode_refuses_clipping(mpo):
     a = TinyLM().cuda()
     opt = mpo.ResidualAdamW(a.parameters(), fmt=torch.bfloat16, max_grad_norm=1.0)
