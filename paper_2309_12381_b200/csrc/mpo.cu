@@ -817,19 +817,31 @@ MPO_API mpo_status mpo_nvls_alloc_local(int64_t bytes, void** uc_ptr, void** mc_
     CUresult last = CUDA_ERROR_UNKNOWN;
     size_t size = 0;
     unsigned long long chosen = 0;
+    std::string tried;
+    const CUmulticastGranularity_flags grans[2] = {CU_MULTICAST_GRANULARITY_MINIMUM, CU_MULTICAST_GRANULARITY_RECOMMENDED};
     for (unsigned long long hk : kinds) {
-        mp.handleTypes = hk;
-        mp.size = size_t(bytes);
-        if (pGran(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS) continue;
-        size = (size_t(bytes) + gran - 1) / gran * gran;
-        mp.size = size;
-        last = pMcCreate(&a.mc, &mp);
-        if (last == CUDA_SUCCESS) {
-            chosen = hk;
-            break;
+        for (CUmulticastGranularity_flags gf : grans) {
+            mp.handleTypes = hk;
+            mp.size = size_t(bytes);
+            const CUresult gr = pGran(&gran, &mp, gf);
+            if (gr != CUDA_SUCCESS) {
+                tried += " [handle " + std::to_string(hk) + " gran " + std::to_string(int(gf)) + ": granularity " +
+                         std::to_string(int(gr)) + "]";
+                continue;
+            }
+            size = (size_t(bytes) + gran - 1) / gran * gran;
+            mp.size = size;
+            last = pMcCreate(&a.mc, &mp);
+            tried += " [handle " + std::to_string(hk) + " gran " + std::to_string(gran) + ": create " +
+                     std::to_string(int(last)) + "]";
+            if (last == CUDA_SUCCESS) {
+                chosen = hk;
+                break;
+            }
         }
+        if (last == CUDA_SUCCESS) break;
     }
-    if (last != CUDA_SUCCESS) return fail(MPO_ECUDA, "cuMulticastCreate failed: CUresult " + std::to_string(int(last)));
+    if (last != CUDA_SUCCESS) return fail(MPO_ECUDA, "cuMulticastCreate failed:" + tried);
     a.size = size;
     MPO_CU(pMcAdd(a.mc, dev), "cuMulticastAddDevice");
     CUmemAllocationProp ap = {};
