@@ -94,14 +94,16 @@ int num_sms() {
     return sms;
 }
 
-// Kernel variant: "tma" (default, bulk-copy pipeline) or "lsu" (per-thread 128-bit loads; built
-// only with -DMPO_WITH_LSU), chosen once per process from MPO_STEP_KERNEL (A/B evidence).
-bool use_tma() {
-    static const bool tma = [] {
-        const char* e = std::getenv("MPO_STEP_KERNEL");
-        return !(e && std::strcmp(e, "lsu") == 0);
-    }();
-    return tma;
+// Step-kernel choice per launch: the bulk-copy pipeline (step_tma_kernel) for large launches, the
+// per-thread-load kernel (step_kernel) for launches of at most kLsuMaxTiles tiles, where the
+// pipeline's fill and its one-CTA-per-SM grid dominate (device-only, single tensor: 2^20 elements
+// 5.7 vs 6.8 us, 2^21 8.9 vs 10.6 us, equal at 2^22, TMA ahead from 2^23; profiles/r02_small_launch_graph.log).
+// MPO_STEP_KERNEL=tma|lsu forces one (tests cover both; read at every launch).
+int step_kernel_choice() {
+    const char* e = std::getenv("MPO_STEP_KERNEL");
+    if (e && std::strcmp(e, "lsu") == 0) return 1;
+    if (e && std::strcmp(e, "tma") == 0) return 0;
+    return -1;
 }
 
 bool finite(double x) { return std::isfinite(x); }

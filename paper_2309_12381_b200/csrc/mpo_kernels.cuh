@@ -40,9 +40,8 @@ constexpr int kThreads = 256;
 constexpr int kUnitEl = 8;                          // elements per unit (128-bit of 16-bit data)
 constexpr int64_t kTileEl = int64_t(MPO_CW) * 32 * kUnitEl;   // 4096 elements: one unit per consumer thread
 constexpr int kUnroll = int(kTileEl / (kThreads * kUnitEl));  // LSU kernel: units per thread per tile
-#ifdef MPO_WITH_LSU
 static_assert(kUnroll >= 1 && kTileEl % (kThreads * kUnitEl) == 0, "LSU kernel needs whole 2048-element passes");
-#endif
+constexpr int64_t kLsuMaxTiles = 640;   // launches of at most this many tiles use step_kernel (auto)
 constexpr int kNormBlocksMax = 2048;                // partial sums of the norm pre-pass
 constexpr int kBigT = 512;    // 512 x 56 B + 16 groups fits the 32 KB kernel-parameter limit
 constexpr int kMidT = 32;
@@ -95,7 +94,7 @@ extern std::atomic<int64_t> g_launches;
 mpo_status fail(mpo_status s, const std::string& msg);
 mpo_status check_launch(const char* what);
 int num_sms();
-bool use_tma();
+int step_kernel_choice();
 
 inline int64_t grid_for(int64_t work_items, int per_sm) {
     int64_t cap = int64_t(num_sms()) * per_sm;
@@ -641,7 +640,9 @@ __device__ __forceinline__ void store_unit(const KT& T, int64_t e, const uint4& 
     }
 }
 
-// ---- variant A ("lsu"): every thread loads its own units with 128-bit LDG, computes, stores ----
+// ---- variant A ("lsu"): every thread loads its own units with 128-bit LDG, computes, stores.  The
+// default for small launches (<= kLsuMaxTiles tiles: hook mode's per-parameter steps, config C1),
+// where a grid of several CTAs per SM with every load in flight at once beats the pipeline's fill.
 template <int MAXT, int SF, int G, class Op, bool CLIP>
 __global__ void __launch_bounds__(kThreads) step_kernel(const __grid_constant__ Table<MAXT> tab,
                                                         const __grid_constant__ HP<typename Op::K> hp,
@@ -651,7 +652,7 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const __grid_constant__ 
     if (skip && !isfinite(sumsq[0])) return;   // loss-scaling found-inf: no update at all
     float coef = 1.0f;
     if constexpr (CLIP) coef = clip_coef(sumsq, max_norm);
-    int cur = 0;
+    int cur = first_tensor(tab, int(blockIdx.x));   // not a dependent walk from tensor 0
     for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
         while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
         const KT& T = tab.t[cur];
@@ -1524,8 +1525,8 @@ mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typen
     const int64_t tiles = fill_table(tab, t, lo, hi, one_hp);
     if (tiles == 0) return MPO_OK;
     if (tiles > INT32_MAX) return fail(MPO_EINVAL, "table slice too large");
-#ifdef MPO_WITH_LSU
-    if (!use_tma()) {
+    const int choice = step_kernel_choice();
+    if (choice == 1 || (choice < 0 && tiles <= kLsuMaxTiles)) {
         auto kern = step_kernel<MAXT, SF, G, Op, CLIP>;
         static int per_sm = resident_blocks(kern);
         const int64_t grid = grid_for(tiles, per_sm);
@@ -1533,7 +1534,6 @@ mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typen
         ++g_launches;
         return check_launch("step_kernel");
     }
-#endif
     const int64_t grid = grid_for(tiles, MPO_CTAS_PER_SM);
     auto kern = step_tma_kernel<MAXT, SF, G, Op, CLIP>;
     constexpr int SB = stage_bytes<Fmt<SF>::rbytes, G, Op::kHasV>();

@@ -18,3 +18,11 @@ def orc():
     oracle.build()
     assert oracle.fpenv_ok(), "FTZ/DAZ set in this process: subnormal pins would be meaningless"
     return oracle
+
+
+@pytest.fixture(params=["tma", "lsu"])
+def step_kernel(request, monkeypatch):
+    """Run a GPU parity test through both step kernels: the bulk-copy pipeline and the per-thread
+    load kernel (the library picks by launch size; MPO_STEP_KERNEL forces one, read per launch)."""
+    monkeypatch.setenv("MPO_STEP_KERNEL", request.param)
+    return request.param

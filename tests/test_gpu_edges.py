@@ -105,7 +105,7 @@ def _hps(mpo, kind, t, seed):
 @pytest.mark.parametrize("scheme,fmt", FORMATS)
 @pytest.mark.parametrize("kind", KINDS)
 @pytest.mark.parametrize("gsame", [True, False])
-def test_edge_steps_bit_exact(mpo, orc, scheme, fmt, kind, gsame):
+def test_edge_steps_bit_exact(mpo, orc, scheme, fmt, kind, gsame, step_kernel):
     gf = fmt if gsame else "fp32"
     hs, rs, gs, ms, vs = [], [], [], [], []
     for shift in range(3):

@@ -148,7 +148,7 @@ def _adam_hp_kw(hp):
 
 @pytest.mark.parametrize("fmt,wd,adamw", [("fp16", 0.0, False), ("fp16", 0.01, True), ("bf16", 0.01, True),
                                           ("bf16", 0.01, False)])
-def test_adam_c1_bit_exact_100_steps(mpo, orc, fmt, wd, adamw):
+def test_adam_c1_bit_exact_100_steps(mpo, orc, fmt, wd, adamw, step_kernel):
     """configs[0]: 1M-param flat tensor, Adam, 100 steps, every step bit-exact (exact build)."""
     n, steps = 1 << 20, 100 if fmt == "fp16" and not adamw else 30
     h, r, m, v = _adam_case(mpo, fmt, fmt, n, 0xB0B)
@@ -251,7 +251,7 @@ RAGGED = [0, 1, 7, 8, 9, 64, 4095, 4096, 4097, 12345, 65539, 3]
 @pytest.mark.parametrize("fmt", ["fp16", "bf16"])
 @pytest.mark.parametrize("gfmt", ["same", "fp32", "other"])
 @pytest.mark.parametrize("kind", ["adam", "sgd"])
-def test_multi_tensor_ragged_bit_exact(mpo, orc, fmt, gfmt, kind):
+def test_multi_tensor_ragged_bit_exact(mpo, orc, fmt, gfmt, kind, step_kernel):
     gf = fmt if gfmt == "same" else ("fp32" if gfmt == "fp32" else ("bf16" if fmt == "fp16" else "fp16"))
     sizes = RAGGED
     hs, rs, gs, ms, vs = [], [], [], [], []
@@ -326,7 +326,7 @@ def test_multi_tensor_equals_per_tensor(mpo):
 # Global-norm clipping (config C5 reading R9)
 # ------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("target_norm", [4.0, 0.5])
-def test_clip_sumsq_and_hybrid_step(mpo, orc, target_norm):
+def test_clip_sumsq_and_hybrid_step(mpo, orc, target_norm, step_kernel):
     fmt = "fp16"
     sizes = [1024 * 197 + 5, 3 * 1024 * 1024, 1024, 4096 * 1024 + 3]
     hs, rs, gs, ms, vs = [], [], [], [], []
@@ -470,7 +470,7 @@ def test_fast_sqrt_div_match_ieee(mpo, exact):
     assert sq_fast > (1 << 30) and div_fast > (1 << 29)
 
 
-def test_table_larger_than_one_launch(mpo, orc):
+def test_table_larger_than_one_launch(mpo, orc, step_kernel):
     """A table of 1100 tensors spans three launches (<= 512 entries each); every tensor bit-exact,
     including empty and single-element ones (exact build)."""
     fmt = "bf16"

@@ -78,7 +78,7 @@ def _kw(hp):
 @pytest.mark.parametrize("scheme,fmt", VARIANTS)
 @pytest.mark.parametrize("kind", ["adam", "sgd"])
 @pytest.mark.parametrize("gsame", [True, False])
-def test_variant_steps_bit_exact(mpo, orc, scheme, fmt, kind, gsame):
+def test_variant_steps_bit_exact(mpo, orc, scheme, fmt, kind, gsame, step_kernel):
     gf = fmt if gsame else "fp32"
     hs, rs, ms, vs = [], [], [], []
     for i, n in enumerate(SIZES):
@@ -150,7 +150,7 @@ def test_sr_hook_mode_equals_multi_tensor(mpo):
 
 
 @pytest.mark.parametrize("scheme,fmt,kind", [("rne", "bf16", "adam"), ("x8", "fp16", "sgd"), ("rne", "fp16", "sgd")])
-def test_schedule_many_tensors_with_guards(mpo, orc, scheme, fmt, kind):
+def test_schedule_many_tensors_with_guards(mpo, orc, scheme, fmt, kind, step_kernel):
     """The step kernel's schedule (tiles dealt round-robin to the CTAs, each
     stage's piece published by the producer warp): 400 tensors of mixed sizes (empty, tiny,
     ragged, several tiles) over every CTA, more tiles than one wave, tails of the int8 residual's
