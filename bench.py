@@ -563,19 +563,31 @@ def e2e_measure(wl, steps, dist=None):
             comp.wait_stream(cin)
         h2d = d2h = L.total * 2
     else:
+        # data parallel: every rank's backward hands over its full 16-bit gradient (H2D of all of it)
+        # and the step's result is this rank's shard of the new values (D2H of 1/N; after the
+        # all-gather every replica holds the same values).  Pinned host memory per rank: grads + shard.
         L = wl.layout
+        lo, hi = L.shard_range(wl.rank)
+        need = (L.total + (hi - lo)) * 2 * int(os.environ.get("LOCAL_WORLD_SIZE", wl.world))
+        avail = _mem_available()
+        ok = torch.tensor([0 if (avail is not None and need > 0.7 * avail) else 1], device=dev, dtype=torch.int32)
+        if dist is not None:
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)      # every rank measures or none does
+        if not int(ok.item()):
+            return {"skipped": f"host memory: {need / 1e9:.0f} GB of pinned buffers over the local ranks > 70 % "
+                               f"of MemAvailable {(avail or 0) / 1e9:.0f} GB on some rank"}
         host = torch.empty(L.total, dtype=wl.tdt, pin_memory=True)
         tmp = torch.empty(L.total, dtype=wl.tdt, device=dev)
         torch_normal_(tmp, 1e-3 if wl.kind == "adam" else 1e-2, 0xB0B, 7000 + wl.rank)
         host.copy_(tmp)
         del tmp
-        out = torch.empty(L.total, dtype=wl.tdt, pin_memory=True)
+        out = torch.empty(hi - lo, dtype=wl.tdt, pin_memory=True)
 
         def step():
             wl.grad.copy_(host, non_blocking=True)
             wl.step()
-            out.copy_(wl.value, non_blocking=True)
-        h2d = d2h = L.total * 2
+            out.copy_(wl.value[lo:hi], non_blocking=True)
+        h2d, d2h = L.total * 2, (hi - lo) * 2
     if wl.world == 1:
         def step_and_drain():
             step()
@@ -652,6 +664,17 @@ def cpu_baseline(name, budget_s=10.0):
             "cpu": cpu_model(), "host_cores": len(os.sched_getaffinity(0)),
             "sample": allc["sample"] + f"; OpenMP build, {allc['threads']} threads",
             "threads_1": one, "threads_all": allc}
+
+
+def _mem_available():
+    """Bytes of MemAvailable in /proc/meminfo (None if unreadable)."""
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
 
 
 def cpu_model() -> str:

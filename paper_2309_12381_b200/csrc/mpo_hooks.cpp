@@ -22,6 +22,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -107,6 +108,7 @@ class HookState : public std::enable_shared_from_this<HookState> {
     // skip_nonfinite: roll back the step counts of the parameters whose update the last backward
     // skipped (their S reached the host through the copy queued at its end)
     void resolve() {
+        std::lock_guard<std::recursive_mutex> lk(mu_);
         if (!check_pending_) return;
         check_pending_ = false;
         if (cudaEventSynchronize(ev_) != cudaSuccess) throw std::runtime_error("mpo hook: cudaEventSynchronize failed");
@@ -115,6 +117,8 @@ class HookState : public std::enable_shared_from_this<HookState> {
     }
 
     void on_grad(int idx, const at::Tensor& t) {
+        // parameters on several devices: the engine may run their hooks from several device threads
+        std::lock_guard<std::recursive_mutex> lk(mu_);
         if (!alive_) return;
         at::Tensor& g = t.mutable_grad();
         if (!g.defined()) return;
@@ -158,6 +162,7 @@ class HookState : public std::enable_shared_from_this<HookState> {
     }
 
     void flush(bool final) {
+        std::lock_guard<std::recursive_mutex> lk(mu_);
         if (final) flush_queued_ = false;
         if (!pending_.empty()) launch_pending();
         if (final && hook_S_ && alive_) {
@@ -240,6 +245,7 @@ class HookState : public std::enable_shared_from_this<HookState> {
         // the gradients are released here (stream order keeps their reuse safe)
     }
 
+    std::recursive_mutex mu_;   // on_grad -> flush / resolve re-enter it on the same thread
     int kind_;
     uint64_t seed_;
     int64_t batch_below_, flush_elems_;
