@@ -512,10 +512,13 @@ def _windows(sizes, per_tensor=2, width=4104, seed=7):
     return out
 
 
-def test_llama7b_sharded_world1_sampled(mpo, orc):
-    """configs[3] at N=1 in the bench's launch configuration: the LLaMA-7B parameter set (6.74e9
-    params) as one flat bf16 buffer through mpo_sharded_step (world 1); sampled windows (every
-    tensor's head and tail + random interior) bit-exact against the oracle (exact build)."""
+def test_llama7b_full_size_sampled(mpo, orc):
+    """configs[3] at N=1 at full size: the LLaMA-7B parameter set (6.74e9 params, 291 tensors) in the
+    bench's own buffers.  Steps 1 and 2 go through exactly the call bench.py times (Workload.step:
+    one mpo_adam_step over the 291-tensor table -- the headline launch), step 3 through
+    mpo_sharded_step at world 1 on the flat buffer; after every step sampled windows (every tensor's
+    head and tail + random interior) are bit-exact against the oracle stepped from the same inputs
+    (exact build, the library's default)."""
     import bench
     if torch.cuda.get_device_properties(0).total_memory < 150e9:
         pytest.skip("needs a B200-class device (~100 GB)")
@@ -523,33 +526,47 @@ def test_llama7b_sharded_world1_sampled(mpo, orc):
     try:
         L = wl.layout
         offs = L.offsets
+        cum = np.cumsum([0] + wl.sizes)
         wins = []
         for (a, b) in _windows(wl.sizes):
             # map flat (unpadded) windows to the padded layout offsets of the owning tensor
-            i = int(np.searchsorted(np.cumsum([0] + wl.sizes), a, side="right") - 1)
-            base = int(np.cumsum([0] + wl.sizes)[i])
-            wins.append((offs[i] + a - base, offs[i] + b - base))
+            i = int(np.searchsorted(cum, a, side="right") - 1)
+            wins.append((offs[i] + a - int(cum[i]), offs[i] + b - int(cum[i])))
         take = lambda t, a, b: t[a:b].detach().cpu().numpy()
-        pre = [(take(wl.value.view(torch.int16), a, b).view(np.uint16), take(wl.resid, a, b), take(wl.grad.view(torch.int16), a, b).view(np.uint16),
-                take(wl.m, a, b), take(wl.v, a, b)) for a, b in wins]
+
+        def snap():
+            return [(take(wl.value.view(torch.int16), a, b).view(np.uint16), take(wl.resid, a, b),
+                     take(wl.grad.view(torch.int16), a, b).view(np.uint16), take(wl.m, a, b), take(wl.v, a, b))
+                    for a, b in wins]
+
+        def check(pre, hp, what):
+            for (a, b), (h, r, g, m, v) in zip(wins, pre):
+                orc.adam_step("bf16", "bf16", h, r, g, m, v, **_adam_hp_kw(hp))
+                assert np.array_equal(take(wl.value.view(torch.int16), a, b).view(np.uint16), h), (what, a, b)
+                assert np.array_equal(take(wl.resid, a, b), r), (what, a, b)
+                assert same_bits_nan_equal(take(wl.m, a, b), m) and same_bits_nan_equal(take(wl.v, a, b), v), what
+
+        for step in (1, 2):                         # the bench's headline call, from zero and nonzero state
+            pre = snap()
+            n0 = mpo.api.launch_count(exact=True)
+            wl.step()
+            torch.cuda.synchronize()
+            assert mpo.api.launch_count(exact=True) - n0 == 1          # one launch per step
+            check(pre, wl.hp(), f"multi-tensor step {step}")
         from paper_2309_12381_b200._lib import MPO_ADAM
-        wl.t = 1
-        hp = wl.hp()
         import torch.distributed as tdist
-        # one step through the exact build, same call bench.py times
         from paper_2309_12381_b200.sharded import nccl_comm_ptr
         if not tdist.is_initialized():
             import socket
             sk = socket.socket(); sk.bind(("127.0.0.1", 0))
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1"); os.environ["MASTER_PORT"] = str(sk.getsockname()[1]); sk.close()
             tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+        pre = snap()
+        wl.t += 1
+        hp = wl.hp()
         mpo.mpo_sharded_step(MPO_ADAM, nccl_comm_ptr(), 0, 1, wl.value, wl.grad, wl.resid, wl.m, wl.v, hp, exact=True)
         torch.cuda.synchronize()
-        for (a, b), (h, r, g, m, v) in zip(wins, pre):
-            orc.adam_step("bf16", "bf16", h, r, g, m, v, **_adam_hp_kw(hp))
-            assert np.array_equal(take(wl.value.view(torch.int16), a, b).view(np.uint16), h), (a, b)
-            assert np.array_equal(take(wl.resid, a, b), r), (a, b)
-            assert same_bits_nan_equal(take(wl.m, a, b), m) and same_bits_nan_equal(take(wl.v, a, b), v)
+        check(pre, hp, "sharded world 1, step 3")
     finally:
         del wl
         torch.cuda.empty_cache()
