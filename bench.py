@@ -785,6 +785,30 @@ def _secondary_one(name, steps, warmup, hbm_peak, scheme="rne"):
         return res
 
 
+def split_reconstruct_secondary(hbm_peak, n=1 << 28, steps=50, warmup=5):
+    """a1 / a2 (one-off conversions): mpo_split of n fp32 weights into bf16 value + int16
+    residual and mpo_reconstruct back, 8 B/param each (read 4 + write 2 + 2, read 2 + 2 + write 4)."""
+    import torch
+    import paper_2309_12381_b200 as mpo
+    w = torch.randn(n, device="cuda") * 0.02
+    v = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    r = torch.empty(n, dtype=torch.int16, device="cuda")
+    out = torch.empty(n, device="cuda")
+    res = {}
+    for name, fn in (("split", lambda: mpo.mpo_split(w, torch.bfloat16, value=v, resid=r)),
+                     ("reconstruct", lambda: mpo.mpo_reconstruct(v, r, out=out))):
+        ms, launches = timed(fn, steps, warmup)
+        gbs = 8 * n / (ms * 1e-3) / 1e9
+        res[name] = {"params_per_s": n / (ms * 1e-3), "ms": ms, "gbs": gbs, "frac_of_measured_hbm": gbs / hbm_peak,
+                     "launches": launches / steps}
+    # the round trip is exact except on bf16's RNE upper ties (R3: 1 binary32 ulp low, ~2^-17 of them)
+    res["round_trip_inexact_fraction"] = float((out != w).float().mean().item())
+    res["config"] = f"{n} fp32 weights N(0, 0.02), bf16 value + int16 residual, 8 B/param each way"
+    del w, v, r, out
+    torch.cuda.empty_cache()
+    return res
+
+
 def flat1m_secondary(hbm_peak, steps=100, warmup=10):
     """BASELINE configs[0]: one flat 2^20-param fp16 + residual tensor, Adam, 100 steps per
     measurement.  Its 27 MB per step fits the 126 MB L2 and one launch is a few microseconds, so
@@ -1144,6 +1168,10 @@ def main():
             line["secondary"]["flat1m_adam"] = flat1m_secondary(hbm_peak)
         except Exception as ex:
             line["secondary"]["flat1m_adam"] = {"error": f"{type(ex).__name__}: {ex}"}
+        try:
+            line["secondary"]["split_reconstruct"] = split_reconstruct_secondary(hbm_peak)
+        except Exception as ex:
+            line["secondary"]["split_reconstruct"] = {"error": f"{type(ex).__name__}: {ex}"}
         for sch in ("rtz", "sr", "x8"):    # paper variants of the storage scheme, GPT-2 AdamW set
             name = "gpt2_adamw"
             fmt_ok = sch != "sr" or WORKLOADS[name][1] == "fp16"
