@@ -231,8 +231,8 @@ mpo_status mpo_fused_backward_hook_step(mpo_optim kind, mpo_dtype vdt, mpo_dtype
  *   hp          : mpo_sgd_hp* | mpo_adam_hp* (HOST); grad_scale should be 1/world for a mean
  *   norm_ws     : as for mpo_adam_step (clipping: the shard sums are all-reduced in fp64)
  * Sequence on `stream`: ncclReduceScatter(sum) -> [sumsq + ncclAllReduce] -> step on the shard
- * -> ncclAllGather of the 16-bit values only (world 1: the collectives are identities and are
- * skipped).  The shard's stochastic-rounding stream is its rank. */
+ * -> ncclAllGather of the 16-bit values only (in place; at world 1 NCCL's single-rank path makes
+ * them no-ops, but they are still issued).  The shard's stochastic-rounding stream is its rank. */
 mpo_status mpo_sharded_step(mpo_optim kind, uintptr_t nccl_comm, int32_t rank, int32_t world,
                             mpo_dtype vdt, void* value_flat, void* grad_flat,
                             void* resid_shard, float* m_shard, float* v_shard,

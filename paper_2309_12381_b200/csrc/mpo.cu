@@ -598,10 +598,10 @@ static mpo_status sharded_common(mpo_optim kind, uintptr_t nccl_comm, int32_t ra
     // a communicator that already failed asynchronously is reported instead of hanging
     if ((st = comm_status(comm)) != MPO_OK) return st;
     void* grad_shard = static_cast<uint16_t*>(grad_flat) + rank * shard;
-    // 1. reduce-scatter of the 16-bit gradients (sum), in place: shard `rank` of grad_flat
-    //    (world 1: the reduction of one rank is the identity and the in-place shard is the buffer)
-    if (world > 1)
-        MPO_NCCL(ncclReduceScatter(grad_flat, grad_shard, size_t(shard), nccl_dtype(vdt), ncclSum, comm, s));
+    // 1. reduce-scatter of the 16-bit gradients (sum), in place: shard `rank` of grad_flat.  Issued
+    //    at world 1 too: NCCL's single-rank path makes an in-place collective a no-op, and the call
+    //    (arguments, communicator, stream) then runs on every one-GPU test
+    MPO_NCCL(ncclReduceScatter(grad_flat, grad_shard, size_t(shard), nccl_dtype(vdt), ncclSum, comm, s));
     // 2. residual-compensated update of this rank's pieces
     //    (clipping / found-inf: the shard's sum of squares, all-reduced so every rank agrees)
     const bool need = kind == MPO_ADAM ? (static_cast<const mpo_adam_hp*>(hp)->max_grad_norm > 0.0 ||
@@ -613,7 +613,7 @@ static mpo_status sharded_common(mpo_optim kind, uintptr_t nccl_comm, int32_t ra
             gs[i] = float(kind == MPO_ADAM ? static_cast<const mpo_adam_hp*>(hp)[i].grad_scale
                                            : static_cast<const mpo_sgd_hp*>(hp)[i].grad_scale);
         if ((st = prepass(gdt, tab.data(), nseg, gs, nhp, norm_ws, s)) != MPO_OK) return st;
-        if (world > 1) MPO_NCCL(ncclAllReduce(norm_ws, norm_ws, 1, ncclFloat64, ncclSum, comm, s));
+        MPO_NCCL(ncclAllReduce(norm_ws, norm_ws, 1, ncclFloat64, ncclSum, comm, s));
     }
     if (kind == MPO_ADAM) {
         const mpo_adam_hp* h = static_cast<const mpo_adam_hp*>(hp);
@@ -622,10 +622,9 @@ static mpo_status sharded_common(mpo_optim kind, uintptr_t nccl_comm, int32_t ra
         const mpo_sgd_hp* h = static_cast<const mpo_sgd_hp*>(hp);
         if ((st = sgd_common(vdt, gdt, tab.data(), nseg, h, nhp, norm_ws, false, s, true)) != MPO_OK) return st;
     }
-    // 3. all-gather of the 16-bit values only (residual and state never move)
-    if (world > 1)
-        MPO_NCCL(ncclAllGather(static_cast<uint16_t*>(value_flat) + rank * shard, value_flat, size_t(shard),
-                               nccl_dtype(vdt), comm, s));
+    // 3. all-gather of the 16-bit values only (residual and state never move); in place
+    MPO_NCCL(ncclAllGather(static_cast<uint16_t*>(value_flat) + rank * shard, value_flat, size_t(shard),
+                           nccl_dtype(vdt), comm, s));
     return MPO_OK;
 }
 
