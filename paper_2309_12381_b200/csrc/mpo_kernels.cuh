@@ -154,6 +154,14 @@ __device__ __forceinline__ void stf8(float* p, const float (&x)[8]) {
     stf(p + 4, make_float4(x[4], x[5], x[6], x[7]));
 }
 
+// 256-bit global store of 8 fp32 (sm_100: st.global.v8.f32): one thread covers a whole 32-B
+// sector, so a warp's store is 1 KB contiguous instead of two half-sector passes.
+__device__ __forceinline__ void st8f(float* p, const float (&x)[8]) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(x[0]), "f"(x[1]), "f"(x[2]),
+                 "f"(x[3]), "f"(x[4]), "f"(x[5]), "f"(x[6]), "f"(x[7])
+                 : "memory");
+}
+
 // 8 gradient values of a unit.
 template <int G>
 struct GradUnit {
@@ -299,6 +307,7 @@ __global__ void __launch_bounds__(kThreads) split_kernel(const float* __restrict
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < nunits; u += stride) {
         const int64_t e = u * kUnitEl;
+        // (256-bit loads here: +3 % at 2^24 elements, -1.2 % at 2^28; profiles/r02_ab_conv.log)
         const float4 x0 = ldf(w + e), x1 = ldf(w + e + 4);
         const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
         uint32_t hv[4];
@@ -344,7 +353,9 @@ __global__ void __launch_bounds__(kThreads) reconstruct_kernel(const uint16_t* _
         float o[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) o[k] = reconstruct1_s<SF>((k & 1) ? hi16(h[k >> 1]) : lo16(h[k >> 1]), code_at<SF>(rv, k));
-        stf8(w + e, o);
+        // one 256-bit store per thread (a whole 32-B sector; a warp writes 1 KB contiguous): +15 % at
+        // 2^28 elements over two 128-bit half-sector stores (profiles/r02_ab_conv.log)
+        st8f(w + e, o);
     }
     const int64_t t = nunits * kUnitEl + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t < n && t < nunits * kUnitEl + kUnitEl) {

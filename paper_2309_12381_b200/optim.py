@@ -19,6 +19,7 @@ import math
 import weakref
 from typing import Iterable, Optional
 
+import numpy as np
 import torch
 
 from . import api
@@ -95,6 +96,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         # per-parameter step counts, one int64 each: state[p]["step"] is a 0-dim view of this host
         # buffer, which the native hooks update in place (one source of truth for both paths)
         self._steps = torch.zeros(sum(len(g["params"]) for g in self.param_groups), dtype=torch.int64)
+        self._steps_np = self._steps.numpy()     # the same memory: host-side updates without torch ops
         idx = 0
         for group in self.param_groups:
             for p in group["params"]:
@@ -227,7 +229,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             bad = bad * len(params)
         for p, b in zip(params, bad):
             if b:
-                self.state[p]["step"] -= 1
+                self._steps_np[self.state[p]["index"]] -= 1
 
     # -- multi-tensor step -----------------------------------------------------------------
     def _table_for(self, params):
@@ -241,6 +243,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                                   [s.get("m") for s in st], [s.get("v") for s in st],
                                   [0] * len(params), scheme=self.scheme, sr_streams=[s["index"] for s in st])
             tab._group_of = [gi[id(p)] for p in params]
+            tab._idx = np.array([s["index"] for s in st], dtype=np.int64)
             self._tables[key] = tab
         elif [g.data_ptr() for g in grads] != tab.grad_ptrs:
             tab.set_grads(grads)
@@ -261,16 +264,18 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         launches = []
         for plist in by_dtype.values():
             tab = self._table_for(plist)
-            # hyper-parameter groups: one per (param group, step)
+            # hyper-parameter groups: one per (param group, step); the counts advance in the shared
+            # host buffer with one vectorised numpy update (no per-parameter torch op)
+            self._steps_np[tab._idx] += 1
             keys, hp_index = {}, []
-            for p, gi in zip(plist, tab._group_of):
-                self.state[p]["step"] += 1
-                k = (gi, int(self.state[p]["step"]))
-                hp_index.append(keys.setdefault(k, len(keys)))
+            for gi, stp in zip(tab._group_of, self._steps_np[tab._idx].tolist()):
+                hp_index.append(keys.setdefault((gi, stp), len(keys)))
             if len(keys) > MPO_MAX_HP_GROUPS:
                 raise MpoError(1, "more than 16 distinct (group, step) pairs in one step")
-            for i, h in enumerate(hp_index):
-                tab.arr[i].hp = h
+            if hp_index != getattr(tab, "_hp_index", None):     # usually unchanged from the last step
+                for i, h in enumerate(hp_index):
+                    tab.arr[i].hp = h
+                tab._hp_index = hp_index
             launches.append((tab, [self._hp(self.param_groups[gi], stp) for (gi, stp) in keys]))
         need_norm = self._needs_norm()
         if need_norm and len(launches) > 1:
@@ -406,7 +411,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             self._resolve_skips()          # the previous backward's skipped parameters
         st = self.state[p]
         g = p.grad
-        st["step"] += 1
+        self._steps_np[st["index"]] += 1
         if p.numel() < self._batch_below:
             self._pending.append((p, g))
             self._pending_elems += p.numel()
@@ -421,7 +426,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         row.grad = g.data_ptr()
         # host cost per hook matters when backward is short: the ctypes hyper-parameters are built
         # once per (group, step) and shared by the group's parameters; format codes are cached
-        key = (group, int(st["step"]))
+        key = (group, int(self._steps_np[st["index"]]))
         hp = self._hp_c.get(key)
         if hp is None:
             if len(self._hp_c) > 64:
@@ -462,7 +467,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                 sts = [self.state[p] for p in ps]
                 keys, hp_index = {}, []
                 for p_, s_ in zip(ps, sts):
-                    hp_index.append(keys.setdefault((self._rows[p_][1], int(s_["step"])), len(keys)))
+                    hp_index.append(keys.setdefault((self._rows[p_][1], int(self._steps_np[s_["index"]])), len(keys)))
                 tab = api.TensorTable([p.data for p in ps], [s_["resid"] for s_ in sts], [g for _, g in items],
                                       [s_.get("m") for s_ in sts], [s_.get("v") for s_ in sts], hp_index,
                                       scheme=self.scheme, sr_streams=[s_["index"] for s_ in sts])
