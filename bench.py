@@ -1064,8 +1064,8 @@ def main():
     _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=12000)   # ~1 s timed region (clock samples)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=40)      # ~1.2 s timed region at the LLaMA-7B step
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mpo", choices=["mpo", "reference"])
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--no-secondary", action="store_true")
