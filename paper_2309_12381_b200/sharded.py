@@ -115,6 +115,45 @@ def _peer_addrs(h, t: torch.Tensor, rank: int) -> List[int]:
     return [int(p) + off for p in ptrs]
 
 
+def _shard_state_dict(opt, layout_desc):
+    """Checkpoint of one rank's sharded optimizer state (R17): this rank's residual / m / v shard in
+    their own dtypes, the step count, the hyper-parameters and what identifies the layout.  The
+    16-bit values are the parameters themselves (replicated: model.state_dict())."""
+    import dataclasses
+    hps = getattr(opt, "hps", None) or [opt.hp]
+    return {"format": 1, "kind": "adam" if opt.kind == MPO_ADAM else "sgd", "scheme": opt.scheme, "seed": opt.seed,
+            "world": opt.world, "rank": opt.rank, "layout": layout_desc, "step_count": int(opt.step_count),
+            "resid": opt.resid, "m": opt.m, "v": opt.v, "hp": [dataclasses.asdict(h) for h in hps]}
+
+
+def _load_shard_state_dict(opt, sd, layout_desc):
+    if sd.get("format") != 1:
+        raise MpoError(1, "not a sharded residual-optimizer state dict")
+    kind = "adam" if opt.kind == MPO_ADAM else "sgd"
+    for key, mine in (("kind", kind), ("scheme", opt.scheme), ("world", opt.world), ("rank", opt.rank),
+                      ("layout", layout_desc)):
+        if sd.get(key) != mine:
+            raise MpoError(1, f"state dict {key} {sd.get(key)!r} does not match this optimizer's {mine!r}")
+    with torch.no_grad():
+        for key in ("resid", "m", "v"):
+            src, dst = sd.get(key), getattr(opt, key)
+            if (src is None) != (dst is None):
+                raise MpoError(1, f"'{key}' present in only one of state dict / optimizer")
+            if src is None:
+                continue
+            if src.dtype != dst.dtype or tuple(src.shape) != tuple(dst.shape):
+                raise MpoError(3, f"'{key}' is {src.dtype}{tuple(src.shape)}, expected {dst.dtype}{tuple(dst.shape)}")
+            dst.copy_(src)
+    opt.step_count = int(sd["step_count"])
+    opt.seed = int(sd["seed"])
+    hps = getattr(opt, "hps", None) or [opt.hp]
+    if len(sd["hp"]) != len(hps):
+        raise MpoError(1, "state dict has a different number of hyper-parameter groups")
+    for h, d in zip(hps, sd["hp"]):
+        for k, v in d.items():
+            setattr(h, k, v)
+
+
 class ShardedResidualOptimizer:
     """Sharded residual-compensated Adam/AdamW (``kind='adam'``) or SGD-momentum (``kind='sgd'``).
 
@@ -238,6 +277,14 @@ class ShardedResidualOptimizer:
         the sharded step also checks before issuing its collectives)."""
         if self.comm is not None:
             api.mpo_comm_check(self.comm, exact=self.exact)
+
+    def state_dict(self):
+        """This rank's shard of the optimizer state (residual / m / v, step count, hyper-parameters);
+        every rank saves its own.  Resume needs the same world size, rank and parameter layout."""
+        return _shard_state_dict(self, {"sizes": list(self.layout.sizes), "align": self.layout.align})
+
+    def load_state_dict(self, sd):
+        _load_shard_state_dict(self, sd, {"sizes": list(self.layout.sizes), "align": self.layout.align})
 
     def persistent_bytes(self) -> int:
         b = self.value.numel() * 2 + self.grad.numel() * 2 + self.resid.numel() * self.resid.element_size()
@@ -409,6 +456,15 @@ class BucketedShardedOptimizer:
             self.grad[o:o + length].zero_()       # ready for the next backward's accumulation
         if all(x == 0 for x in self._pending):  # backward done: re-arm the bucket counters
             self._pending = [len(idx) for _, _, idx in L.buckets]
+
+    def state_dict(self):
+        """This rank's parts of every bucket's state (see ShardedResidualOptimizer.state_dict)."""
+        self.wait()
+        return _shard_state_dict(self, {"sizes": list(self.layout.sizes), "bucket_elems": self.layout.bucket_elems})
+
+    def load_state_dict(self, sd):
+        self.wait()
+        _load_shard_state_dict(self, sd, {"sizes": list(self.layout.sizes), "bucket_elems": self.layout.bucket_elems})
 
     def wait(self):
         """Make the current stream wait for every bucket step issued so far."""
