@@ -10,9 +10,10 @@ from .api import (AdamParams, SgdParams, TensorTable, mpo_adam_step, mpo_comm_ch
                   mpo_sharded_step, mpo_split, norm_ws_doubles)
 from ._lib import MpoError  # noqa: F401
 from .optim import ResidualAdamW, ResidualSGD  # noqa: F401
-from .sharded import BucketedShardedOptimizer, BucketLayout, ShardedResidualOptimizer, ShardLayout  # noqa: F401
+from .sharded import (BucketedShardedOptimizer, BucketLayout, ShardedResidualAdamW, ShardedResidualOptimizer,  # noqa: F401
+                      ShardedResidualSGD, ShardLayout)
 
 __all__ = ["mpo_split", "mpo_reconstruct", "mpo_sgd_step", "mpo_adam_step", "mpo_fused_backward_hook_step",
            "mpo_sharded_step", "mpo_p2p_sharded_step", "mpo_grad_sumsq", "mpo_comm_check", "TensorTable", "SgdParams", "AdamParams", "ResidualSGD", "ResidualAdamW",
-           "ShardedResidualOptimizer", "ShardLayout", "BucketedShardedOptimizer", "BucketLayout", "MpoError",
+           "ShardedResidualOptimizer", "ShardedResidualAdamW", "ShardedResidualSGD", "ShardLayout", "BucketedShardedOptimizer", "BucketLayout", "MpoError",
            "norm_ws_doubles"]

@@ -293,6 +293,29 @@ class ShardedResidualOptimizer:
         return b
 
 
+class ShardedResidualAdamW(ShardedResidualOptimizer):
+    """SURVEY 8(b)'s `ShardedResidualAdamW(flat_params, process_group, ...)`: the sharded optimizer
+    with torch-style Adam/AdamW arguments."""
+
+    def __init__(self, params, process_group=None, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
+                 weight_decay: float = 0.0, adamw: bool = True, max_grad_norm: Optional[float] = None,
+                 grad_scale: float = 1.0, fmt: Optional[torch.dtype] = None, **kw):
+        hp = api.AdamParams(lr=lr, beta1=betas[0], beta2=betas[1], eps=eps, weight_decay=weight_decay, adamw=adamw,
+                            max_grad_norm=float(max_grad_norm or 0.0), grad_scale=grad_scale)
+        super().__init__(params, kind="adam", fmt=fmt, group=process_group, hp=hp, **kw)
+
+
+class ShardedResidualSGD(ShardedResidualOptimizer):
+    """The sharded optimizer with torch-style SGD(-momentum) arguments."""
+
+    def __init__(self, params, process_group=None, lr: float = 1e-2, momentum: float = 0.0, dampening: float = 0.0,
+                 weight_decay: float = 0.0, nesterov: bool = False, grad_scale: float = 1.0,
+                 fmt: Optional[torch.dtype] = None, **kw):
+        hp = api.SgdParams(lr=lr, momentum=momentum, dampening=dampening, weight_decay=weight_decay, nesterov=nesterov,
+                           grad_scale=grad_scale)
+        super().__init__(params, kind="sgd", fmt=fmt, group=process_group, hp=hp, **kw)
+
+
 # ---------------------------------------------------------------------------------------------
 # Hook mode x sharding (SURVEY 8(f) row 2): bucketed reduce-scatter issued from the
 # post-accumulate-grad hooks, each bucket's residual-compensated step on this rank's part, and the

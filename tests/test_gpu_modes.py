@@ -249,13 +249,15 @@ def test_sharded_world1_equals_unsharded(mpo, nccl1, kind, clip):
     pa = [nn.Parameter(t.clone()) for t in src]
     pb = [nn.Parameter(t.clone()) for t in src]
     if kind == "adam":
-        hp = mpo.AdamParams(lr=1e-3, weight_decay=0.1, max_grad_norm=0.05 if clip else 0.0)
         ref = mpo.ResidualAdamW(pa, lr=1e-3, weight_decay=0.1, fmt=torch.bfloat16,
                                 max_grad_norm=0.05 if clip else None)
     else:
-        hp = mpo.SgdParams(lr=0.1, momentum=0.9)
         ref = mpo.ResidualSGD(pa, lr=0.1, momentum=0.9, fmt=torch.bfloat16)
-    sh = mpo.ShardedResidualOptimizer(pb, kind=kind, fmt=torch.bfloat16, hp=hp)
+    if kind == "adam":   # SURVEY 8(b)'s torch-style names over the same optimizer
+        sh = mpo.ShardedResidualAdamW(pb, lr=1e-3, weight_decay=0.1, fmt=torch.bfloat16,
+                                      max_grad_norm=0.05 if clip else None)
+    else:
+        sh = mpo.ShardedResidualSGD(pb, lr=0.1, momentum=0.9, fmt=torch.bfloat16)
     for t in range(3):
         grads = [torch.randn(s, device="cuda").to(torch.bfloat16) * 1e-2 for s in shapes]
         if clip:   # exact-sum construction: every |g| = 2^-7, so S is exact in any order (P8)
