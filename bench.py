@@ -233,16 +233,8 @@ class Workload:
             if self.comm is None:
                 import torch.distributed as tdist
                 from paper_2309_12381_b200.sharded import nccl_comm_ptr
-                if not tdist.is_initialized():   # world 1: a single-rank NCCL group (degenerate RS/AG)
-                    import socket
-                    import torch
-                    sk = socket.socket()
-                    sk.bind(("127.0.0.1", 0))
-                    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-                    os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
-                    sk.close()
-                    tdist.init_process_group("nccl", rank=0, world_size=1,
-                                             device_id=torch.device("cuda", torch.cuda.current_device()))
+                if not tdist.is_initialized():   # world 1: a single-rank NCCL group (no-op RS/AG)
+                    _single_rank_group()
                 self.comm = nccl_comm_ptr()
             mpo.mpo_sharded_step(MPO_ADAM if self.kind == "adam" else MPO_SGD, self.comm, self.rank, self.world,
                                  self.value, self.grad, self.resid, self.m, self.v, hp,
@@ -809,6 +801,21 @@ def split_reconstruct_secondary(hbm_peak, n=1 << 28, steps=50, warmup=5):
     return res
 
 
+def _single_rank_group():
+    """A one-rank NCCL process group (for the sharded optimizers at world 1), once per process."""
+    import socket
+    import torch
+    import torch.distributed as tdist
+    if tdist.is_initialized():
+        return
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+    sk.close()
+    tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", torch.cuda.current_device()))
+
+
 def flat1m_secondary(hbm_peak, steps=100, warmup=10):
     """BASELINE configs[0]: one flat 2^20-param fp16 + residual tensor, Adam, 100 steps per
     measurement.  Its 27 MB per step fits the 126 MB L2 and one launch is a few microseconds, so
@@ -943,6 +950,29 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024, modes=("hook", "tw
                     for p in model.parameters():
                         p.grad = None
                 return loss
+        elif mode in ("sharded_two_phase", "sharded_bucketed"):
+            # hook mode x sharding at world 1: bucket steps issued from the hooks
+            # on a side stream overlap the rest of backward, vs backward + one sharded step
+            _single_rank_group()
+            mk = mpo.BucketedShardedOptimizer if mode == "sharded_bucketed" else mpo.ShardedResidualOptimizer
+            b1, b2 = hp["betas"]
+            ahp = mpo.AdamParams(lr=hp["lr"], beta1=b1, beta2=b2, weight_decay=hp["weight_decay"])
+            kw = {"bucket_elems": 1 << 24} if mode == "sharded_bucketed" else {}
+            opt = mk(list(model.parameters()), kind="adam", fmt=torch.bfloat16, hp=ahp, **kw)
+
+            def step(rec=None):
+                loss = loss_of(model)
+                if rec is not None:
+                    rec[0].record()
+                loss.backward()
+                if mode == "sharded_bucketed":
+                    opt.wait()
+                if rec is not None:
+                    rec[1].record()
+                if mode == "sharded_two_phase":
+                    opt.step()
+                    opt.zero_grad()
+                return loss
         else:   # paper's baseline: fp32 master + bf16 working copy + fp32 grads + fused AdamW
             master = [p.detach().clone().float() for p in model.parameters()]
             model = model.to(torch.bfloat16)
@@ -1033,6 +1063,14 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024, modes=("hook", "tw
             "two_phase_backward_plus_step_ms": t["backward_ms"] + t["after_backward_ms"],
             "hook_backward_ms": h["backward_ms"],
             "hook_vs_two_phase_train_step": h["ms_per_train_step"] / t["ms_per_train_step"] - 1.0}
+    except Exception:
+        pass
+    try:   # hook mode x sharding at world 1: bucket steps overlapping backward vs a step after it
+        b_, t_ = out["sharded_bucketed"], out["sharded_two_phase"]
+        out["bucketed_sharding_world1"] = {
+            "bucketed_train_step_ms": b_["ms_per_train_step"], "two_phase_sharded_train_step_ms": t_["ms_per_train_step"],
+            "two_phase_step_after_backward_ms": t_["after_backward_ms"],
+            "bucketed_vs_two_phase": b_["ms_per_train_step"] / t_["ms_per_train_step"] - 1.0}
     except Exception:
         pass
     out["config"] = (f"BASELINE configs[2]: HF GPT2LMHeadModel random init (124439808 params, 148 tensors), "
@@ -1185,7 +1223,8 @@ def main():
                 line["secondary"][key] = {"error": f"{type(ex).__name__}: {ex}"}
             torch.cuda.empty_cache()
         try:
-            line["secondary"]["gpt2_hook_mode"] = hook_mode_secondary()
+            line["secondary"]["gpt2_hook_mode"] = hook_mode_secondary(
+                modes=("hook", "two_phase", "amp_fp32_master", "sharded_two_phase", "sharded_bucketed"))
         except Exception as ex:
             line["secondary"]["gpt2_hook_mode"] = {"error": f"{type(ex).__name__}: {ex}"}
         try:   # small activations (B=1, T=128): gradients are a large share of the peak
