@@ -1202,6 +1202,14 @@ def main():
         torch.cuda.empty_cache()
         line["secondary"] = secondary([n for n in ("resnet50_sgd", "gpt2_adamw", "vit_l16_adam_clip", "llama7b_adam")
                                        if n != args.workload], 200, 5, hbm_peak)
+        if args.workload == "llama7b_adam":
+            # the same LLaMA-7B step through the sharded entry point at world 1 (one flat piece, the
+            # NCCL reduce-scatter / all-gather issued as single-rank no-ops): the N>1 path's cost at N=1
+            try:
+                line["secondary"]["llama7b_adam_sharded_world1"] = _secondary_one("llama7b_adam", 20, 3, hbm_peak)
+            except Exception as ex:
+                line["secondary"]["llama7b_adam_sharded_world1"] = {"error": f"{type(ex).__name__}: {ex}"}
+            torch.cuda.empty_cache()
         try:
             line["secondary"]["flat1m_adam"] = flat1m_secondary(hbm_peak)
         except Exception as ex:

@@ -818,6 +818,12 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 #endif
 
+#ifdef MPO_L2_PREFETCH
+__device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+#endif
+
 template <int G>
 struct GradBytes {
     static constexpr int v = G == kFP32 ? 4 : 2;
@@ -924,6 +930,19 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
                 while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
                 const int64_t base = int64_t(tile - tab.t[cur].tile0) * TE;
                 issue(cur, base, tab.t[cur].n - base < TE ? tab.t[cur].n - base : TE);
+#ifdef MPO_L2_PREFETCH
+                {   // A/B knob: bulk-prefetch into L2 the tile this CTA loads MPO_L2_PREFETCH rounds later
+                    const KT& T = tab.t[cur];
+                    const int64_t fb = base + int64_t(MPO_L2_PREFETCH) * gridDim.x * TE;
+                    if (fb + TE <= T.n) {
+                        l2_prefetch(static_cast<const uint16_t*>(T.value) + fb, uint32_t(TE * 2));
+                        l2_prefetch(static_cast<const unsigned char*>(T.resid) + fb * RB, uint32_t(TE * RB));
+                        l2_prefetch(static_cast<const unsigned char*>(T.grad) + fb * GB, uint32_t(TE * GB));
+                        l2_prefetch(T.m + fb, uint32_t(TE * 4));
+                        if constexpr (Op::kHasV) l2_prefetch(T.v + fb, uint32_t(TE * 4));
+                    }
+                }
+#endif
             }
             // end of schedule: a descriptor with no tensor, completed by a plain arrive
             mbar_wait(&empty[s], ph ^ 1u);
