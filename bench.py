@@ -816,6 +816,60 @@ def _single_rank_group():
     tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", torch.cuda.current_device()))
 
 
+def per_tensor_secondary(name, hbm_peak, steps=50, warmup=5):
+    """SURVEY 8(d) "multi-tensor vs per-tensor launch" ("too many kernel launches can hinder
+    performance on smaller parameters"): the same step as one launch over the whole table, as one
+    launch per tensor from Python, and as those per-tensor launches captured in a CUDA graph
+    (device-side cost of the launches alone)."""
+    import torch
+    wl = Workload(name)
+    mpo = wl.mpo
+    L = wl.layout
+    shapes = [(n,) for n in wl.sizes]
+    V, R, G, M = (L.views(t, shapes) for t in (wl.value, wl.resid, wl.grad, wl.m))
+    W = L.views(wl.v, shapes) if wl.v is not None else [None] * len(shapes)
+    tabs = [mpo.TensorTable([v], [r], [g], [m], [w], scheme=wl.scheme) for v, r, g, m, w in zip(V, R, G, M, W)]
+
+    def per_tensor():
+        wl.t += 1
+        hp = wl.hp()
+        for t in tabs:
+            (mpo.mpo_sgd_step if wl.kind == "sgd" else mpo.mpo_adam_step)(t, hp)
+    ms_multi, _ = timed(wl.step, steps, warmup)
+    ms_py, launches = timed(per_tensor, steps, warmup)
+    g_ms = None
+    try:
+        s_ = torch.cuda.Stream()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s_):
+            per_tensor()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph, stream=s_):
+                per_tensor()
+        graph.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            graph.replay()
+        b.record()
+        torch.cuda.synchronize()
+        g_ms = a.elapsed_time(b) / steps
+        del graph
+    except Exception as ex:   # recorded, not hidden
+        g_ms = f"unavailable: {type(ex).__name__}: {ex}"[:200]
+    per = wl.P * wl.bytes_per_param
+    res = {"config": f"{name}: {wl.P} params, {wl.ntensors} tensors",
+           "multi_tensor_one_launch": {"ms_per_step": ms_multi, "frac_of_measured_hbm": per / (ms_multi * 1e-3) / 1e9 / hbm_peak},
+           "per_tensor_from_python": {"ms_per_step": ms_py, "launches_per_step": launches / steps,
+                                      "frac_of_measured_hbm": per / (ms_py * 1e-3) / 1e9 / hbm_peak},
+           "per_tensor_cuda_graph": ({"ms_per_step": g_ms, "frac_of_measured_hbm": per / (g_ms * 1e-3) / 1e9 / hbm_peak}
+                                     if isinstance(g_ms, float) else g_ms)}
+    del wl, tabs
+    torch.cuda.empty_cache()
+    return res
+
+
 def flat1m_secondary(hbm_peak, steps=100, warmup=10):
     """BASELINE configs[0]: one flat 2^20-param fp16 + residual tensor, Adam, 100 steps per
     measurement.  Its 27 MB per step fits the 126 MB L2 and one launch is a few microseconds, so
@@ -1210,6 +1264,10 @@ def main():
             except Exception as ex:
                 line["secondary"]["llama7b_adam_sharded_world1"] = {"error": f"{type(ex).__name__}: {ex}"}
             torch.cuda.empty_cache()
+        try:
+            line["secondary"]["resnet50_multi_vs_per_tensor"] = per_tensor_secondary("resnet50_sgd", hbm_peak)
+        except Exception as ex:
+            line["secondary"]["resnet50_multi_vs_per_tensor"] = {"error": f"{type(ex).__name__}: {ex}"}
         try:
             line["secondary"]["flat1m_adam"] = flat1m_secondary(hbm_peak)
         except Exception as ex:
