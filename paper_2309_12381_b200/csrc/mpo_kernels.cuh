@@ -5,10 +5,12 @@
 //
 // Kernel design.  The step is an elementwise stream (no contraction, so
 // no tensor cores): per element Adam moves 26 B (value 2 + resid 2 + grad 2 + m 4 + v 4 read;
-// value, resid, m, v written), SGD-momentum 18 B.  It is HBM-bound on B200, so the default
-// kernel (step_tma_kernel) is a persistent warp-specialised pipeline: one producer warp streams
-// each 4096-element tile of every stream into shared-memory stages with 1-D TMA bulk copies while
-// 16 consumer warps compute one 8-element unit per thread and store with 128-bit stores.  The
+// value, resid, m, v written), SGD-momentum 18 B.  It is HBM-bound on B200, so the kernel of
+// every launch above 640 tiles (step_tma_kernel) is a persistent warp-specialised pipeline: one
+// producer warp streams each 4096-element tile of every stream into shared-memory stages with 1-D
+// TMA bulk copies while 16 consumer warps compute one 8-element unit per thread and store with
+// 128-bit stores; smaller launches (hook-mode steps, small models) use step_kernel, whose
+// per-thread loads avoid the pipeline's fill.  The
 // multi-tensor table ("one only stream of values") travels by value as a __grid_constant__
 // kernel parameter; ragged tails (n % 8) are handled element by element; warp shuffles appear
 // only in the global-norm reduction (clipping).
