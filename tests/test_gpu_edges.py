@@ -189,3 +189,38 @@ def test_edge_hook_step_bit_exact(mpo, orc, fmt, kind):
     assert same_bits_nan_equal(M.cpu().numpy(), m)
     if kind == "adamw":
         assert same_bits_nan_equal(Vv.cpu().numpy(), v)
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+@pytest.mark.parametrize("kind", ["adamw", "sgd_m"])
+def test_edge_steps_fma_build(mpo, orc, fmt, kind):
+    """The FMA build (exact=False) on the same edge cross product: every special outcome is the
+    oracle's exactly (NaN -> 0x7FFF, +-Inf, signed zeros, overflow to Inf at the same elements), and
+    the finite values are within 1 ulp16 or R12's operand-scaled bound of the oracle."""
+    from gpu_util import ulp16_dist
+    W, G = cross(fmt, fmt, 0)
+    h, r = orc.split(fmt, W)
+    m, v = state(W.size, 91)
+    V, R, Gd, M, Vv = dev16(h, fmt), dev_resid(r), dev_grad(G, fmt), devf(m), devf(v)
+    hp = _hps(mpo, kind, 2, 0)
+    adam = kind == "adamw"
+    tab = mpo.TensorTable([V], [R], [Gd], [M], [Vv] if adam else [None])
+    if adam:
+        mpo.mpo_adam_step(tab, hp, exact=False)
+        orc.adam_step(fmt, fmt, h, r, G, m, v, lr=hp.lr, beta1=hp.beta1, beta2=hp.beta2, eps=hp.eps,
+                      weight_decay=hp.weight_decay, adamw=hp.adamw, step=hp.step)
+    else:
+        mpo.mpo_sgd_step(tab, hp, exact=False)
+        orc.sgd_step(fmt, fmt, h, r, G, m, lr=hp.lr, momentum=hp.momentum, weight_decay=hp.weight_decay,
+                     first_step=hp.first_step)
+    hg = host16(V)
+    inf16 = (0x7C00, 0xFC00) if fmt == "fp16" else (0x7F80, 0xFF80)
+    special = lambda x: np.isin(x, np.array(inf16 + (0x7FFF,), np.uint16))
+    assert np.array_equal(special(hg), special(h))
+    assert np.array_equal(hg[special(h)], h[special(h)])
+    fin = ~special(h)
+    wg = orc.reconstruct(fmt, hg, R.cpu().numpy().view(np.int16)).astype(np.float64)
+    wo = orc.reconstruct(fmt, h, r).astype(np.float64)
+    w0 = W.astype(np.float64)
+    close = (ulp16_dist(hg, h, fmt) <= 1) | (np.abs(wg - wo) <= 1e-6 * (np.abs(w0) + np.abs(wo)) + 2.0 ** -24)
+    assert close[fin].all(), np.flatnonzero(fin & ~close)[:8]

@@ -126,19 +126,23 @@ def test_variant_steps_bit_exact(mpo, orc, scheme, fmt, kind, gsame, step_kernel
             assert same_bits_nan_equal(W[i].cpu().numpy(), vs[i]), i
 
 
-def test_sr_hook_mode_equals_multi_tensor(mpo):
-    """Stochastic rounding keyed by per-parameter streams: the fused-backward path and the
-    multi-tensor path draw the same numbers and agree bitwise."""
+@pytest.mark.parametrize("scheme,fmt,native", [("sr", torch.float16, True), ("sr", torch.float16, False),
+                                               ("rtz", torch.bfloat16, True), ("x8", torch.float16, True),
+                                               ("x8", torch.bfloat16, False)])
+def test_variant_hook_mode_equals_multi_tensor(mpo, scheme, fmt, native):
+    """Every storage variant through the fused backward (native C++ and Python hooks): == the
+    multi-tensor step bitwise; stochastic rounding is keyed by per-parameter streams, so both paths
+    draw the same numbers."""
     torch.manual_seed(0)
     d = 96
     mk = lambda: torch.nn.Sequential(torch.nn.Linear(d, 2 * d), torch.nn.GELU(), torch.nn.Linear(2 * d, d)).cuda()
     a, b = mk(), mk()
     b.load_state_dict(a.state_dict())
-    oa = mpo.ResidualAdamW(a.parameters(), lr=1e-3, weight_decay=0.1, fmt=torch.float16, scheme="sr", seed=9)
-    ob = mpo.ResidualAdamW(b.parameters(), lr=1e-3, weight_decay=0.1, fmt=torch.float16, scheme="sr", seed=9)
-    ob.install_backward_hooks()
+    oa = mpo.ResidualAdamW(a.parameters(), lr=1e-3, weight_decay=0.1, fmt=fmt, scheme=scheme, seed=9)
+    ob = mpo.ResidualAdamW(b.parameters(), lr=1e-3, weight_decay=0.1, fmt=fmt, scheme=scheme, seed=9)
+    ob.install_backward_hooks(native=native, batch_below=0 if native else 1 << 16)
     for t in range(3):
-        x = torch.randn(32, d, device="cuda", dtype=torch.float16)
+        x = torch.randn(32, d, device="cuda", dtype=fmt)
         a(x).float().square().mean().backward()
         oa.step()
         for p in a.parameters():
