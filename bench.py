@@ -63,6 +63,28 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def same_box_copy_gbs():
+    """The copy bandwidth of THIS box, measured like MEASURED_PEAKS.json's hbm_gbs (torch copy of
+    1 Gi bf16 elements, read + write bytes, best of 10, CUDA events): boxes differ by a few %, so the
+    line also states the kernel's fraction of its own box's copy (the roofline peak stays the
+    driver-measured number)."""
+    import torch
+    a = torch.empty(1 << 30, dtype=torch.bfloat16, device="cuda")
+    b = torch.empty_like(a)
+    best = None
+    for _ in range(12):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        best = t if best is None else min(best, t)
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * 2 * (1 << 30) / (best * 1e-3) / 1e9
+
+
 def ncu_traffic(workload):
     """dram read+write bytes per launch of the step kernel from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -1205,6 +1227,12 @@ def main():
     # measurement of multi_gpu_breakdown below.
     achieved = alg_bytes / (per_launch * 1e-3) / 1e9
     traffic = ncu_traffic(args.workload)
+    box_copy = None
+    try:
+        if world == 1 and torch.cuda.mem_get_info()[0] > 5 * (1 << 30):   # two 2 GiB buffers
+            box_copy = same_box_copy_gbs()
+    except Exception:
+        box_copy = None
     mg = None
     if world > 1 or args.mg_breakdown:
         try:
@@ -1242,7 +1270,8 @@ def main():
                      "frac_of_8tbs_spec": achieved / 8000.0,
                      "kernel": "step_tma_kernel (reconstruct -> update -> re-split)",
                      "algorithmic_bytes_per_launch": alg_bytes, "bytes_per_param": wl.bytes_per_param,
-                     "mean_launch_ms": per_launch},
+                     "mean_launch_ms": per_launch, "same_box_copy_gbs": box_copy,
+                     "frac_of_same_box_copy": (achieved / box_copy) if box_copy else None},
         "gpu_launches": launches,
         **({"multi_gpu": mg} if mg is not None else {}),
         "clocks": clocks,
