@@ -64,5 +64,21 @@ model2 = torch.nn.Sequential(torch.nn.Linear(32, 40), torch.nn.Linear(40, 8)).cu
 o3 = mpo.ResidualSGD(model2.parameters(), lr=0.1, momentum=0.9, fmt=torch.float16)
 o3.install_backward_hooks(native=False, batch_below=0)
 model2(torch.randn(4, 32, device=dev, dtype=torch.float16)).float().sum().backward()
+# both step kernels on the same small tables (the library picks the per-thread-load kernel for
+# launches of <= 640 tiles; MPO_STEP_KERNEL forces either), and a table above the threshold
+for forced in ("tma", "lsu"):
+    os.environ["MPO_STEP_KERNEL"] = forced
+    V, R, G, M, W = [], [], [], [], []
+    for n in sizes:
+        v, r = mpo.mpo_split(torch.randn(n, device=dev) * 0.02, torch.bfloat16)
+        V.append(v); R.append(r); G.append((torch.randn(n, device=dev) * 1e-2).to(torch.bfloat16))
+        M.append(torch.zeros(n, device=dev)); W.append(torch.zeros(n, device=dev))
+    mpo.mpo_adam_step(mpo.TensorTable(V, R, G, M, W), mpo.AdamParams(lr=1e-3, step=1))
+os.environ.pop("MPO_STEP_KERNEL")
+big = 700 * 4096 + 5
+v, r = mpo.mpo_split(torch.randn(big, device=dev) * 0.02, torch.float16)
+mpo.mpo_sgd_step(mpo.TensorTable([v], [r], [(torch.randn(big, device=dev) * 1e-2).to(torch.float16)],
+                                 [torch.zeros(big, device=dev)], [None]), mpo.SgdParams(lr=0.1, momentum=0.9))
+mpo.mpo_reconstruct(v, r)
 torch.cuda.synchronize()
 print("sanitize run ok")
