@@ -206,6 +206,33 @@ int64_t mpo_norm_ws_doubles(void);
 mpo_status mpo_grad_sumsq(mpo_dtype gdt, const mpo_tensor* t, int32_t nt, const double* grad_scale,
                           int32_t nhp, double* norm_ws, int32_t accumulate, mpo_stream stream);
 
+/* A step that can be captured ONCE in a CUDA graph and replayed every step (whole-iteration graph
+ * capture, "CUDA graphs instead of a tracing compiler"): the per-step derived hyper-parameters --
+ * bias corrections (step), lr, betas, eps, weight decay, SGD's first step, the stochastic-rounding
+ * seed -- are not kernel arguments but a block that the call copies from host_block to dev_block
+ * in stream order before the kernels read it.  A graph that captured the call repeats that copy at
+ * every replay, reading host_block's CURRENT contents, so the caller refills host_block with
+ * mpo_hp_block_fill (a host function, no CUDA call) before each replay.
+ *   kind, vdt, gdt, t, nt, norm_ws : as mpo_sgd_step / mpo_adam_step (the table -- pointers, sizes,
+ *               groups -- is fixed at capture)
+ *   hp, nhp   : HOST hyper-parameters used for validation and the step's static parts: the kernel
+ *               choice, max_grad_norm, skip_nonfinite and the norm pre-pass's grad scales
+ *   host_block: mpo_hp_block_bytes(kind) bytes of PAGE-LOCKED host memory (cudaHostAlloc / torch
+ *               pin_memory), filled by mpo_hp_block_fill
+ *   dev_block : mpo_hp_block_bytes(kind) bytes of device memory, 16-B aligned (owned by the caller)
+ *   ack       : NULL, or a page-locked host word the device writes the block's sequence number to
+ *               right after the copy: a caller that reads back the sequence number it wrote may
+ *               refill host_block for the next replay without racing this one's copy
+ * Bit-identical to the corresponding mpo_sgd_step / mpo_adam_step with the same hp. */
+int64_t mpo_hp_block_bytes(mpo_optim kind);
+/* Derive the kernel's per-group scalars from nhp hyper-parameter groups (host memory, R7: in double,
+ * rounded once to float) into host_block (mpo_hp_block_bytes(kind) bytes) and tag it with `seq`.
+ * No CUDA call. */
+mpo_status mpo_hp_block_fill(mpo_optim kind, const void* hp, int32_t nhp, uint64_t seq, void* host_block);
+mpo_status mpo_step_graphed(mpo_optim kind, mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t, int32_t nt,
+                            const void* hp, int32_t nhp, const void* host_block, void* dev_block,
+                            unsigned long long* ack, double* norm_ws, mpo_stream stream);
+
 /* Fused backward + optimizer step for ONE parameter, called from its post-accumulate-grad hook
  * ("operate the optimization step as soon as the gradient is computed").
  *   kind : MPO_SGD (hp -> mpo_sgd_hp) | MPO_ADAM (hp -> mpo_adam_hp), hp in HOST memory

@@ -26,7 +26,7 @@ SYMBOLS = ("mpo_split", "mpo_reconstruct", "mpo_sgd_step", "mpo_adam_step", "mpo
            "mpo_fused_backward_hook_step", "mpo_sharded_step", "mpo_last_error", "mpo_build_exact",
            "mpo_launch_count", "mpo_selfcheck_fastmath", "mpo_nvls_sharded_step", "mpo_nvls_alloc_local",
            "mpo_nvls_free_local", "mpo_p2p_sharded_step", "mpo_grad_sumsq", "mpo_sharded_step_grouped",
-           "mpo_comm_check")
+           "mpo_comm_check", "mpo_hp_block_bytes", "mpo_hp_block_fill", "mpo_step_graphed")
 
 
 class MpoError(RuntimeError):
@@ -77,8 +77,13 @@ def _declare(L):
                                            P, I32, P, P]
     L.mpo_grad_sumsq.argtypes = [D, C.POINTER(Tensor), I32, C.POINTER(C.c_double), I32, P, I32, P]
     L.mpo_comm_check.argtypes = [C.c_size_t]
+    L.mpo_hp_block_bytes.argtypes = [D]
+    L.mpo_hp_block_bytes.restype = I64
+    L.mpo_hp_block_fill.argtypes = [D, P, I32, C.c_uint64, P]
+    L.mpo_step_graphed.argtypes = [D, D, D, C.POINTER(Tensor), I32, P, I32, P, P, P, P, P]
     for f in ("mpo_split", "mpo_reconstruct", "mpo_sgd_step", "mpo_adam_step", "mpo_fused_backward_hook_step",
-              "mpo_sharded_step", "mpo_sharded_step_grouped", "mpo_grad_sumsq", "mpo_comm_check"):
+              "mpo_sharded_step", "mpo_sharded_step_grouped", "mpo_grad_sumsq", "mpo_comm_check", "mpo_hp_block_fill",
+              "mpo_step_graphed"):
         getattr(L, f).restype = C.c_int
     L.mpo_last_error.restype = C.c_char_p
     L.mpo_last_error.argtypes = []

@@ -294,6 +294,38 @@ def mpo_grad_sumsq(table: TensorTable, grad_scales, norm_ws: torch.Tensor, accum
                                    int(bool(accumulate)), _stream(stream)))
 
 
+def hp_block_bytes(kind: int, exact: bool = True) -> int:
+    """Bytes of the per-step hyper-parameter block of mpo_step_graphed."""
+    return int(_lib_of(exact).mpo_hp_block_bytes(kind))
+
+
+def hp_block_fill(kind: int, hps, host_block: torch.Tensor, seq: int = 0, exact: bool = True):
+    """Derive this step's kernel scalars from ``hps`` into ``host_block`` (pinned uint8 tensor of
+    hp_block_bytes(kind) bytes), tagged with ``seq``; a host function, no CUDA call (include/mpo.h)."""
+    arr, nhp = _hp_array(hps, AdamHP if kind == MPO_ADAM else SgdHP)
+    if host_block.device.type != "cpu" or host_block.numel() * host_block.element_size() < hp_block_bytes(kind, exact):
+        raise MpoError(_lib.MPO_EINVAL, "host_block must be a host tensor of hp_block_bytes() bytes")
+    L = _lib_of(exact)
+    _lib.check(L, L.mpo_hp_block_fill(kind, C.cast(arr, C.c_void_p), nhp, int(seq), host_block.data_ptr()))
+
+
+def mpo_step_graphed(kind: int, table: TensorTable, hps, host_block: torch.Tensor, dev_block: torch.Tensor,
+                     ack: Optional[torch.Tensor] = None, norm_ws: Optional[torch.Tensor] = None, stream=None,
+                     exact: bool = True):
+    """A step whose per-step hyper-parameters are copied host_block -> dev_block in stream order and
+    read by the kernels from there: capturable once in a CUDA graph, replayed every step after
+    hp_block_fill (include/mpo.h mpo_step_graphed).  host_block (and ack: one pinned int64 the
+    device echoes the block's sequence number to) must be pinned."""
+    if not host_block.is_pinned() or (ack is not None and not ack.is_pinned()):
+        raise MpoError(_lib.MPO_EINVAL, "host_block / ack must be pinned (page-locked) host memory")
+    arr, nhp = _hp_array(hps, AdamHP if kind == MPO_ADAM else SgdHP)
+    L = _lib_of(exact)
+    _check_ws(norm_ws, exact)
+    _lib.check(L, L.mpo_step_graphed(kind, table.vdt, table.gdt, table.arr, table.nt, C.cast(arr, C.c_void_p), nhp,
+                                     host_block.data_ptr(), _ptr(dev_block), None if ack is None else ack.data_ptr(),
+                                     _ptr(norm_ws), _stream(stream)))
+
+
 def mpo_comm_check(comm_ptr: int, exact: bool = True):
     """Raises MpoError(MPO_ENCCL) if the NCCL communicator failed asynchronously (never blocks)."""
     L = _lib_of(exact)

@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(kThreads) selfcheck_div_kernel(int64_t pairs, 
 // Host side
 // ------------------------------------------------------------------------------------------
 thread_local std::string g_err;
+thread_local const void* g_dev_hp = nullptr;
 std::atomic<int64_t> g_launches{0};
 
 mpo_status fail(mpo_status s, const std::string& msg) {
@@ -462,6 +463,84 @@ MPO_API mpo_status mpo_adam_step(mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor*
     if ((st = check_adam_hp(hp, nhp)) != MPO_OK) return st;
     if ((st = check_table(t, nt, nhp, true, nullptr)) != MPO_OK) return st;
     return adam_common(vdt, gdt, t, nt, hp, nhp, norm_ws, false, static_cast<cudaStream_t>(stream), false);
+}
+
+// The per-step block of mpo_step_graphed: the derived scalars of every group, then a 16-B slot whose
+// first uint64 is the block's sequence number (written by mpo_hp_block_fill, echoed to the
+// caller's acknowledgement word once the device copy has happened).
+static size_t hp_part_bytes(mpo_optim kind) { return kind == MPO_ADAM ? sizeof(HP<AdamK>) : sizeof(HP<SgdK>); }
+
+MPO_API int64_t mpo_hp_block_bytes(mpo_optim kind) { return int64_t(hp_part_bytes(kind) + 16); }
+
+MPO_API mpo_status mpo_hp_block_fill(mpo_optim kind, const void* hp, int32_t nhp, uint64_t seq, void* host_block) {
+    g_err.clear();
+    mpo_status st;
+    if (!hp || !host_block) return fail(MPO_EINVAL, "NULL hyper-parameters or block");
+    if (kind == MPO_ADAM) {
+        const mpo_adam_hp* h = static_cast<const mpo_adam_hp*>(hp);
+        if ((st = check_adam_hp(h, nhp)) != MPO_OK) return st;
+        HP<AdamK> k;
+        for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) k.g[i] = i < nhp ? derive_adam(h[i]) : k.g[0];
+        std::memcpy(host_block, &k, sizeof(k));
+    } else if (kind == MPO_SGD) {
+        const mpo_sgd_hp* h = static_cast<const mpo_sgd_hp*>(hp);
+        if ((st = check_sgd_hp(h, nhp)) != MPO_OK) return st;
+        HP<SgdK> k;
+        for (int i = 0; i < MPO_MAX_HP_GROUPS; ++i) k.g[i] = i < nhp ? derive_sgd(h[i]) : k.g[0];
+        std::memcpy(host_block, &k, sizeof(k));
+    } else {
+        return fail(MPO_EINVAL, "unknown optimizer kind");
+    }
+    std::memcpy(static_cast<unsigned char*>(host_block) + hp_part_bytes(kind), &seq, sizeof(seq));
+    return MPO_OK;
+}
+
+// Echo the device copy's sequence number to the caller's (host-mapped) acknowledgement word: the
+// host may refill the block once it reads back the sequence number it wrote.
+__global__ void ack_kernel(const uint64_t* __restrict__ seq, volatile unsigned long long* ack) {
+    *ack = static_cast<unsigned long long>(*seq);
+    __threadfence_system();
+}
+
+MPO_API mpo_status mpo_step_graphed(mpo_optim kind, mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* t, int32_t nt,
+                                    const void* hp, int32_t nhp, const void* host_block, void* dev_block,
+                                    unsigned long long* ack, double* norm_ws, mpo_stream stream) {
+    g_err.clear();
+    mpo_status st;
+    if (!host_block || !dev_block) return fail(MPO_EINVAL, "NULL hyper-parameter block");
+    if (!aligned16(dev_block)) return fail(MPO_EALIGN, "device hyper-parameter block not 16-byte aligned");
+    if ((st = check_dtypes(vdt, gdt)) != MPO_OK) return st;
+    if (kind != MPO_SGD && kind != MPO_ADAM) return fail(MPO_EINVAL, "unknown optimizer kind");
+    if (kind == MPO_ADAM) {
+        const mpo_adam_hp* h = static_cast<const mpo_adam_hp*>(hp);
+        if ((st = check_adam_hp(h, nhp)) != MPO_OK) return st;
+        if ((st = check_table(t, nt, nhp, true, nullptr)) != MPO_OK) return st;
+    } else {
+        const mpo_sgd_hp* h = static_cast<const mpo_sgd_hp*>(hp);
+        if ((st = check_sgd_hp(h, nhp)) != MPO_OK) return st;
+        if ((st = check_table(t, nt, nhp, false, h)) != MPO_OK) return st;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // the step's derived hyper-parameters travel host block -> device block in stream order, so a
+    // CUDA graph that captured this call re-reads the host block (refilled by mpo_hp_block_fill)
+    // every time it is replayed
+    const cudaError_t ce = cudaMemcpyAsync(dev_block, host_block, size_t(mpo_hp_block_bytes(kind)),
+                                           cudaMemcpyHostToDevice, s);
+    if (ce != cudaSuccess) return fail(MPO_ECUDA, std::string("cudaMemcpyAsync: ") + cudaGetErrorString(ce));
+    if (ack) {
+        ack_kernel<<<1, 1, 0, s>>>(reinterpret_cast<const uint64_t*>(static_cast<unsigned char*>(dev_block) +
+                                                                     hp_part_bytes(kind)),
+                                   ack);
+        ++g_launches;
+        if ((st = check_launch("ack_kernel")) != MPO_OK) return st;
+    }
+    g_dev_hp = dev_block;
+    if (kind == MPO_ADAM)
+        st = adam_common(vdt, gdt, t, nt, static_cast<const mpo_adam_hp*>(hp), nhp, norm_ws, false, s, false);
+    else
+        st = sgd_common(vdt, gdt, t, nt, static_cast<const mpo_sgd_hp*>(hp), nhp, norm_ws, false, s, false);
+    g_dev_hp = nullptr;
+    return st;
 }
 
 MPO_API mpo_status mpo_fused_backward_hook_step(mpo_optim kind, mpo_dtype vdt, mpo_dtype gdt, const mpo_tensor* one,

@@ -92,6 +92,9 @@ __device__ __forceinline__ uint32_t stream_of(const KT& T) { return static_cast<
 // Host state shared by the translation units (defined in mpo.cu)
 // ------------------------------------------------------------------------------------------
 extern thread_local std::string g_err;
+// Device copy of the call's derived hyper-parameters (HP<AdamK> / HP<SgdK>) when the step is issued
+// by mpo_step_graphed (set around that call only; nullptr otherwise).
+extern thread_local const void* g_dev_hp;
 extern std::atomic<int64_t> g_launches;
 mpo_status fail(mpo_status s, const std::string& msg);
 mpo_status check_launch(const char* what);
@@ -659,6 +662,7 @@ __device__ __forceinline__ void store_unit(const KT& T, int64_t e, const uint4& 
 template <int MAXT, int SF, int G, class Op, bool CLIP>
 __global__ void __launch_bounds__(kThreads) step_kernel(const __grid_constant__ Table<MAXT> tab,
                                                         const __grid_constant__ HP<typename Op::K> hp,
+                                                        const HP<typename Op::K>* __restrict__ dhp,
                                                         const double* __restrict__ sumsq, double max_norm,
                                                         int skip) {
     using K = typename Op::K;
@@ -669,7 +673,7 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const __grid_constant__ 
     for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
         while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
         const KT& T = tab.t[cur];
-        const K c = hp.g[hp_of(T)];
+        const K c = dhp ? dhp->g[hp_of(T)] : hp.g[hp_of(T)];   // dhp: a graph-replayed step (mpo_step_graphed)
         const bool need_m = Op::reads_m(c);
         const bool has_m = Op::writes_m(c);
         const int64_t base = int64_t(tile - T.tile0) * kTileEl;
@@ -849,6 +853,7 @@ __host__ __device__ constexpr int stage_bytes() {
 template <int MAXT, int SF, int G, class Op, bool CLIP>
 __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(const __grid_constant__ Table<MAXT> tab,
                                                                   const __grid_constant__ HP<typename Op::K> hp,
+                                                                  const HP<typename Op::K>* __restrict__ dhp,
                                                                   const double* __restrict__ sumsq, double max_norm,
                                                                   int stages, int skip) {
     using K = typename Op::K;
@@ -893,7 +898,7 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
             auto issue = [&](int cur, int64_t base, int64_t nvalid) {
                 mbar_wait(&empty[s], ph ^ 1u);
                 const KT& T = tab.t[cur];
-                const K c = hp.g[hp_of(T)];
+                const K c = dhp ? dhp->g[hp_of(T)] : hp.g[hp_of(T)];
                 const uint32_t nvec = uint32_t(nvalid) & ~(kGran - 1u);
                 const bool need_m = Op::reads_m(c);
                 uint32_t bytes = nvec * (2u + RB + GB);
@@ -966,7 +971,7 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
         const StageDesc d = desc[s];
         if (d.cur < 0) break;
         const KT& T = tab.t[d.cur];
-        const K c = hp.g[hp_of(T)];
+        const K c = dhp ? dhp->g[hp_of(T)] : hp.g[hp_of(T)];
         const int64_t base = d.base, nvalid = d.nvalid;
         const int64_t nvec = nvalid & ~int64_t(kGran - 1u);
         const bool full_unit = el + kUnitEl <= nvec;
@@ -1562,7 +1567,8 @@ mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typen
         auto kern = step_kernel<MAXT, SF, G, Op, CLIP>;
         static int per_sm = resident_blocks(kern);
         const int64_t grid = grid_for(tiles, per_sm);
-        kern<<<unsigned(grid), kThreads, 0, s>>>(tab, hp, sumsq, max_norm, skip);
+        kern<<<unsigned(grid), kThreads, 0, s>>>(tab, hp, static_cast<const HP<typename Op::K>*>(g_dev_hp), sumsq,
+                                                 max_norm, skip);
         ++g_launches;
         return check_launch("step_kernel");
     }
@@ -1575,7 +1581,8 @@ mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typen
     constexpr int smem = kBarBytes + kDescBytes + stages * SB;
     static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (attr != cudaSuccess) return fail(MPO_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr));
-    kern<<<unsigned(grid), kTmaThreads, smem, s>>>(tab, hp, sumsq, max_norm, stages, skip);
+    kern<<<unsigned(grid), kTmaThreads, smem, s>>>(tab, hp, static_cast<const HP<typename Op::K>*>(g_dev_hp), sumsq,
+                                                   max_norm, stages, skip);
     ++g_launches;
     return check_launch("step_tma_kernel");
 }

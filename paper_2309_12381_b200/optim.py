@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import time
 import weakref
 from typing import Iterable, Optional
 
@@ -253,6 +254,8 @@ class _ResidualOptimizer(torch.optim.Optimizer):
     def step(self, closure=None):
         if closure is not None:
             raise MpoError(1, "closure optimizers are not supported (the step is fused, P:194)")
+        if getattr(self, "_graph", None) is not None:
+            return self._graph_step()        # prepare_step() did the host side
         self._resolve_skips()
         params = [p for g in self.param_groups for p in g["params"] if p.grad is not None]
         if not params:
@@ -294,6 +297,90 @@ class _ResidualOptimizer(torch.optim.Optimizer):
 
     def _needs_norm(self):
         return self.skip_nonfinite or getattr(self, "max_grad_norm", 0.0) > 0
+
+    # -- CUDA-graph step -------------------------------------------------------------------
+    def enable_graph_step(self):
+        """Make step() capturable ONCE in a CUDA graph together with the rest of the training
+        iteration, then replayed every step (mpo_step_graphed: the step's hyper-parameters are not
+        kernel arguments but a block copied from pinned host memory at execution time)::
+
+            opt.enable_graph_step()
+            # warm up eagerly so every parameter has its gradient buffer (fixed addresses)
+            with torch.cuda.graph(g):
+                loss = model(x).loss; loss.backward(); opt.step()     # captures, runs nothing
+            for it in range(...):
+                opt.prepare_step()          # step counts + this step's lr / bias corrections
+                g.replay()
+
+        (Eagerly, ``opt.prepare_step(); opt.step()`` is one ordinary step.)  prepare_step() first
+        waits until the previous step's hyper-parameter copy has happened (the device echoes each
+        block's sequence number to a pinned word right after its copy) or the current stream is
+        idle, so it never rewrites a block a pending replay still has to read.  Bit-identical to
+        the eager step() sequence.  Not with the backward hooks or skip_nonfinite (whose step-count
+        rollback reads back from the device)."""
+        if self.skip_nonfinite:
+            raise MpoError(1, "graph step: skip_nonfinite needs a device read-back per step")
+        if self._hooks or self._native is not None:
+            raise MpoError(1, "graph step: not with the backward hooks (they step inside backward)")
+        self._graph = {}
+        self._graph_seq = 0
+
+    def prepare_step(self):
+        """Host side of a graph-replayed step (see enable_graph_step): advance the step counts and
+        write this step's hyper-parameters into the pinned blocks the captured copies read."""
+        if getattr(self, "_graph", None) is None:
+            raise MpoError(1, "call enable_graph_step() first")
+        # never rewrite a block an issued step still has to copy: wait until the device echoed the
+        # last sequence number -- or the stream ran dry (a block prepared but never replayed will
+        # not be copied any more)
+        stream = torch.cuda.current_stream()
+        for ent in self._graph.values():
+            while int(ent["ack"][0]) != self._graph_seq and not stream.query():
+                time.sleep(0)
+        self._graph_seq += 1
+        self._graph_tables(advance=True)
+
+    def _graph_tables(self, advance):
+        params = [p for g in self.param_groups for p in g["params"] if p.grad is not None]
+        by_dtype = {}
+        for p in params:
+            by_dtype.setdefault((p.dtype, p.grad.dtype), []).append(p)
+        for key, plist in by_dtype.items():
+            tab = self._table_for(plist)
+            ent = self._graph.get(key)
+            if ent is not None and ent["tab"] is not tab:
+                raise MpoError(1, "graph step: the gradients moved since capture (keep them allocated)")
+            if advance:
+                self._steps_np[tab._idx] += 1
+            groups = sorted(set(tab._group_of))
+            step_of = {}
+            for gi, stp in zip(tab._group_of, self._steps_np[tab._idx].tolist()):
+                if step_of.setdefault(gi, stp) != stp:
+                    raise MpoError(1, "graph step: parameters of one group at different step counts")
+            hp_index = [groups.index(gi) for gi in tab._group_of]
+            if hp_index != getattr(tab, "_hp_index", None):
+                if ent is not None:
+                    raise MpoError(1, "graph step: the group layout changed since capture")
+                for i, h in enumerate(hp_index):
+                    tab.arr[i].hp = h
+                tab._hp_index = hp_index
+            hps = [self._hp(self.param_groups[gi], max(1, step_of[gi])) for gi in groups]
+            if ent is None:
+                nb = api.hp_block_bytes(self._kind, self.exact)
+                dev = params[0].device
+                ent = self._graph[key] = {"tab": tab, "host": torch.empty(nb, dtype=torch.uint8, pin_memory=True),
+                                          "dev": torch.empty(nb, dtype=torch.uint8, device=dev),
+                                          "ack": torch.full((1,), -1, dtype=torch.int64, pin_memory=True)}
+            ent["hps"] = hps
+            api.hp_block_fill(self._kind, hps, ent["host"], seq=self._graph_seq, exact=self.exact)
+
+    def _graph_step(self):
+        if not self._graph:
+            self._graph_tables(advance=False)      # first call (typically the capture): set up only
+        ws = self._ws(self.param_groups[0]["params"][0].device) if self._needs_norm() else None
+        for ent in self._graph.values():
+            api.mpo_step_graphed(self._kind, ent["tab"], ent["hps"], ent["host"], ent["dev"], ack=ent["ack"],
+                                 norm_ws=ws, exact=self.exact)
 
     # -- hook mode ---------------------------------------------------------------------------
     def install_backward_hooks(self, batch_below: int = 1 << 16, flush_elems: int = 1 << 22, native: bool = True):
