@@ -1026,6 +1026,40 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024, modes=("hook", "tw
                     for p in model.parameters():
                         p.grad = None
                 return loss
+        elif mode == "two_phase_graph":
+            # the whole training iteration -- forward, backward, the residual AdamW step -- captured
+            # once as a CUDA graph and replayed (the step's hyper-parameters travel through the
+            # pinned block of mpo_step_graphed): no per-kernel host cost at all
+            opt = mpo.ResidualAdamW(model.parameters(), fmt=torch.bfloat16, **hp)
+            x_in, y_in = idx[:, :-1].contiguous(), idx[:, 1:].contiguous()
+
+            def loss_static():
+                logits = model(x_in).logits
+                return torch.nn.functional.cross_entropy(logits.float().reshape(-1, logits.shape[-1]),
+                                                         y_in.reshape(-1))
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):       # warm-up: every gradient buffer allocated once
+                for _ in range(2):
+                    loss_static().backward()
+            torch.cuda.current_stream().wait_stream(side)
+            opt.enable_graph_step()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for p in model.parameters():
+                    p.grad.zero_()
+                loss_g = loss_static()
+                loss_g.backward()
+                opt.step()
+
+            def step(rec=None):
+                opt.prepare_step()
+                if rec is not None:
+                    rec[0].record()
+                graph.replay()
+                if rec is not None:
+                    rec[1].record()
+                return loss_g
         elif mode in ("sharded_two_phase", "sharded_bucketed"):
             # hook mode x sharding at world 1: bucket steps issued from the hooks
             # on a side stream overlap the rest of backward, vs backward + one sharded step
@@ -1139,6 +1173,10 @@ def hook_mode_secondary(steps=8, warmup=3, batch=8, seq=1024, modes=("hook", "tw
             "two_phase_backward_plus_step_ms": t["backward_ms"] + t["after_backward_ms"],
             "hook_backward_ms": h["backward_ms"],
             "hook_vs_two_phase_train_step": h["ms_per_train_step"] / t["ms_per_train_step"] - 1.0}
+    except Exception:
+        pass
+    try:   # the same iteration as one CUDA graph (mpo_step_graphed) vs eager
+        out["graph_vs_eager_two_phase"] = out["two_phase_graph"]["ms_per_train_step"] / out["two_phase"]["ms_per_train_step"]
     except Exception:
         pass
     try:   # hook mode x sharding at world 1: bucket steps overlapping backward vs a step after it
@@ -1324,7 +1362,8 @@ def main():
             line["secondary"]["gpt2_hook_mode"] = {"error": f"{type(ex).__name__}: {ex}"}
         try:   # small activations (B=1, T=128): gradients are a large share of the peak
             line["secondary"]["gpt2_hook_mode_b1_t128"] = hook_mode_secondary(
-                steps=20, batch=1, seq=128, modes=("hook", "two_phase", "amp_fp32_master", "hook_python"))
+                steps=20, batch=1, seq=128,
+                modes=("hook", "two_phase", "amp_fp32_master", "hook_python", "two_phase_graph"))
         except Exception as ex:
             line["secondary"]["gpt2_hook_mode_b1_t128"] = {"error": f"{type(ex).__name__}: {ex}"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
