@@ -209,3 +209,24 @@ def test_grouped_sharded_and_sumsq_validation(libs):
     rc, msg = _status(L, L.mpo_fused_backward_hook_step(_lib.MPO_ADAM, _lib.MPO_BF16, _lib.MPO_BF16, C.byref(one),
                                                         C.byref(ready), None, None))
     assert rc == _lib.MPO_EINVAL and "norm_ready" in msg
+
+
+def test_graphed_step_validation(libs):
+    """mpo_hp_block_fill / mpo_step_graphed validate before touching the device (no GPU needed)."""
+    _lib, L, _ = libs
+    assert L.mpo_hp_block_bytes(_lib.MPO_ADAM) > L.mpo_hp_block_bytes(_lib.MPO_SGD) > 16
+    hp = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1, 0)
+    buf = (C.c_uint8 * L.mpo_hp_block_bytes(_lib.MPO_ADAM))()
+    assert L.mpo_hp_block_fill(_lib.MPO_ADAM, C.byref(hp), 1, 7, buf) == _lib.MPO_OK
+    assert bytes(buf[-16:-8]) == (7).to_bytes(8, "little")        # the sequence number slot
+    assert L.mpo_hp_block_fill(_lib.MPO_ADAM, C.byref(hp), 0, 7, buf) == _lib.MPO_EINVAL
+    assert L.mpo_hp_block_fill(9, C.byref(hp), 1, 7, buf) == _lib.MPO_EINVAL
+    bad = _lib.AdamHP(float("inf"), 0.9, 0.999, 1e-8, 0.0, 1.0, 0.0, 1, 0, 1, 0)
+    assert L.mpo_hp_block_fill(_lib.MPO_ADAM, C.byref(bad), 1, 7, buf) == _lib.MPO_EINVAL
+    tab = (_lib.Tensor * 1)(_lib.Tensor(16, 32, 48, 64, 80, 8, 0, 0))
+    rc, msg = _status(L, L.mpo_step_graphed(_lib.MPO_ADAM, _lib.MPO_BF16, _lib.MPO_BF16, tab, 1, C.byref(hp), 1, None,
+                                            4096, None, None, None))
+    assert rc == _lib.MPO_EINVAL and "block" in msg
+    rc, msg = _status(L, L.mpo_step_graphed(_lib.MPO_ADAM, _lib.MPO_BF16, _lib.MPO_BF16, tab, 1, C.byref(hp), 1, buf,
+                                            4100, None, None, None))
+    assert rc == _lib.MPO_EALIGN
