@@ -78,11 +78,8 @@ mpo_status FormatOps<SF>::nvls(int kind, void* value_mc, const void* value_uc, c
 template <>
 mpo_status FormatOps<SF>::p2p(int kind, const Peers& peers, int world, int rank, void* resid, float* m, float* v,
                               int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak, cudaStream_t s) {
-    static const bool lsu = [] {
-        const char* e = std::getenv("MPO_P2P_KERNEL");
-        return e && std::strcmp(e, "lsu") == 0;
-    }();
-    if (lsu) {   // per-thread 128-bit loads of every stream (A/B; round-1 kernel)
+    const char* env = std::getenv("MPO_P2P_KERNEL");   // read per call: tests cover both kernels
+    if (env && std::strcmp(env, "lsu") == 0) {   // per-thread 128-bit loads of every stream (round-1 kernel)
         const int64_t grid = grid_for((n / kUnitEl + kThreads - 1) / kThreads, 8);
         if (kind == MPO_ADAM)
             p2p_step_kernel<SF, AdamOp><<<unsigned(grid), kThreads, 0, s>>>(peers, world, rank, resid, m, v, shard_base,

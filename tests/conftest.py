@@ -26,3 +26,10 @@ def step_kernel(request, monkeypatch):
     load kernel (the library picks by launch size; MPO_STEP_KERNEL forces one, read per launch)."""
     monkeypatch.setenv("MPO_STEP_KERNEL", request.param)
     return request.param
+
+
+@pytest.fixture(params=["tma", "lsu"])
+def p2p_kernel(request, monkeypatch):
+    """Run a P2P fused-step test through both kernels (bulk-copy pipeline / per-thread loads)."""
+    monkeypatch.setenv("MPO_P2P_KERNEL", request.param)
+    return request.param
