@@ -799,6 +799,61 @@ def _secondary_one(name, steps, warmup, hbm_peak, scheme="rne"):
         return res
 
 
+def torch_comparators_secondary(name, hbm_peak, steps=20, warmup=3):
+    """SURVEY 8(a) "same-box comparators": the optimizer steps the paper's method replaces, on the
+    same parameter set (one tensor per parameter shape), timed like the headline:
+      * amp_fp32_master: torch.optim.AdamW(fused=True) over fp32 master weights with fp32 grads,
+        then the per-iteration recast of the masters into the bf16/fp16 model copy (the AMP
+        inventory the paper compares with, P:135) -- 28 + 6 B/param;
+      * low_precision_only: torch.optim.AdamW(fused=True) directly on the 16-bit parameters with
+        16-bit grads and (torch's choice) 16-bit state: no master, lossy (the paper's "fp16" row,
+        P:135) -- 14 B/param.
+    Same hyper-parameters as the workload; grads N(0, 1e-3), weights N(0, 0.02), seeded."""
+    import torch
+    from synth import workloads
+    wl, fmt, kind, hpkw, cfg = WORKLOADS[name]
+    assert kind == "adam"
+    sizes = workloads.sizes(wl)
+    P = sum(sizes)
+    tdt = torch.float16 if fmt == "fp16" else torch.bfloat16
+    hp = dict(lr=hpkw["lr"], betas=(hpkw["beta1"], hpkw["beta2"]), eps=hpkw["eps"],
+              weight_decay=hpkw.get("weight_decay", 0.0))
+    opt_cls = torch.optim.AdamW if hpkw.get("adamw", False) else torch.optim.Adam
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(0xB0B)
+    res = {"config": f"BASELINE configs[{cfg}] parameter set {wl} ({P} params, {len(sizes)} tensors), "
+                     f"torch {opt_cls.__name__}(fused=True), hyper-parameters of the workload"}
+
+    def run(master_dtype, model_dtype):
+        ps = [torch.empty(n, dtype=master_dtype, device="cuda").normal_(0, 0.02, generator=gen) for n in sizes]
+        for p in ps:
+            p.grad = torch.empty_like(p).normal_(0, 1e-3, generator=gen)
+        model = [torch.empty(n, dtype=model_dtype, device="cuda") for n in sizes] if model_dtype != master_dtype else None
+        opt = opt_cls(ps, fused=True, **hp)
+
+        def step():
+            opt.step()
+            if model is not None:
+                torch._foreach_copy_(model, ps)      # the AMP recast of the masters into the model copy
+        ms, _ = timed(step, steps, warmup)
+        esz = ps[0].element_size()
+        st = opt.state[ps[0]]["exp_avg"].element_size()
+        b = (2 * esz + 2 * st) + (esz + 2 * st)      # read p, g, m, v; write p, m, v
+        if model is not None:
+            b += esz + model[0].element_size()          # recast: read master, write model copy
+        out = {"params_per_s": P / (ms * 1e-3), "ms_per_step": ms, "steps": steps, "bytes_per_param": b,
+               "achieved_gbs": P * b / (ms * 1e-3) / 1e9,
+               "frac_of_measured_hbm": P * b / (ms * 1e-3) / 1e9 / hbm_peak,
+               "state_dtype": str(opt.state[ps[0]]["exp_avg"].dtype).replace("torch.", "")}
+        del opt, ps, model
+        torch.cuda.empty_cache()
+        return out
+
+    res["amp_fp32_master"] = run(torch.float32, tdt)
+    res["low_precision_only"] = run(tdt, tdt)
+    return res
+
+
 def split_reconstruct_secondary(hbm_peak, n=1 << 28, steps=50, warmup=5):
     """a1 / a2 (one-off conversions): mpo_split of n fp32 weights into bf16 value + int16
     residual and mpo_reconstruct back, 8 B/param each (read 4 + write 2 + 2, read 2 + 2 + write 4)."""
@@ -1335,6 +1390,18 @@ def main():
             line["secondary"]["resnet50_multi_vs_per_tensor"] = per_tensor_secondary("resnet50_sgd", hbm_peak)
         except Exception as ex:
             line["secondary"]["resnet50_multi_vs_per_tensor"] = {"error": f"{type(ex).__name__}: {ex}"}
+        for cname, mpo_ms in (("gpt2_adamw", line["secondary"].get("gpt2_adamw", {}).get("ms_per_step")),
+                              ("llama7b_adam", ms if args.workload == "llama7b_adam" else None)):
+            try:
+                cmp_ = torch_comparators_secondary(cname, hbm_peak)
+                if isinstance(mpo_ms, float):
+                    cmp_["mpo_step_ms"] = mpo_ms
+                    cmp_["mpo_speedup_vs_amp_fp32_master"] = cmp_["amp_fp32_master"]["ms_per_step"] / mpo_ms
+                    cmp_["mpo_speedup_vs_low_precision_only"] = cmp_["low_precision_only"]["ms_per_step"] / mpo_ms
+                line["secondary"][f"torch_fused_adam_{cname}"] = cmp_
+            except Exception as ex:
+                line["secondary"][f"torch_fused_adam_{cname}"] = {"error": f"{type(ex).__name__}: {ex}"}
+            torch.cuda.empty_cache()
         try:
             line["secondary"]["flat1m_adam"] = flat1m_secondary(hbm_peak)
         except Exception as ex:
@@ -1370,8 +1437,9 @@ def main():
         line["cpu_baseline"] = cpu_baseline(args.workload)
     if rank == 0:
         emit(line)
-    if dist is not None:
-        dist.destroy_process_group()
+    import torch.distributed as tdist
+    if tdist.is_initialized():   # the N>1 group, or the single-rank group of the world-1 sharded secondaries
+        tdist.destroy_process_group()
 
 
 if __name__ == "__main__":
