@@ -319,6 +319,23 @@ mpo_status mpo_nvls_sharded_step(mpo_optim kind, int32_t rank, int32_t world, mp
                                  void* resid_shard, float* m_shard, float* v_shard,
                                  int64_t n_total, const void* hp, mpo_stream stream);
 
+/* Validation entry point of the NVLS kernel on a box without a multicast object (one GPU):
+ * the SAME kernel as mpo_nvls_sharded_step (indexing, state streams, update, re-split, fences),
+ * with its two multicast operations performed over ordinary peer pointers instead --
+ *   multimem.ld_reduce.add.acc::f32  ->  the ranks' 8 gradients summed in fp32 in rank order
+ *                                         and rounded once to the 16-bit format (RNE; NaN ->
+ *                                         0x7FFF), equal to the switch's result whenever the
+ *                                         fp32 sum is order-independent (exact-sum inputs);
+ *   multimem.st                      ->  a store into every rank's replica.
+ * Arguments as mpo_p2p_sharded_step (value_peers / grad_peers: HOST arrays of `world` device
+ * pointers, value_peers[rank] is the replica read), constraints as mpo_nvls_sharded_step
+ * (MPO_FP16 | MPO_BF16 RNE storage, grads of the same dtype, no pre-pass); 1 <= world <= 8.
+ * Not a product path: the multi-GPU path is mpo_nvls_sharded_step on a real multicast object. */
+mpo_status mpo_nvls_emulated_step(mpo_optim kind, int32_t rank, int32_t world, mpo_dtype vdt,
+                                  void* const* value_peers, const void* const* grad_peers,
+                                  void* resid_shard, float* m_shard, float* v_shard,
+                                  int64_t n_total, const void* hp, mpo_stream stream);
+
 /* The sharded step fused with its collectives over NVLink peer memory (the
  * P2P form; needs no multicast object): one kernel per rank that, for each 8-element unit of its
  * shard [rank*S, (rank+1)*S), S = n_total/world,

@@ -26,7 +26,8 @@ SYMBOLS = ("mpo_split", "mpo_reconstruct", "mpo_sgd_step", "mpo_adam_step", "mpo
            "mpo_fused_backward_hook_step", "mpo_sharded_step", "mpo_last_error", "mpo_build_exact",
            "mpo_launch_count", "mpo_selfcheck_fastmath", "mpo_nvls_sharded_step", "mpo_nvls_alloc_local",
            "mpo_nvls_free_local", "mpo_p2p_sharded_step", "mpo_grad_sumsq", "mpo_sharded_step_grouped",
-           "mpo_comm_check", "mpo_hp_block_bytes", "mpo_hp_block_fill", "mpo_step_graphed")
+           "mpo_comm_check", "mpo_hp_block_bytes", "mpo_hp_block_fill", "mpo_step_graphed",
+           "mpo_nvls_emulated_step")
 
 
 class MpoError(RuntimeError):
@@ -100,6 +101,8 @@ def _declare(L):
     L.mpo_nvls_free_local.restype = C.c_int
     L.mpo_p2p_sharded_step.argtypes = [D, I32, I32, D, P, P, P, P, P, I64, P, P]
     L.mpo_p2p_sharded_step.restype = C.c_int
+    L.mpo_nvls_emulated_step.argtypes = [D, I32, I32, D, P, P, P, P, P, I64, P, P]
+    L.mpo_nvls_emulated_step.restype = C.c_int
 
 
 def load(exact: bool = True):

@@ -792,22 +792,23 @@ MPO_API mpo_status mpo_p2p_sharded_step(mpo_optim kind, int32_t rank, int32_t wo
 // ------------------------------------------------------------------------------------------
 // NVLS (NVLink SHARP) fused sharded step and a single-device multicast allocator for tests
 // ------------------------------------------------------------------------------------------
-MPO_API mpo_status mpo_nvls_sharded_step(mpo_optim kind, int32_t rank, int32_t world, mpo_dtype vdt, void* value_mc,
-                                         const void* value_uc, const void* grad_mc, void* resid_shard, float* m_shard,
-                                         float* v_shard, int64_t n_total, const void* hp, mpo_stream stream) {
-    g_err.clear();
+namespace {
+// Shared validation + dispatch of the NVLS step: `emu` == nullptr launches the multicast kernel,
+// otherwise its emulation over `world` peer buffers (mpo_nvls_emulated_step).
+mpo_status nvls_step(mpo_optim kind, int32_t rank, int32_t world, mpo_dtype vdt, void* value_mc, const void* value_uc,
+                     const void* grad_mc, const Peers* emu, void* resid_shard, float* m_shard, float* v_shard,
+                     int64_t n_total, const void* hp, cudaStream_t s) {
     mpo_status st;
-    if (world < 1 || rank < 0 || rank >= world) return fail(MPO_EINVAL, "bad rank / world");
+    if (world < 1 || rank < 0 || rank >= world || (emu && world > kMaxPeers)) return fail(MPO_EINVAL, "bad rank / world");
     if (n_total < 0 || n_total % (int64_t(8) * world) != 0)
         return fail(MPO_EINVAL, "n_total must be a non-negative multiple of 8*world");
     if (vdt != MPO_FP16 && vdt != MPO_BF16) return fail(MPO_EDTYPE, "the NVLS step takes MPO_FP16 or MPO_BF16 values");
     if (!hp) return fail(MPO_EINVAL, "NULL hyper-parameters");
     if (n_total == 0) return MPO_OK;
-    if (!value_mc || !value_uc || !grad_mc || !resid_shard) return fail(MPO_EINVAL, "NULL buffer");
-    if (!aligned16(value_mc) || !aligned16(value_uc) || !aligned16(grad_mc) || !aligned16(resid_shard))
+    if ((!emu && (!value_mc || !grad_mc)) || !value_uc || !resid_shard) return fail(MPO_EINVAL, "NULL buffer");
+    if ((!emu && (!aligned16(value_mc) || !aligned16(grad_mc))) || !aligned16(value_uc) || !aligned16(resid_shard))
         return fail(MPO_EALIGN, "buffer not 16-byte aligned");
     const int64_t shard = n_total / world;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (kind == MPO_ADAM) {
         const mpo_adam_hp* h = static_cast<const mpo_adam_hp*>(hp);
         if ((st = check_adam_hp(h, 1)) != MPO_OK) return st;
@@ -818,9 +819,9 @@ MPO_API mpo_status mpo_nvls_sharded_step(mpo_optim kind, int32_t rank, int32_t w
         const AdamK k = derive_adam(*h);
         if (vdt == MPO_BF16)
             return FormatOps<MPO_BF16>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, v_shard,
-                                             rank * shard, shard, nullptr, &k, s);
+                                             rank * shard, shard, nullptr, &k, emu, world, s);
         return FormatOps<MPO_FP16>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, v_shard,
-                                         rank * shard, shard, nullptr, &k, s);
+                                         rank * shard, shard, nullptr, &k, emu, world, s);
     }
     if (kind == MPO_SGD) {
         const mpo_sgd_hp* h = static_cast<const mpo_sgd_hp*>(hp);
@@ -831,11 +832,40 @@ MPO_API mpo_status mpo_nvls_sharded_step(mpo_optim kind, int32_t rank, int32_t w
         const SgdK k = derive_sgd(*h);
         if (vdt == MPO_BF16)
             return FormatOps<MPO_BF16>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, nullptr,
-                                             rank * shard, shard, &k, nullptr, s);
+                                             rank * shard, shard, &k, nullptr, emu, world, s);
         return FormatOps<MPO_FP16>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, nullptr,
-                                         rank * shard, shard, &k, nullptr, s);
+                                         rank * shard, shard, &k, nullptr, emu, world, s);
     }
     return fail(MPO_EINVAL, "unknown optimizer kind");
+}
+}  // namespace
+
+MPO_API mpo_status mpo_nvls_sharded_step(mpo_optim kind, int32_t rank, int32_t world, mpo_dtype vdt, void* value_mc,
+                                         const void* value_uc, const void* grad_mc, void* resid_shard, float* m_shard,
+                                         float* v_shard, int64_t n_total, const void* hp, mpo_stream stream) {
+    g_err.clear();
+    return nvls_step(kind, rank, world, vdt, value_mc, value_uc, grad_mc, nullptr, resid_shard, m_shard, v_shard,
+                     n_total, hp, static_cast<cudaStream_t>(stream));
+}
+
+MPO_API mpo_status mpo_nvls_emulated_step(mpo_optim kind, int32_t rank, int32_t world, mpo_dtype vdt,
+                                          void* const* value_peers, const void* const* grad_peers, void* resid_shard,
+                                          float* m_shard, float* v_shard, int64_t n_total, const void* hp,
+                                          mpo_stream stream) {
+    g_err.clear();
+    if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+        return fail(MPO_EINVAL, "bad rank / world (1 <= world <= 8)");
+    if (!value_peers || !grad_peers) return fail(MPO_EINVAL, "NULL peer pointer array");
+    Peers peers{};
+    for (int k = 0; k < world; ++k) {
+        if (!value_peers[k] || !grad_peers[k]) return fail(MPO_EINVAL, "NULL peer buffer (rank " + std::to_string(k) + ")");
+        if (!aligned16(value_peers[k]) || !aligned16(grad_peers[k]))
+            return fail(MPO_EALIGN, "peer buffer not 16-byte aligned (rank " + std::to_string(k) + ")");
+        peers.g[k] = static_cast<const uint16_t*>(grad_peers[k]);
+        peers.v[k] = static_cast<uint16_t*>(value_peers[k]);
+    }
+    return nvls_step(kind, rank, world, vdt, nullptr, value_peers[rank], nullptr, &peers, resid_shard, m_shard,
+                     v_shard, n_total, hp, static_cast<cudaStream_t>(stream));
 }
 
 namespace {

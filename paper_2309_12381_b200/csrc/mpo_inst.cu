@@ -62,15 +62,23 @@ mpo_status FormatOps<SF>::reconstruct(const void* value, const void* resid, floa
 template <>
 mpo_status FormatOps<SF>::nvls(int kind, void* value_mc, const void* value_uc, const void* grad_mc, void* resid,
                                float* m, float* v, int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak,
-                               cudaStream_t s) {
+                               const Peers* emu, int world, cudaStream_t s) {
+    constexpr int B = Fmt<SF>::base;
     const int64_t grid = grid_for((n / kUnitEl + kThreads - 1) / kThreads, 8);
-    auto* vm = static_cast<uint16_t*>(value_mc);
     auto* vu = static_cast<const uint16_t*>(value_uc);
-    auto* gm = static_cast<const uint16_t*>(grad_mc);
-    if (kind == MPO_ADAM)
-        nvls_step_kernel<SF, AdamOp><<<unsigned(grid), kThreads, 0, s>>>(vm, vu, gm, resid, m, v, shard_base, n, *ak);
-    else
-        nvls_step_kernel<SF, SgdOp><<<unsigned(grid), kThreads, 0, s>>>(vm, vu, gm, resid, m, v, shard_base, n, *sk);
+    if (emu) {
+        const NvlsEmulated<B> mc{*emu, world};
+        if (kind == MPO_ADAM)
+            nvls_step_kernel<SF, AdamOp><<<unsigned(grid), kThreads, 0, s>>>(mc, vu, resid, m, v, shard_base, n, *ak);
+        else
+            nvls_step_kernel<SF, SgdOp><<<unsigned(grid), kThreads, 0, s>>>(mc, vu, resid, m, v, shard_base, n, *sk);
+    } else {
+        const NvlsMulticast<B> mc{static_cast<uint16_t*>(value_mc), static_cast<const uint16_t*>(grad_mc)};
+        if (kind == MPO_ADAM)
+            nvls_step_kernel<SF, AdamOp><<<unsigned(grid), kThreads, 0, s>>>(mc, vu, resid, m, v, shard_base, n, *ak);
+        else
+            nvls_step_kernel<SF, SgdOp><<<unsigned(grid), kThreads, 0, s>>>(mc, vu, resid, m, v, shard_base, n, *sk);
+    }
     ++g_launches;
     return check_launch("nvls_step_kernel");
 }

@@ -1234,10 +1234,62 @@ __device__ __forceinline__ void multimem_st_v4(void* mc, const uint4& v) {
                  : "memory");
 }
 
-template <int SF, class Op>
-__global__ void __launch_bounds__(kThreads) nvls_step_kernel(uint16_t* __restrict__ value_mc,
-                                                             const uint16_t* __restrict__ value_uc,
-                                                             const uint16_t* __restrict__ grad_mc, void* resid,
+// The kernel reaches the multicast object through an access policy: NvlsMulticast issues the
+// real multimem instructions; NvlsEmulated (validation on one device, where no multicast team
+// can be created) performs the same two operations with ordinary loads/stores over the ranks'
+// unicast buffers -- the sum of every rank's 8 gradients in fp32 in rank order, rounded once to
+// the 16-bit format (RNE, canonical NaN), which is what ld_reduce.add.acc::f32 returns whenever
+// the fp32 sum does not depend on the order (exact-sum inputs), and a store into every replica.
+// Everything else in the kernel (indexing, state streams, update, re-split, fences) is shared.
+template <int B>
+struct NvlsMulticast {
+    static constexpr bool kMulticast = true;
+    uint16_t* value_mc;
+    const uint16_t* grad_mc;
+    __device__ __forceinline__ uint4 grad_sum(int64_t i) const { return multimem_ld_reduce_v4<B>(grad_mc + i); }
+    __device__ __forceinline__ void store_value(int64_t i, const uint4& h) const { multimem_st_v4(value_mc + i, h); }
+};
+
+constexpr int kMaxPeers = 8;
+struct Peers {
+    const uint16_t* g[kMaxPeers];
+    uint16_t* v[kMaxPeers];
+};
+
+template <int B>
+struct NvlsEmulated {
+    static constexpr bool kMulticast = false;
+    Peers P;
+    int world;
+    __device__ __forceinline__ uint4 grad_sum(int64_t i) const {
+        float sum[8];
+        GradUnit<B> u;
+        u.a = ldv(P.g[0] + i);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sum[j] = grad_at<B>(u, j);
+        for (int k = 1; k < world; ++k) {
+            u.a = ldv(P.g[k] + i);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sum[j] = sum[j] + grad_at<B>(u, j);
+        }
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t h = round2<B>(sum[2 * j], sum[2 * j + 1]);
+            if (sum[2 * j] != sum[2 * j]) h = (h & 0xFFFF0000u) | 0x7FFFu;
+            if (sum[2 * j + 1] != sum[2 * j + 1]) h = (h & 0x0000FFFFu) | 0x7FFF0000u;
+            w[j] = h;
+        }
+        return make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    __device__ __forceinline__ void store_value(int64_t i, const uint4& h) const {
+        for (int k = 0; k < world; ++k) stv(P.v[k] + i, h);
+    }
+};
+
+template <int SF, class Op, class MC>
+__global__ void __launch_bounds__(kThreads) nvls_step_kernel(const __grid_constant__ MC mc,
+                                                             const uint16_t* __restrict__ value_uc, void* resid,
                                                              float* __restrict__ m, float* __restrict__ v,
                                                              int64_t shard_base, int64_t n,
                                                              const __grid_constant__ typename Op::K c) {
@@ -1248,7 +1300,7 @@ __global__ void __launch_bounds__(kThreads) nvls_step_kernel(uint16_t* __restric
     for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < nunits; u += stride) {
         const int64_t e = u * kUnitEl;                      // index inside the shard
         GradUnit<B> gu;
-        gu.a = multimem_ld_reduce_v4<B>(grad_mc + shard_base + e);
+        gu.a = mc.grad_sum(shard_base + e);                 // reduce-scatter of this unit
         gu.b = gu.a;
         const uint4 hv = ldv(value_uc + shard_base + e);
         const ResidUnit<SF> rv = ld_resid<SF>(resid, e);
@@ -1270,7 +1322,7 @@ __global__ void __launch_bounds__(kThreads) nvls_step_kernel(uint16_t* __restric
         uint4 ho;
         ResidUnit<SF> ro;
         process_unit<SF, B, Op, false>(hv, rv, gu, mm, vv, c, 1.0f, 0u, shard_base + e, ho, ro);
-        multimem_st_v4(value_mc + shard_base + e, ho);     // every rank's replica
+        mc.store_value(shard_base + e, ho);                 // all-gather: every rank's replica
         st_resid<SF>(resid, e, ro);
         if (has_m) {
             stf8(m + e, mm);
@@ -1281,7 +1333,7 @@ __global__ void __launch_bounds__(kThreads) nvls_step_kernel(uint16_t* __restric
     }
     // make the multicast stores visible system-wide, and ordered with later accesses through the
     // unicast alias of the same memory
-    asm volatile("fence.proxy.alias;" ::: "memory");
+    if constexpr (MC::kMulticast) asm volatile("fence.proxy.alias;" ::: "memory");
     asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
@@ -1294,11 +1346,6 @@ __global__ void __launch_bounds__(kThreads) nvls_step_kernel(uint16_t* __restric
 // values into EVERY rank's replica (P2P stores).  This is the reduce-scatter + update +
 // all-gather of mpo_sharded_step as one kernel: no collective launches, no reduced-gradient
 // buffer, and the NVLink transfers overlap the arithmetic unit by unit.
-constexpr int kMaxPeers = 8;
-struct Peers {
-    const uint16_t* g[kMaxPeers];
-    uint16_t* v[kMaxPeers];
-};
 
 template <int SF, class Op>
 __global__ void __launch_bounds__(kThreads) p2p_step_kernel(const __grid_constant__ Peers P, int world, int rank,
@@ -1612,8 +1659,11 @@ struct FormatOps {
     static mpo_status split(const float* w, void* value, void* resid, int64_t n, uint64_t seed, uint32_t stream,
                             cudaStream_t s);
     static mpo_status reconstruct(const void* value, const void* resid, float* w, int64_t n, cudaStream_t s);
+    // emu == nullptr: the multicast kernel on value_mc / grad_mc; otherwise the emulated access
+    // over emu's `world` peer buffers (value_mc / grad_mc unused)
     static mpo_status nvls(int kind, void* value_mc, const void* value_uc, const void* grad_mc, void* resid, float* m,
-                           float* v, int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak, cudaStream_t s);
+                           float* v, int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak,
+                           const Peers* emu, int world, cudaStream_t s);
     static mpo_status p2p(int kind, const Peers& peers, int world, int rank, void* resid, float* m, float* v,
                           int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak, cudaStream_t s);
 };
