@@ -55,6 +55,16 @@ DEFAULT_WORKLOAD = "llama7b_adam"
 BYTES_PER_PARAM = {"sgd": 18, "adam": 26, "adam_clip": 28}
 
 
+def workload_config(name):
+    """The bench line's `config` (identical in both arms): the workload and its hyper-parameters."""
+    from synth import workloads
+    wl, fmt, kind, hp, cfg = WORKLOADS[name]
+    sizes = workloads.sizes(wl)
+    return {"workload": f"{name}: BASELINE configs[{cfg}] parameter set {wl} ({sum(sizes)} params, "
+                        f"{len(sizes)} tensors)",
+            "optimizer": kind, "hyper_parameters": hp, "value_dtype": fmt}
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -756,8 +766,9 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "storage": f"{fmt} value + int16 residual, fp32 optimizer state", "data": "synthetic",
-            "config": {"workload": f"{name} ({wl}, BASELINE configs[{WORKLOADS[name][4]}])",
-                       "sample_params_per_step": n, "params_in_workload": P},
+            "config": workload_config(name),
+            "sample": {"params_per_step": n, "params_in_workload": P,
+                       "note": "each step runs the oracle over a bounded prefix of the workload's recipe"},
             "cpu_baseline": {"value": value, "unit": "params/s", "cores": threads, "kind": "oracle", "cpu": cpu_model(),
                              "host_cores": len(os.sched_getaffinity(0)),
                              "sample": f"{n} of {P} params per step, {args.steps} steps; OpenMP build, "
@@ -1351,13 +1362,11 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
         "dtype": "f32", "storage": f"{wl.fmt} value + int16 residual, fp32 optimizer state", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: BASELINE configs[{wl.cfg}] parameter set "
-                               f"{WORKLOADS[args.workload][0]} ({wl.P} params, {wl.ntensors} tensors)",
-                   "optimizer": wl.kind, "hyper_parameters": wl.hpkw, "value_dtype": wl.fmt,
-                   "path": "mpo_sharded_step (NCCL RS -> shard update -> NCCL AG)" if world > 1
-                   else "mpo_sgd_step/mpo_adam_step, one multi-tensor launch",
-                   "parallelism": f"dp{world} sharded optimizer state" if world > 1 else "single GPU",
-                   "l2": f"working set {alg_bytes / 1e6:.0f} MB/step > L2 {L2_BYTES / 2**20:.0f} MiB (no flush)"},
+        "config": workload_config(args.workload),
+        "path": "mpo_sharded_step (NCCL RS -> shard update -> NCCL AG)" if world > 1
+                else "mpo_sgd_step/mpo_adam_step, one multi-tensor launch",
+        "parallelism": f"dp{world} sharded optimizer state" if world > 1 else "single GPU",
+        "l2": f"working set {alg_bytes / 1e6:.0f} MB/step > L2 {L2_BYTES / 2**20:.0f} MiB (no flush)",
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
                      "frac_of_8tbs_spec": achieved / 8000.0,
