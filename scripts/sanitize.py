@@ -1,6 +1,7 @@
 """Small runs of every kernel family for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck): split/reconstruct, SGD and Adam steps (with clip, found-inf skip, ragged tails, every
-storage format), the hook entry and the sharded entry at world 1."""
+storage format), the hook entry and the sharded entry at world 1, the P2P and the emulated NVLS
+fused sharded steps, and the graph-replayed step."""
 import os
 import sys
 
@@ -80,5 +81,37 @@ v, r = mpo.mpo_split(torch.randn(big, device=dev) * 0.02, torch.float16)
 mpo.mpo_sgd_step(mpo.TensorTable([v], [r], [(torch.randn(big, device=dev) * 1e-2).to(torch.float16)],
                                  [torch.zeros(big, device=dev)], [None]), mpo.SgdParams(lr=0.1, momentum=0.9))
 mpo.mpo_reconstruct(v, r)
+# round 2 (late): the NVLS kernel with its multicast operations emulated over 2 ranks' buffers
+# (mpo_nvls_emulated_step), the LSU P2P kernel, and the graph-replayed step (eager prepare + step,
+# and one captured step replayed)
+n2 = 2 * 4104
+for k in range(W2):
+    S = n2 // W2
+    api.mpo_nvls_emulated_step(MPO_ADAM, k, W2, [t.data_ptr() for t in reps], [t.data_ptr() for t in grads],
+                               torch.zeros(S, dtype=torch.int16, device=dev), torch.zeros(S, device=dev),
+                               torch.zeros(S, device=dev), n2, mpo.AdamParams(lr=1e-3, step=1), torch.bfloat16)
+    api.mpo_nvls_emulated_step(MPO_SGD, k, W2, [t.data_ptr() for t in reps], [t.data_ptr() for t in grads],
+                               torch.zeros(S, dtype=torch.int16, device=dev), torch.zeros(S, device=dev), None, n2,
+                               mpo.SgdParams(lr=0.1, momentum=0.9), torch.bfloat16)
+os.environ["MPO_P2P_KERNEL"] = "lsu"
+for k in range(W2):
+    S = n2 // W2
+    api.mpo_p2p_sharded_step(MPO_ADAM, k, W2, [t.data_ptr() for t in reps], [t.data_ptr() for t in grads],
+                             torch.zeros(S, dtype=torch.int16, device=dev), torch.zeros(S, device=dev),
+                             torch.zeros(S, device=dev), n2, mpo.AdamParams(lr=1e-3, step=1), torch.bfloat16)
+os.environ.pop("MPO_P2P_KERNEL")
+model3 = torch.nn.Sequential(torch.nn.Linear(32, 40), torch.nn.Linear(40, 8)).cuda().to(torch.bfloat16)
+o4 = mpo.ResidualAdamW(model3.parameters(), lr=1e-3, fmt=torch.bfloat16)
+o4.enable_graph_step()
+xg = torch.randn(4, 32, device=dev, dtype=torch.bfloat16)
+model3(xg).float().sum().backward()
+o4.prepare_step()
+o4.step()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):
+    o4.step()                                   # captured, nothing executed
+for _ in range(2):
+    o4.prepare_step()
+    g.replay()
 torch.cuda.synchronize()
 print("sanitize run ok")
