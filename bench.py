@@ -387,7 +387,7 @@ def multi_gpu_breakdown(wl, dist, steps, warmup, p2p=False):
     return out
 
 
-def _fused_in_children(wl, steps, warmup, timeout_s=900):
+def _fused_in_children(wl, steps, warmup, timeout_s=300):
     """Every rank runs `bench.py --fused-child` (same workload, a fresh process group on
     MASTER_PORT + 101) and reads its JSON line; an error or a timeout is reported, not raised."""
     import torch
