@@ -813,23 +813,27 @@ def _secondary_one(name, steps, warmup, hbm_peak, scheme="rne"):
 def torch_comparators_secondary(name, hbm_peak, steps=20, warmup=3):
     """SURVEY 8(a) "same-box comparators": the optimizer steps the paper's method replaces, on the
     same parameter set (one tensor per parameter shape), timed like the headline:
-      * amp_fp32_master: torch.optim.AdamW(fused=True) over fp32 master weights with fp32 grads,
-        then the per-iteration recast of the masters into the bf16/fp16 model copy (the AMP
-        inventory the paper compares with, P:135) -- 28 + 6 B/param;
-      * low_precision_only: torch.optim.AdamW(fused=True) directly on the 16-bit parameters with
-        16-bit grads and (torch's choice) 16-bit state: no master, lossy (the paper's "fp16" row,
-        P:135) -- 14 B/param.
-    Same hyper-parameters as the workload; grads N(0, 1e-3), weights N(0, 0.02), seeded."""
+      * amp_fp32_master: torch's fused optimizer (Adam/AdamW/SGD, fused=True) over fp32 master
+        weights with fp32 grads, then the per-iteration recast of the masters into the bf16/fp16
+        model copy (the AMP inventory the paper compares with) -- Adam 28 + 6 B/param,
+        SGD-momentum 20 + 6;
+      * low_precision_only: the same fused optimizer directly on the 16-bit parameters with 16-bit
+        grads and (torch's choice) 16-bit state: no master, lossy (the paper's "fp16" row, P:135) --
+        Adam 14, SGD-momentum 10 B/param.
+    Same hyper-parameters as the workload; weights N(0, 0.02), grads N(0, 1e-3), seeded."""
     import torch
     from synth import workloads
     wl, fmt, kind, hpkw, cfg = WORKLOADS[name]
-    assert kind == "adam"
     sizes = workloads.sizes(wl)
     P = sum(sizes)
     tdt = torch.float16 if fmt == "fp16" else torch.bfloat16
-    hp = dict(lr=hpkw["lr"], betas=(hpkw["beta1"], hpkw["beta2"]), eps=hpkw["eps"],
-              weight_decay=hpkw.get("weight_decay", 0.0))
-    opt_cls = torch.optim.AdamW if hpkw.get("adamw", False) else torch.optim.Adam
+    if kind == "adam":
+        hp = dict(lr=hpkw["lr"], betas=(hpkw["beta1"], hpkw["beta2"]), eps=hpkw["eps"],
+                  weight_decay=hpkw.get("weight_decay", 0.0))
+        opt_cls = torch.optim.AdamW if hpkw.get("adamw", False) else torch.optim.Adam
+    else:
+        hp = dict(lr=hpkw["lr"], momentum=hpkw.get("momentum", 0.0), weight_decay=hpkw.get("weight_decay", 0.0))
+        opt_cls = torch.optim.SGD
     gen = torch.Generator(device="cuda")
     gen.manual_seed(0xB0B)
     res = {"config": f"BASELINE configs[{cfg}] parameter set {wl} ({P} params, {len(sizes)} tensors), "
@@ -848,14 +852,15 @@ def torch_comparators_secondary(name, hbm_peak, steps=20, warmup=3):
                 torch._foreach_copy_(model, ps)      # the AMP recast of the masters into the model copy
         ms, _ = timed(step, steps, warmup)
         esz = ps[0].element_size()
-        st = opt.state[ps[0]]["exp_avg"].element_size()
-        b = (2 * esz + 2 * st) + (esz + 2 * st)      # read p, g, m, v; write p, m, v
+        state = [t for t in opt.state[ps[0]].values() if torch.is_tensor(t) and t.numel() == ps[0].numel()]
+        st = sum(t.element_size() for t in state)
+        b = (2 * esz + st) + (esz + st)              # read p, g, state; write p, state
         if model is not None:
             b += esz + model[0].element_size()          # recast: read master, write model copy
         out = {"params_per_s": P / (ms * 1e-3), "ms_per_step": ms, "steps": steps, "bytes_per_param": b,
                "achieved_gbs": P * b / (ms * 1e-3) / 1e9,
                "frac_of_measured_hbm": P * b / (ms * 1e-3) / 1e9 / hbm_peak,
-               "state_dtype": str(opt.state[ps[0]]["exp_avg"].dtype).replace("torch.", "")}
+               "state_dtype": str(state[0].dtype).replace("torch.", "") if state else None}
         del opt, ps, model
         torch.cuda.empty_cache()
         return out
@@ -1399,7 +1404,8 @@ def main():
             line["secondary"]["resnet50_multi_vs_per_tensor"] = per_tensor_secondary("resnet50_sgd", hbm_peak)
         except Exception as ex:
             line["secondary"]["resnet50_multi_vs_per_tensor"] = {"error": f"{type(ex).__name__}: {ex}"}
-        for cname, mpo_ms in (("gpt2_adamw", line["secondary"].get("gpt2_adamw", {}).get("ms_per_step")),
+        for cname, mpo_ms in (("resnet50_sgd", line["secondary"].get("resnet50_sgd", {}).get("ms_per_step")),
+                              ("gpt2_adamw", line["secondary"].get("gpt2_adamw", {}).get("ms_per_step")),
                               ("llama7b_adam", ms if args.workload == "llama7b_adam" else None)):
             try:
                 cmp_ = torch_comparators_secondary(cname, hbm_peak)
@@ -1407,9 +1413,9 @@ def main():
                     cmp_["mpo_step_ms"] = mpo_ms
                     cmp_["mpo_speedup_vs_amp_fp32_master"] = cmp_["amp_fp32_master"]["ms_per_step"] / mpo_ms
                     cmp_["mpo_speedup_vs_low_precision_only"] = cmp_["low_precision_only"]["ms_per_step"] / mpo_ms
-                line["secondary"][f"torch_fused_adam_{cname}"] = cmp_
+                line["secondary"][f"torch_fused_{cname}"] = cmp_
             except Exception as ex:
-                line["secondary"][f"torch_fused_adam_{cname}"] = {"error": f"{type(ex).__name__}: {ex}"}
+                line["secondary"][f"torch_fused_{cname}"] = {"error": f"{type(ex).__name__}: {ex}"}
             torch.cuda.empty_cache()
         try:
             line["secondary"]["flat1m_adam"] = flat1m_secondary(hbm_peak)
