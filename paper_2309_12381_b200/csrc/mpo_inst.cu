@@ -59,25 +59,29 @@ mpo_status FormatOps<SF>::reconstruct(const void* value, const void* resid, floa
     return check_launch("reconstruct_kernel");
 }
 
+template <class Op, class MC>
+static void launch_nvls(const MC& mc, const uint16_t* vu, void* resid, float* m, float* v, int64_t shard_base,
+                        int64_t n, const typename Op::K& k, cudaStream_t s) {
+    auto kern = nvls_step_kernel<SF, Op, MC>;
+    static const int per_sm = resident_blocks(kern);   // persistent: one wave of resident CTAs
+    const int64_t grid = grid_for((n / kUnitEl + kThreads * kUnroll - 1) / (kThreads * kUnroll), per_sm);
+    kern<<<unsigned(grid), kThreads, 0, s>>>(mc, vu, resid, m, v, shard_base, n, k);
+}
+
 template <>
 mpo_status FormatOps<SF>::nvls(int kind, void* value_mc, const void* value_uc, const void* grad_mc, void* resid,
                                float* m, float* v, int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak,
                                const Peers* emu, int world, cudaStream_t s) {
     constexpr int B = Fmt<SF>::base;
-    const int64_t grid = grid_for((n / kUnitEl + kThreads - 1) / kThreads, 8);
     auto* vu = static_cast<const uint16_t*>(value_uc);
     if (emu) {
         const NvlsEmulated<B> mc{*emu, world};
-        if (kind == MPO_ADAM)
-            nvls_step_kernel<SF, AdamOp><<<unsigned(grid), kThreads, 0, s>>>(mc, vu, resid, m, v, shard_base, n, *ak);
-        else
-            nvls_step_kernel<SF, SgdOp><<<unsigned(grid), kThreads, 0, s>>>(mc, vu, resid, m, v, shard_base, n, *sk);
+        if (kind == MPO_ADAM) launch_nvls<AdamOp>(mc, vu, resid, m, v, shard_base, n, *ak, s);
+        else launch_nvls<SgdOp>(mc, vu, resid, m, v, shard_base, n, *sk, s);
     } else {
         const NvlsMulticast<B> mc{static_cast<uint16_t*>(value_mc), static_cast<const uint16_t*>(grad_mc)};
-        if (kind == MPO_ADAM)
-            nvls_step_kernel<SF, AdamOp><<<unsigned(grid), kThreads, 0, s>>>(mc, vu, resid, m, v, shard_base, n, *ak);
-        else
-            nvls_step_kernel<SF, SgdOp><<<unsigned(grid), kThreads, 0, s>>>(mc, vu, resid, m, v, shard_base, n, *sk);
+        if (kind == MPO_ADAM) launch_nvls<AdamOp>(mc, vu, resid, m, v, shard_base, n, *ak, s);
+        else launch_nvls<SgdOp>(mc, vu, resid, m, v, shard_base, n, *sk, s);
     }
     ++g_launches;
     return check_launch("nvls_step_kernel");
