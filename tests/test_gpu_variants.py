@@ -221,3 +221,40 @@ def test_schedule_many_tensors_with_guards(mpo, orc, scheme, fmt, kind, step_ker
     assert np.array_equal(M.cpu().numpy().view(np.uint32), fm.view(np.uint32)), "m (tensor or guard) differs"
     assert np.array_equal(W.cpu().numpy().view(np.uint32), fv.view(np.uint32)), "v (tensor or guard) differs"
     assert np.array_equal(host16(G), fg), "gradients must be read-only"
+
+
+def test_forward_error_of_in_place_addition(mpo):
+    """Fig. rstoc through the GPU step (scripts/error_bench.py): K = 200 in-place
+    additions of N(0,1) tensors (the SGD step with lr = -1).  With 13 / 16 extra bits every scheme
+    (RNE, RTZ, SR) gives exactly fp32's result, element by element (those bits "maintain a
+    full fp32 accuracy"); with 8 extra bits (X8) the forward error lies between fp32's and
+    classical fp16's."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "error_bench", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts",
+                                    "error_bench.py"))
+    eb = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(eb)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7)
+    n, K = 1 << 16, 200
+    a = torch.randn(n, device="cuda", generator=gen)
+    bs = [torch.randn(n, device="cuda", generator=gen).half() for _ in range(K)]
+    ref = None
+    for s in ("rne", "rtz", "sr"):
+        got, exact = eb.accumulate(mpo, a, bs, s)
+        v, r = mpo.mpo_split(a, torch.float16, scheme=s, seed=1234, sr_stream=0)
+        acc = mpo.mpo_reconstruct(v, r, scheme=s)         # the stored start, then fp32 additions
+        keep = acc.abs() >= 2.0 ** -16                    # lossless range of the fp16 residual (R5)
+        for b in bs:
+            acc = acc + b.float()
+        assert torch.equal(got.float()[keep], acc[keep]), s
+        ref = eb._metrics(got, exact)["rel_err"] if s == "rne" else ref
+    got, exact = eb.accumulate(mpo, a, bs, "x8")
+    e8 = eb._metrics(got, exact)["rel_err"]
+    a16 = a.half()
+    acc16 = a16.clone()
+    for b in bs:
+        acc16 += b
+    e16 = eb._metrics(acc16.double(), a16.double() + sum(b.double() for b in bs))["rel_err"]
+    assert ref < e8 < e16, (ref, e8, e16)
