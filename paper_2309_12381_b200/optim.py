@@ -77,6 +77,7 @@ class _ResidualOptimizer(torch.optim.Optimizer):
 
     def __init__(self, params, defaults, fmt: Optional[torch.dtype], exact: bool, scheme: str = "rne",
                  seed: int = 0, clip_value: float = 0.0, skip_nonfinite: bool = False):
+        self._fmt = fmt
         super().__init__(params, defaults)
         self.exact = exact
         self.scheme = scheme
@@ -103,6 +104,29 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             for p in group["params"]:
                 self._init_param(p, fmt, idx)
                 idx += 1
+
+    def add_param_group(self, param_group):
+        """torch.optim semantics: a new group joins the optimizer (its fp32 parameters are split into
+        16-bit value + residual like the constructor's, their step counts start at 0).  Not while
+        the backward hooks or the graph-replayed step are installed (they hold the tables)."""
+        if not hasattr(self, "_steps"):          # called by torch's constructor
+            return super().add_param_group(param_group)
+        if self._hooks or self._native is not None or getattr(self, "_graph", None) is not None:
+            raise MpoError(1, "add_param_group: remove the backward hooks / graph step first")
+        self._resolve_skips()
+        self._pull_native_steps()
+        super().add_param_group(param_group)
+        new = self.param_groups[-1]["params"]
+        n_old = self._steps.numel()
+        steps = torch.zeros(n_old + len(new), dtype=torch.int64)
+        steps[:n_old] = self._steps
+        self._steps, self._steps_np = steps, steps.numpy()
+        for group in self.param_groups[:-1]:
+            for p in group["params"]:
+                self.state[p]["step"] = self._steps[self.state[p]["index"]]
+        for i, p in enumerate(new):
+            self._init_param(p, self._fmt, n_old + i)
+        self._tables.clear()
 
     # -- state ------------------------------------------------------------------------------
     def _init_param(self, p: torch.Tensor, fmt, idx: int):

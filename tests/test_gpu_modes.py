@@ -859,3 +859,54 @@ def test_residual_adamw_tracks_fp32_master_over_many_steps(mpo, fmt, kind):
     scale = max(float(r.detach().abs().max()) for r in ref)
     assert err_res <= 300 * 2.0 ** -23 * scale, (err_res, scale)      # <= 1 fp32 ulp of the scale per step
     assert err_low > 100 * err_res, (err_low, err_res)
+
+
+@pytest.mark.parametrize("kind", ["adam", "sgd"])
+def test_add_param_group(mpo, kind):
+    """torch.optim's add_param_group: (a) a group added before the first step gives the same
+    steps as passing both groups to the constructor; (b) added after two steps, the first group
+    continues exactly as an optimizer over it alone and the new group steps like a fresh optimizer
+    over it (its counts start at 0); refused while backward hooks are installed."""
+    torch.manual_seed(5)
+    A = [torch.randn(300, 17, device="cuda") * 0.02, torch.randn(4100, device="cuda") * 0.02]
+    B = [torch.randn(64, 65, device="cuda") * 0.02]
+    mk = (lambda groups: mpo.ResidualAdamW(groups, lr=1e-3, weight_decay=0.1, fmt=torch.bfloat16)) \
+        if kind == "adam" else (lambda groups: mpo.ResidualSGD(groups, lr=0.1, momentum=0.9, fmt=torch.bfloat16))
+    grads = [[(torch.randn(t.shape, device="cuda") * 1e-2).to(torch.bfloat16) for t in A + B] for _ in range(4)]
+
+    def run(opt, ps, steps):
+        for t in steps:
+            for p, g in zip(ps, grads[t]):
+                p.grad = g.clone()
+            opt.step()
+
+    pa = [nn.Parameter(t.clone()) for t in A + B]
+    oa = mk([{"params": pa[:2]}])
+    oa.add_param_group({"params": pa[2:], "lr": 5e-4 if kind == "adam" else 0.05})
+    pb = [nn.Parameter(t.clone()) for t in A + B]
+    ob = mk([{"params": pb[:2]}, {"params": pb[2:], "lr": 5e-4 if kind == "adam" else 0.05}])
+    run(oa, pa, range(4)); run(ob, pb, range(4))
+    for x, y in zip(pa, pb):
+        assert torch.equal(x.view(torch.int16), y.view(torch.int16))
+        assert torch.equal(oa.state[x]["resid"], ob.state[y]["resid"])
+    # (b) added after two steps
+    pc = [nn.Parameter(t.clone()) for t in A + B]
+    oc = mk([{"params": pc[:2]}])
+    run(oc, pc[:2], range(2))
+    oc.add_param_group({"params": pc[2:]})
+    run(oc, pc, range(2, 4))
+    pd = [nn.Parameter(t.clone()) for t in A]
+    od = mk([{"params": pd}])
+    run(od, pd, range(4))
+    pe = [nn.Parameter(t.clone()) for t in B]
+    oe = mk([{"params": pe}])
+    for t in range(2, 4):
+        pe[0].grad = grads[t][2].clone()
+        oe.step()
+    for x, y in zip(pc, pd + pe):
+        assert torch.equal(x.view(torch.int16), y.view(torch.int16))
+    assert [int(oc.state[p]["step"]) for p in pc] == [4, 4, 2]
+    assert set(oc.state_dict()["state"]) == {0, 1, 2}
+    oc.install_backward_hooks()
+    with pytest.raises(mpo.MpoError, match="add_param_group"):
+        oc.add_param_group({"params": [nn.Parameter(torch.zeros(8, device="cuda"))]})
