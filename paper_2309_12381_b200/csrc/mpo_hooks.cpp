@@ -232,15 +232,24 @@ class HookState : public std::enable_shared_from_this<HookState> {
                 row.hp = h;
                 rows.push_back(row);
             }
-            if (keys.size() > MPO_MAX_HP_GROUPS)
-                throw std::runtime_error("mpo hook: more than 16 distinct (group, step) pairs in one flush");
-            mpo_status st = kind_ == MPO_ADAM
-                                ? adam_fn_(mpo_dtype(kv.first.first), mpo_dtype(kv.first.second), rows.data(),
-                                           int32_t(rows.size()), ahp.data(), int32_t(ahp.size()), nullptr, s)
-                                : sgd_fn_(mpo_dtype(kv.first.first), mpo_dtype(kv.first.second), rows.data(),
-                                          int32_t(rows.size()), shp.data(), int32_t(shp.size()), nullptr, s);
-            if (st != MPO_OK) throw std::runtime_error(std::string("mpo step (batched hook flush): ") + err_fn_());
-            ++calls_;
+            // one launch per MPO_MAX_HP_GROUPS (group, step) pairs (a launch's hyper-parameter bank)
+            const int nk = int(keys.size());
+            for (int c = 0; c < nk; c += MPO_MAX_HP_GROUPS) {
+                const int ce = c + MPO_MAX_HP_GROUPS < nk ? c + MPO_MAX_HP_GROUPS : nk;
+                std::vector<mpo_tensor> sub;
+                for (const mpo_tensor& r : rows)
+                    if (r.hp >= c && r.hp < ce) {
+                        sub.push_back(r);
+                        sub.back().hp = r.hp - c;
+                    }
+                mpo_status st = kind_ == MPO_ADAM
+                                    ? adam_fn_(mpo_dtype(kv.first.first), mpo_dtype(kv.first.second), sub.data(),
+                                               int32_t(sub.size()), ahp.data() + c, int32_t(ce - c), nullptr, s)
+                                    : sgd_fn_(mpo_dtype(kv.first.first), mpo_dtype(kv.first.second), sub.data(),
+                                              int32_t(sub.size()), shp.data() + c, int32_t(ce - c), nullptr, s);
+                if (st != MPO_OK) throw std::runtime_error(std::string("mpo step (batched hook flush): ") + err_fn_());
+                ++calls_;
+            }
         }
         // the gradients are released here (stream order keeps their reuse safe)
     }

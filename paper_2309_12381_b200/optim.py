@@ -297,13 +297,23 @@ class _ResidualOptimizer(torch.optim.Optimizer):
             keys, hp_index = {}, []
             for gi, stp in zip(tab._group_of, self._steps_np[tab._idx].tolist()):
                 hp_index.append(keys.setdefault((gi, stp), len(keys)))
+            hps = [self._hp(self.param_groups[gi], stp) for (gi, stp) in keys]
             if len(keys) > MPO_MAX_HP_GROUPS:
-                raise MpoError(1, "more than 16 distinct (group, step) pairs in one step")
+                # more (group, step) pairs than one launch's hyper-parameter bank holds (e.g. layer-
+                # wise lr decay): one launch per 16 of them, over the parameters that use them
+                for c in range(0, len(keys), MPO_MAX_HP_GROUPS):
+                    sel = [i for i, h in enumerate(hp_index) if c <= h < c + MPO_MAX_HP_GROUPS]
+                    sub = self._table_for([plist[i] for i in sel])
+                    for r, i in enumerate(sel):
+                        sub.arr[r].hp = hp_index[i] - c
+                    sub._hp_index = None
+                    launches.append((sub, hps[c:c + MPO_MAX_HP_GROUPS]))
+                continue
             if hp_index != getattr(tab, "_hp_index", None):     # usually unchanged from the last step
                 for i, h in enumerate(hp_index):
                     tab.arr[i].hp = h
                 tab._hp_index = hp_index
-            launches.append((tab, [self._hp(self.param_groups[gi], stp) for (gi, stp) in keys]))
+            launches.append((tab, hps))
         need_norm = self._needs_norm()
         if need_norm and len(launches) > 1:
             # one S over every table of the step (global-norm clipping is over ALL gradients, R9;
@@ -369,6 +379,12 @@ class _ResidualOptimizer(torch.optim.Optimizer):
         by_dtype = {}
         for p in params:
             by_dtype.setdefault((p.dtype, p.grad.dtype), []).append(p)
+        if self._needs_norm() and len(by_dtype) > 1:
+            # each graphed launch runs its own norm pre-pass: one global S over tables of different
+            # gradient dtypes would need the eager step's shared pre-pass
+            raise MpoError(1, "graph step: global-norm clipping over gradients of different dtypes")
+        if len(self.param_groups) > MPO_MAX_HP_GROUPS:
+            raise MpoError(1, f"graph step: at most {MPO_MAX_HP_GROUPS} param groups (one hyper-parameter bank)")
         for key, plist in by_dtype.items():
             tab = self._table_for(plist)
             ent = self._graph.get(key)
@@ -579,13 +595,15 @@ class _ResidualOptimizer(torch.optim.Optimizer):
                 keys, hp_index = {}, []
                 for p_, s_ in zip(ps, sts):
                     hp_index.append(keys.setdefault((self._rows[p_][1], int(self._steps_np[s_["index"]])), len(keys)))
-                tab = api.TensorTable([p.data for p in ps], [s_["resid"] for s_ in sts], [g for _, g in items],
-                                      [s_.get("m") for s_ in sts], [s_.get("v") for s_ in sts], hp_index,
-                                      scheme=self.scheme, sr_streams=[s_["index"] for s_ in sts])
                 hps = [self._hp(self.param_groups[gi], stp) for (gi, stp) in keys]
-                if len(hps) > MPO_MAX_HP_GROUPS:
-                    raise MpoError(1, "more than 16 distinct (group, step) pairs in one flush")
-                self._launch(tab, hps)
+                # one launch per MPO_MAX_HP_GROUPS (group, step) pairs (a launch's hyper-parameter bank)
+                for c in range(0, len(hps), MPO_MAX_HP_GROUPS):
+                    sel = [i for i, h in enumerate(hp_index) if c <= h < c + MPO_MAX_HP_GROUPS]
+                    tab = api.TensorTable([ps[i].data for i in sel], [sts[i]["resid"] for i in sel],
+                                          [items[i][1] for i in sel], [sts[i].get("m") for i in sel],
+                                          [sts[i].get("v") for i in sel], [hp_index[i] - c for i in sel],
+                                          scheme=self.scheme, sr_streams=[sts[i]["index"] for i in sel])
+                    self._launch(tab, hps[c:c + MPO_MAX_HP_GROUPS])
         del pending              # the gradients are released (stream order keeps reuse safe)
 
     # -- loss scaling: found-inf -------------------------------------------------------------

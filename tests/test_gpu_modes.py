@@ -910,3 +910,44 @@ def test_add_param_group(mpo, kind):
     oc.install_backward_hooks()
     with pytest.raises(mpo.MpoError, match="add_param_group"):
         oc.add_param_group({"params": [nn.Parameter(torch.zeros(8, device="cuda"))]})
+
+
+@pytest.mark.parametrize("kind", ["adam", "sgd"])
+def test_more_param_groups_than_one_hp_bank(mpo, kind):
+    """Layer-wise lr decay over 20 param groups (> the 16 hyper-parameter groups one launch
+    carries): the multi-tensor step, the native and the Python hooks (small parameters batched
+    into end-of-backward flushes of 20 (group, step) pairs) all split into launches of <= 16 and
+    equal one optimizer per layer, bitwise."""
+    torch.manual_seed(11)
+    L = 20
+
+    def make():
+        torch.manual_seed(11)
+        return nn.Sequential(*[nn.Linear(16, 16) for _ in range(L)]).cuda()
+
+    def groups(m):
+        return [{"params": list(m[i].parameters()), "lr": (1e-3 if kind == "adam" else 0.1) * 0.9 ** i}
+                for i in range(L)]
+    mk = (lambda g: mpo.ResidualAdamW(g, lr=1e-3, weight_decay=0.1, fmt=torch.bfloat16)) if kind == "adam" else \
+        (lambda g: mpo.ResidualSGD(g, lr=0.1, momentum=0.9, fmt=torch.bfloat16))
+    models = [make() for _ in range(4)]
+    oa = mk(groups(models[0]))
+    ob = mk(groups(models[1])); ob.install_backward_hooks(native=True)
+    oc = mk(groups(models[2])); oc.install_backward_hooks(native=False)
+    od = [mk([g]) for g in groups(models[3])]
+    gen = torch.Generator(device="cuda").manual_seed(12)
+    for _ in range(3):
+        x = torch.randn(8, 16, device="cuda", dtype=torch.bfloat16, generator=gen)
+        for k, m in enumerate(models):
+            m(x).float().square().mean().backward()
+            if k == 0:
+                oa.step()
+            elif k == 3:
+                for o in od:
+                    o.step()
+            if k in (0, 3):
+                for p in m.parameters():
+                    p.grad = None
+    for k in (1, 2, 3):
+        for pa, pk in zip(models[0].parameters(), models[k].parameters()):
+            assert torch.equal(pa.view(torch.int16), pk.view(torch.int16)), k
