@@ -74,6 +74,11 @@ def _weak_hook(opt):
 
 class _ResidualOptimizer(torch.optim.Optimizer):
     _kind = None
+    # torch.amp.GradScaler.step() protocol: it sets `self.grad_scale` (the loss scale, a device
+    # tensor) and `self.found_inf` (device tensor, nonzero when a scaled gradient was not finite)
+    # before calling step(), which then unscales inside the fused step and skips a non-finite one
+    _step_supports_amp_scaling = True
+    _amp_inv = 1.0
 
     def __init__(self, params, defaults, fmt: Optional[torch.dtype], exact: bool, scheme: str = "rne",
                  seed: int = 0, clip_value: float = 0.0, skip_nonfinite: bool = False):
@@ -278,8 +283,26 @@ class _ResidualOptimizer(torch.optim.Optimizer):
     def step(self, closure=None):
         if closure is not None:
             raise MpoError(1, "closure optimizers are not supported (the step is fused, P:194)")
+        found_inf = self.__dict__.get("found_inf")
+        if found_inf is not None:            # called by torch.amp.GradScaler.step()
+            if self._hooks or self._native is not None or getattr(self, "_graph", None) is not None:
+                raise MpoError(1, "GradScaler: the backward hooks / graph step update inside backward / the "
+                                  "graph; use grad_scale= and skip_nonfinite= instead (P:193)")
+            # the scaler's own inf check has run (it reads every gradient); one host read of the
+            # flag and the scale, like torch's non-fused optimizer path
+            if float(found_inf) != 0.0:
+                return None                  # skipped: no update, no step count (R16)
+            scale = self.__dict__.get("grad_scale")
+            self._amp_inv = 1.0 / float(scale) if scale is not None else 1.0
+            try:
+                return self._step_eager()
+            finally:
+                self._amp_inv = 1.0
         if getattr(self, "_graph", None) is not None:
             return self._graph_step()        # prepare_step() did the host side
+        return self._step_eager()
+
+    def _step_eager(self):
         self._resolve_skips()
         params = [p for g in self.param_groups for p in g["params"] if p.grad is not None]
         if not params:
@@ -658,7 +681,7 @@ class ResidualSGD(_ResidualOptimizer):
 
     def _hp(self, g, step):
         return api.SgdParams(lr=g["lr"], momentum=g["momentum"], dampening=g["dampening"],
-                             weight_decay=g["weight_decay"], grad_scale=g["grad_scale"], nesterov=g["nesterov"],
+                             weight_decay=g["weight_decay"], grad_scale=g["grad_scale"] * self._amp_inv, nesterov=g["nesterov"],
                              first_step=(step == 1), seed=api.step_seed(self.seed, step),
                              clip_value=self.clip_value, skip_nonfinite=self.skip_nonfinite)
 
@@ -693,7 +716,7 @@ class ResidualAdamW(_ResidualOptimizer):
     def _hp(self, g, step):
         b1, b2 = g["betas"]
         return api.AdamParams(lr=g["lr"], beta1=b1, beta2=b2, eps=g["eps"], weight_decay=g["weight_decay"],
-                              grad_scale=g["grad_scale"], max_grad_norm=self.max_grad_norm, adamw=g["adamw"],
+                              grad_scale=g["grad_scale"] * self._amp_inv, max_grad_norm=self.max_grad_norm, adamw=g["adamw"],
                               step=step, seed=api.step_seed(self.seed, step), clip_value=self.clip_value,
                               skip_nonfinite=self.skip_nonfinite)
 

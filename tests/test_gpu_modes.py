@@ -951,3 +951,50 @@ def test_more_param_groups_than_one_hp_bank(mpo, kind):
     for k in (1, 2, 3):
         for pa, pk in zip(models[0].parameters(), models[k].parameters()):
             assert torch.equal(pa.view(torch.int16), pk.view(torch.int16)), k
+
+
+@pytest.mark.parametrize("kind", ["adam", "sgd"])
+def test_torch_grad_scaler_protocol(mpo, kind):
+    """torch.amp.GradScaler drives the residual optimizers through its fused-optimizer protocol
+    (`_step_supports_amp_scaling`: it sets optimizer.grad_scale / found_inf before step()): the
+    unscale happens inside the step (grad_scale = 1/scale) and equals an optimizer stepped on the
+    same scaled gradients with that grad_scale, bitwise; a step with a non-finite scaled gradient
+    is skipped (no update, no step count) and the scaler backs off; hook mode refuses it."""
+    torch.manual_seed(21)
+    a, b = TinyLM().cuda().half(), TinyLM().cuda().half()
+    b.load_state_dict(a.state_dict())
+    mk = (lambda m: mpo.ResidualAdamW(m.parameters(), lr=1e-3, weight_decay=0.1, fmt=torch.float16)) \
+        if kind == "adam" else (lambda m: mpo.ResidualSGD(m.parameters(), lr=0.1, momentum=0.9, fmt=torch.float16))
+    oa, ob = mk(a), mk(b)
+    scaler = torch.amp.GradScaler("cuda", init_scale=2.0 ** 10, growth_interval=1)
+    gen = torch.Generator(device="cuda").manual_seed(22)
+    for it in range(4):
+        idx = torch.randint(0, 257, (4, 33), device="cuda", generator=gen)
+        scale = float(scaler.get_scale())
+        scaler.scale(_loss(a, idx)).backward()
+        (_loss(b, idx) * torch.full((), scale, device="cuda")).backward()
+        if it == 3:                                   # a non-finite scaled gradient
+            next(a.parameters()).grad.view(-1)[0] = float("inf")
+            before = [p.detach().clone() for p in a.parameters()]
+        scaler.step(oa)
+        scaler.update()
+        if it < 3:
+            for g in ob.param_groups:
+                g["grad_scale"] = 1.0 / scale
+            ob.step()
+            for pa, pb in zip(a.parameters(), b.parameters()):
+                assert torch.equal(pa.view(torch.int16), pb.view(torch.int16)), it
+        else:
+            assert all(torch.equal(x, p) for x, p in zip(before, a.parameters()))
+            assert all(int(oa.state[p]["step"]) == 3 for p in a.parameters())
+            assert float(scaler.get_scale()) == scale / 2
+        for m in (a, b):
+            for p in m.parameters():
+                p.grad = None
+    assert "found_inf" not in oa.__dict__ and oa._amp_inv == 1.0   # (found_inf() is also a method)
+    oh = mk(b)
+    oh.install_backward_hooks()
+    scaler2 = torch.amp.GradScaler("cuda")
+    scaler2.scale(_loss(b, idx)).backward()
+    with pytest.raises(mpo.MpoError, match="GradScaler"):
+        scaler2.step(oh)
