@@ -137,6 +137,10 @@ class _ResidualOptimizer(torch.optim.Optimizer):
     def _init_param(self, p: torch.Tensor, fmt, idx: int):
         if not p.is_cuda:
             raise MpoError(1, "parameters must live on a CUDA device (no CPU path)")
+        dev = self.param_groups[0]["params"][0].device
+        if p.device != dev:
+            # one launch covers a whole table on one device's stream: one optimizer per device
+            raise MpoError(1, f"parameters on {p.device} and {dev}: use one optimizer per device")
         st = self.state[p]
         st["index"] = idx            # also the stochastic-rounding stream of this parameter
         if p.dtype == torch.float32:
