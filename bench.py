@@ -1368,7 +1368,7 @@ def main():
     # also holds the NCCL collectives, so the kernel's own time comes from the update-only
     # measurement of multi_gpu_breakdown below.
     achieved = alg_bytes / (per_launch * 1e-3) / 1e9
-    traffic = ncu_traffic(args.workload)
+    traffic = ncu_traffic(args.workload) if world == 1 else None   # the committed capture is of the N=1 launch
     box_copy = None
     try:
         if world == 1 and torch.cuda.mem_get_info()[0] > 5 * (1 << 30):   # two 2 GiB buffers
