@@ -556,7 +556,8 @@ def test_llama7b_full_size_sampled(mpo, orc):
         from paper_2309_12381_b200._lib import MPO_ADAM
         import torch.distributed as tdist
         from paper_2309_12381_b200.sharded import nccl_comm_ptr
-        if not tdist.is_initialized():
+        own_group = not tdist.is_initialized()
+        if own_group:
             import socket
             sk = socket.socket(); sk.bind(("127.0.0.1", 0))
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1"); os.environ["MASTER_PORT"] = str(sk.getsockname()[1]); sk.close()
@@ -567,6 +568,8 @@ def test_llama7b_full_size_sampled(mpo, orc):
         mpo.mpo_sharded_step(MPO_ADAM, nccl_comm_ptr(), 0, 1, wl.value, wl.grad, wl.resid, wl.m, wl.v, hp, exact=True)
         torch.cuda.synchronize()
         check(pre, hp, "sharded world 1, step 3")
+        if own_group:
+            tdist.destroy_process_group()
     finally:
         del wl
         torch.cuda.empty_cache()
