@@ -659,7 +659,7 @@ __device__ __forceinline__ void store_unit(const KT& T, int64_t e, const uint4& 
 // ---- variant A ("lsu"): every thread loads its own units with 128-bit LDG, computes, stores.  The
 // default for small launches (<= kLsuMaxTiles tiles: hook mode's per-parameter steps, config C1),
 // where a grid of several CTAs per SM with every load in flight at once beats the pipeline's fill.
-template <int MAXT, int SF, int G, class Op, bool CLIP>
+template <int MAXT, int SF, int G, class Op, bool CLIP, bool DHP>
 __global__ void __launch_bounds__(kThreads) step_kernel(const __grid_constant__ Table<MAXT> tab,
                                                         const __grid_constant__ HP<typename Op::K> hp,
                                                         const HP<typename Op::K>* __restrict__ dhp,
@@ -673,7 +673,12 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const __grid_constant__ 
     for (int tile = blockIdx.x; tile < tab.ntiles; tile += gridDim.x) {
         while (cur + 1 < tab.nt && tile >= tab.t[cur + 1].tile0) ++cur;
         const KT& T = tab.t[cur];
-        const K c = dhp ? dhp->g[hp_of(T)] : hp.g[hp_of(T)];   // dhp: a graph-replayed step (mpo_step_graphed)
+        // DHP: a graph-replayed step (mpo_step_graphed) reads its hyper-parameters from the device
+        // block; its own instantiation, because a runtime select between the two banks kept both
+        // structs in registers (122 -> 156 registers: one CTA per SM instead of two)
+        K c;
+        if constexpr (DHP) c = dhp->g[hp_of(T)];
+        else c = hp.g[hp_of(T)];
         const bool need_m = Op::reads_m(c);
         const bool has_m = Op::writes_m(c);
         const int64_t base = int64_t(tile - T.tile0) * kTileEl;
@@ -1630,11 +1635,16 @@ mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typen
     if (tiles > INT32_MAX) return fail(MPO_EINVAL, "table slice too large");
     const int choice = step_kernel_choice();
     if (choice == 1 || (choice < 0 && tiles <= kLsuMaxTiles)) {
-        auto kern = step_kernel<MAXT, SF, G, Op, CLIP>;
-        static int per_sm = resident_blocks(kern);
-        const int64_t grid = grid_for(tiles, per_sm);
-        kern<<<unsigned(grid), kThreads, 0, s>>>(tab, hp, static_cast<const HP<typename Op::K>*>(g_dev_hp), sumsq,
-                                                 max_norm, skip);
+        const auto* dhp = static_cast<const HP<typename Op::K>*>(g_dev_hp);
+        if (dhp) {
+            auto kern = step_kernel<MAXT, SF, G, Op, CLIP, true>;
+            static int per_sm = resident_blocks(kern);
+            kern<<<unsigned(grid_for(tiles, per_sm)), kThreads, 0, s>>>(tab, hp, dhp, sumsq, max_norm, skip);
+        } else {
+            auto kern = step_kernel<MAXT, SF, G, Op, CLIP, false>;
+            static int per_sm = resident_blocks(kern);
+            kern<<<unsigned(grid_for(tiles, per_sm)), kThreads, 0, s>>>(tab, hp, nullptr, sumsq, max_norm, skip);
+        }
         ++g_launches;
         return check_launch("step_kernel");
     }
