@@ -855,7 +855,7 @@ __host__ __device__ constexpr int stage_bytes() {
 }
 
 
-template <int MAXT, int SF, int G, class Op, bool CLIP>
+template <int MAXT, int SF, int G, class Op, bool CLIP, bool DHP>
 __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(const __grid_constant__ Table<MAXT> tab,
                                                                   const __grid_constant__ HP<typename Op::K> hp,
                                                                   const HP<typename Op::K>* __restrict__ dhp,
@@ -903,7 +903,9 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
             auto issue = [&](int cur, int64_t base, int64_t nvalid) {
                 mbar_wait(&empty[s], ph ^ 1u);
                 const KT& T = tab.t[cur];
-                const K c = dhp ? dhp->g[hp_of(T)] : hp.g[hp_of(T)];
+                                K c;   // DHP: graph-replayed step (device block); see step_kernel
+                if constexpr (DHP) c = dhp->g[hp_of(T)];
+                else c = hp.g[hp_of(T)];
                 const uint32_t nvec = uint32_t(nvalid) & ~(kGran - 1u);
                 const bool need_m = Op::reads_m(c);
                 uint32_t bytes = nvec * (2u + RB + GB);
@@ -976,7 +978,9 @@ __global__ void __launch_bounds__(kTmaThreads, MPO_CTAS_PER_SM) step_tma_kernel(
         const StageDesc d = desc[s];
         if (d.cur < 0) break;
         const KT& T = tab.t[d.cur];
-        const K c = dhp ? dhp->g[hp_of(T)] : hp.g[hp_of(T)];
+                        K c;   // DHP: graph-replayed step (device block); see step_kernel
+                if constexpr (DHP) c = dhp->g[hp_of(T)];
+                else c = hp.g[hp_of(T)];
         const int64_t base = d.base, nvalid = d.nvalid;
         const int64_t nvec = nvalid & ~int64_t(kGran - 1u);
         const bool full_unit = el + kUnitEl <= nvec;
@@ -1626,39 +1630,65 @@ __global__ void __launch_bounds__(kP2PThreads, 2) p2p_tma_kernel(const __grid_co
 // ------------------------------------------------------------------------------------------
 constexpr int kSmemBudget = (MPO_CTAS_PER_SM == 1 ? 227 * 1024 : (228 * 1024) / MPO_CTAS_PER_SM - 1024);
 
+// once per kernel (a static per distinct kernel, whatever its function-pointer type)
+template <auto KERN>
+int resident_per_sm() {
+    static const int v = resident_blocks(KERN);
+    return v;
+}
+template <auto KERN, int SMEM>
+cudaError_t dyn_smem_attr() {
+    static const cudaError_t a = cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    return a;
+}
+
 template <int MAXT, int SF, int G, class Op, bool CLIP>
 mpo_status launch_step_slice(const mpo_tensor* t, int lo, int hi, const HP<typename Op::K>& hp, bool one_hp,
                              const double* sumsq, double max_norm, int skip, cudaStream_t s) {
+    const auto* dhp = static_cast<const HP<typename Op::K>*>(g_dev_hp);
+    // A graph-replayed step (mpo_step_graphed) reads its hyper-parameters from the device block:
+    // kernels of their own (DHP = true; a runtime select of the two banks held both in registers),
+    // instantiated for the largest table only to bound the build
+    if constexpr (MAXT != kBigT) {
+        if (dhp) return launch_step_slice<kBigT, SF, G, Op, CLIP>(t, lo, hi, hp, one_hp, sumsq, max_norm, skip, s);
+    }
     Table<MAXT> tab;
     const int64_t tiles = fill_table(tab, t, lo, hi, one_hp);
     if (tiles == 0) return MPO_OK;
     if (tiles > INT32_MAX) return fail(MPO_EINVAL, "table slice too large");
     const int choice = step_kernel_choice();
     if (choice == 1 || (choice < 0 && tiles <= kLsuMaxTiles)) {
-        const auto* dhp = static_cast<const HP<typename Op::K>*>(g_dev_hp);
-        if (dhp) {
-            auto kern = step_kernel<MAXT, SF, G, Op, CLIP, true>;
-            static int per_sm = resident_blocks(kern);
-            kern<<<unsigned(grid_for(tiles, per_sm)), kThreads, 0, s>>>(tab, hp, dhp, sumsq, max_norm, skip);
+        constexpr auto k0 = step_kernel<MAXT, SF, G, Op, CLIP, false>;
+        if constexpr (MAXT == kBigT) {
+            constexpr auto k1 = step_kernel<MAXT, SF, G, Op, CLIP, true>;
+            if (dhp) k1<<<unsigned(grid_for(tiles, resident_per_sm<k1>())), kThreads, 0, s>>>(tab, hp, dhp, sumsq, max_norm, skip);
+            else k0<<<unsigned(grid_for(tiles, resident_per_sm<k0>())), kThreads, 0, s>>>(tab, hp, nullptr, sumsq, max_norm, skip);
         } else {
-            auto kern = step_kernel<MAXT, SF, G, Op, CLIP, false>;
-            static int per_sm = resident_blocks(kern);
-            kern<<<unsigned(grid_for(tiles, per_sm)), kThreads, 0, s>>>(tab, hp, nullptr, sumsq, max_norm, skip);
+            k0<<<unsigned(grid_for(tiles, resident_per_sm<k0>())), kThreads, 0, s>>>(tab, hp, nullptr, sumsq, max_norm, skip);
         }
         ++g_launches;
         return check_launch("step_kernel");
     }
     const int64_t grid = grid_for(tiles, MPO_CTAS_PER_SM);
-    auto kern = step_tma_kernel<MAXT, SF, G, Op, CLIP>;
     constexpr int SB = stage_bytes<Fmt<SF>::rbytes, G, Op::kHasV>();
     constexpr int kFree = kSmemBudget - kBarBytes - kDescBytes;
     constexpr int stages = kFree / SB < kMaxStages ? kFree / SB : kMaxStages;
     static_assert(stages >= 2, "need at least two pipeline stages");
     constexpr int smem = kBarBytes + kDescBytes + stages * SB;
-    static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t attr;
+    constexpr auto k0 = step_tma_kernel<MAXT, SF, G, Op, CLIP, false>;
+    if constexpr (MAXT == kBigT) {
+        constexpr auto k1 = step_tma_kernel<MAXT, SF, G, Op, CLIP, true>;
+        if (dhp) {
+            if ((attr = dyn_smem_attr<k1, smem>()) == cudaSuccess)
+                k1<<<unsigned(grid), kTmaThreads, smem, s>>>(tab, hp, dhp, sumsq, max_norm, stages, skip);
+        } else if ((attr = dyn_smem_attr<k0, smem>()) == cudaSuccess) {
+            k0<<<unsigned(grid), kTmaThreads, smem, s>>>(tab, hp, nullptr, sumsq, max_norm, stages, skip);
+        }
+    } else if ((attr = dyn_smem_attr<k0, smem>()) == cudaSuccess) {
+        k0<<<unsigned(grid), kTmaThreads, smem, s>>>(tab, hp, nullptr, sumsq, max_norm, stages, skip);
+    }
     if (attr != cudaSuccess) return fail(MPO_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr));
-    kern<<<unsigned(grid), kTmaThreads, smem, s>>>(tab, hp, static_cast<const HP<typename Op::K>*>(g_dev_hp), sumsq,
-                                                   max_norm, stages, skip);
     ++g_launches;
     return check_launch("step_tma_kernel");
 }
