@@ -230,3 +230,41 @@ def test_graphed_step_validation(libs):
     rc, msg = _status(L, L.mpo_step_graphed(_lib.MPO_ADAM, _lib.MPO_BF16, _lib.MPO_BF16, tab, 1, C.byref(hp), 1, buf,
                                             4100, None, None, None))
     assert rc == _lib.MPO_EALIGN
+
+
+def _res_usage(path):
+    import re
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([exe, "-res-usage", path], capture_output=True, text=True).stdout
+    res = {}
+    name = None
+    for line in out.splitlines():
+        m = re.search(r"Function (\S+):", line)
+        if m:
+            name = m.group(1)
+            continue
+        if name and "REG:" in line:
+            res[name] = {k: int(v) for k, v in re.findall(r"(REG|STACK|LOCAL|SHARED):(\d+)", line)}
+            name = None
+    return res
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_kernel_resources(exact):
+    """Build-artifact guard (cuobjdump, no GPU): no kernel spills to local memory, and the
+    per-thread-load step kernel keeps two CTAs of 256 threads per SM (<= 128 registers) in all
+    but a handful of instantiations -- a runtime select of two hyper-parameter banks once pushed
+    60 of them to 160 registers."""
+    from paper_2309_12381_b200 import _build
+    path = _build.lib_path(exact)
+    if not os.path.exists(path):
+        pytest.skip("library not built")
+    res = _res_usage(path)
+    assert len(res) > 300, len(res)
+    assert not [k for k, v in res.items() if v.get("LOCAL", 0) > 0]
+    lsu = {k: v for k, v in res.items() if k.startswith("_ZN3mpo11step_kernel")}
+    assert len(lsu) >= 144
+    high = [k for k, v in lsu.items() if v["REG"] > 128]
+    assert len(high) <= 8, (len(high), high[:4])
