@@ -249,8 +249,8 @@ def bytes_per_param(scheme: str, optim: str) -> int:
 
 
 # ---- paper variants of the storage scheme (oracle.c "Paper variants") ----
-SCHEME = {"rne": 0, "rtz": 1, "sr": 2, "x8": 3}
-RESID_DTYPE = {"rne": np.int16, "rtz": np.uint16, "sr": np.int16, "x8": np.int8}
+SCHEME = {"rne": 0, "rtz": 1, "sr": 2, "x8": 3, "x8z": 4}
+RESID_DTYPE = {"rne": np.int16, "rtz": np.uint16, "sr": np.int16, "x8": np.int8, "x8z": np.uint8}
 
 
 def rtz16(fmt: str, u: int) -> int:

@@ -376,11 +376,15 @@ void or_adam_step_master(int gfmt, float* w, const void* grad, float* m, float* 
 /*             as in the paper's "fp16 + 13 stochastic" run -- 13 + 1 bits fit 16   */
 /*   OR_S_X8   RNE value + only 8 extra bits (int8): "We also explore the performance  */
 /*             when keeping only part of those bits"; "fp16 + 8"; reading R14         */
+/*   OR_S_X8Z  the paper's own fp16+8 / bf16+8: round-to-zero value + the NEXT 8 bits of the  */
+/*             fp32 significand, truncated (uint8) -- P:84 "saving only the first part of   */
+/*             the 32bit significand is equivalent to applying a round-to-zero"; R20        */
 /* ------------------------------------------------------------------------------------- */
 #define OR_S_RNE 0
 #define OR_S_RTZ 1
 #define OR_S_SR 2
 #define OR_S_X8 3
+#define OR_S_X8Z 4
 
 /* IEEE round-toward-zero of a binary32 pattern to fp16 / bf16 by integer truncation of the
  * dropped significand bits (no rounding increment).  Finite values never overflow to Inf: they
@@ -444,7 +448,7 @@ static void split_s(int scheme, int fmt, uint32_t u, uint32_t rnd, uint16_t* h_o
     uint32_t wu;
     int64_t d;
     if ((u & 0x7FFFFFFFu) > 0x7F800000u) { *h_out = 0x7FFF; *r_out = 0; return; }   /* R4 */
-    if (scheme == OR_S_RTZ) h = or_rtz16(fmt, u);
+    if (scheme == OR_S_RTZ || scheme == OR_S_X8Z) h = or_rtz16(fmt, u);
     else if (scheme == OR_S_SR) h = or_sr16(u, rnd);
     else h = or_rne16(fmt, u);
     wu = or_widen16(fmt, h);
@@ -453,6 +457,9 @@ static void split_s(int scheme, int fmt, uint32_t u, uint32_t rnd, uint16_t* h_o
     d = (int64_t)u - (int64_t)wu;          /* same sign: none of the roundings changes it */
     if (scheme == OR_S_RTZ) {              /* |x| >= |t|: d >= 0 */
         *r_out = (int32_t)(d > 65535 ? 65535 : d);
+    } else if (scheme == OR_S_X8Z) {       /* |x| >= |t|: the next 8 bits, truncated (R20) */
+        int64_t q = d >> (fmt == OR_BF16 ? 8 : 5);
+        *r_out = (int32_t)(q > 255 ? 255 : q);
     } else if (scheme == OR_S_X8) {        /* keep the top 8 of the extra bits, nearest (R14) */
         int sh = fmt == OR_BF16 ? 8 : 5;
         int64_t q = floordiv_pow2(d + ((int64_t)1 << (sh - 1)), sh);
@@ -467,19 +474,21 @@ static uint32_t reconstruct_s(int scheme, int fmt, uint16_t h, int32_t r) {
     int64_t add;
     if ((wu & 0x7FFFFFFFu) > 0x7F800000u) return 0x7FFFFFFFu;
     if ((wu & 0x7FFFFFFFu) == 0x7F800000u) return wu;
-    if (scheme == OR_S_X8) add = (int64_t)r * (fmt == OR_BF16 ? 256 : 32);
+    if (scheme == OR_S_X8 || scheme == OR_S_X8Z) add = (int64_t)r * (fmt == OR_BF16 ? 256 : 32);
     else add = r;
     return (uint32_t)((int64_t)wu + add);
 }
 
 static int32_t load_resid(int scheme, const void* resid, int64_t i) {
     if (scheme == OR_S_X8) return ((const int8_t*)resid)[i];
+    if (scheme == OR_S_X8Z) return ((const uint8_t*)resid)[i];
     if (scheme == OR_S_RTZ) return ((const uint16_t*)resid)[i];
     return ((const int16_t*)resid)[i];
 }
 
 static void store_resid(int scheme, void* resid, int64_t i, int32_t r) {
     if (scheme == OR_S_X8) ((int8_t*)resid)[i] = (int8_t)r;
+    else if (scheme == OR_S_X8Z) ((uint8_t*)resid)[i] = (uint8_t)r;
     else if (scheme == OR_S_RTZ) ((uint16_t*)resid)[i] = (uint16_t)r;
     else ((int16_t*)resid)[i] = (int16_t)r;
 }

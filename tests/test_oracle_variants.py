@@ -11,6 +11,10 @@
   uniform.
 * X8 ("keeping only part of those bits", P:134 fp16+8): the value is the RNE value, the
   reconstruction error is at most half the kept quantum except at saturation.
+* X8Z, the paper's own fp16+8 / bf16+8 ("saving only the first part of the 32bit
+  significand"): RTZ value + the next 8 significand bits truncated, i.e. split +
+  reconstruct = the binary32 pattern with its low 5 (fp16) / 8 (bf16) bits cleared, on every
+  pattern of a stratified sample of all exponents (each 16-bit high half x 64 low halves).
 * Trajectories: bf16 RTZ Adam is BIT-IDENTICAL to the fp32-master trajectory on every element
   (lossless storage, an independent numpy/oracle master loop); fp16 SR equals it on every element
   that never went below 2^-15; X8 stays within its per-step bound.
@@ -237,3 +241,62 @@ def test_x8_adam_drift_bounded(orc):
     assert (np.abs(got - wm) <= (T + 1) * 16 * ulp)[normal].all()
     assert (np.abs(got - wm) <= (T + 1) * 2.0 ** -24)[~normal].all()
     assert np.array_equal(m, m0) and np.array_equal(v, v0)   # the state never sees the storage error
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "fp16"])
+def test_x8z_is_significand_truncation(orc, fmt):
+    """keeping only the first part of the fp32 significand is round-to-zero; with 8 extra bits
+    ("fp16+8") split + reconstruct clears the low 8 (bf16) / 5 (fp16: 13 - 8) bits of the
+    binary32 pattern -- where the kept field can hold the remainder (bf16: every finite value;
+    fp16: the normal range [2^-14, 65504]) -- the value is the RTZ value, the code is the next 8
+    bits, and NaN / Inf store no extra bits."""
+    hi = np.arange(1 << 16, dtype=np.uint32) << 16
+    lo = synth.rng(21, 1).integers(0, 1 << 16, size=(1 << 16, 64), dtype=np.uint32)
+    u = (hi[:, None] | lo).reshape(-1)
+    x = u.view(np.float32)
+    h, r = orc.split_s("x8z", fmt, x)
+    assert r.dtype == np.uint8
+    ht = np.array([orc.rtz16(fmt, int(v)) for v in u[::997]], np.uint16)
+    assert np.array_equal(h[::997], ht)                                # the value is RTZ (pinned above)
+    rec = orc.reconstruct_s("x8z", fmt, h, r).view(np.uint32)
+    sh = 8 if fmt == "bf16" else 5
+    a = u & 0x7FFFFFFF
+    fin = a < 0x7F800000
+    if fmt == "bf16":
+        ok = fin & (np.abs(x) <= np.float32(3.3895314e38))             # RTZ saturates above bf16 max
+    else:
+        ok = fin & (a >= 0x38800000) & (np.abs(x) < 65520)             # fp16 normal range
+    assert np.array_equal(rec[ok], u[ok] & ~np.uint32((1 << sh) - 1))
+    # everywhere (saturated codes included) the stored weight is a truncation: never larger in
+    # magnitude, never of the other sign
+    assert (_mag(rec[fin]) <= _mag(u[fin])).all()
+    assert ((rec[fin] ^ u[fin]) & 0x80000000 == 0)[_mag(rec[fin]) != 0].all()
+    nan = a > 0x7F800000
+    assert (h[nan] == 0x7FFF).all() and not r[nan].any()
+    inf = a == 0x7F800000
+    assert not r[inf].any() and np.isinf(orc.reconstruct_s("x8z", fmt, h[inf], r[inf])).all()
+
+
+def test_x8z_adam_error_is_truncation(orc):
+    """fp16+8 (truncated) Adam: every split rounds the weight toward zero by less than one kept
+    quantum (2^5 binary32 ulps), so after T steps the weight lies within (T + 1) quanta of the
+    fp32 master and the state (m, v) never sees the storage error."""
+    n = 1 << 14
+    fmt = "fp16"
+    w = synth.weights(n, 0.02, 5)
+    hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, adamw=False)
+    T = 20
+    grads = [orc.widen(fmt, synth.grads(n, 1e-3, fmt, 5, t)) for t in range(1, T + 1)]
+    wm = w.copy(); m0 = np.zeros(n, np.float32); v0 = np.zeros(n, np.float32)
+    wmax, wmin = np.abs(wm).copy(), np.abs(wm).copy()
+    h, r = orc.split_s("x8z", fmt, w)
+    m = np.zeros(n, np.float32); v = np.zeros(n, np.float32)
+    for t, g in enumerate(grads, start=1):
+        orc.adam_step_master("fp32", wm, g, m0, v0, step=t, **hp)
+        wmax, wmin = np.maximum(wmax, np.abs(wm)), np.minimum(wmin, np.abs(wm))
+        orc.adam_step_s("x8z", fmt, "fp32", h, r, g, m, v, step=t, **hp)
+    got = orc.reconstruct_s("x8z", fmt, h, r).astype(np.float64)
+    ulp = np.spacing(np.maximum(wmax, 2.0 ** -14).astype(np.float32)).astype(np.float64)
+    normal = wmin >= 2.0 ** -14
+    assert (np.abs(got - wm) <= (T + 1) * 32 * ulp)[normal].all()
+    assert np.array_equal(m, m0) and np.array_equal(v, v0)
