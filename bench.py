@@ -246,7 +246,7 @@ class Workload:
     @property
     def bytes_per_param(self):
         b = BYTES_PER_PARAM["adam_clip" if self.clip else self.kind]
-        return b - 2 if self.scheme == "x8" else b      # int8 residual: 1 B read + 1 B written
+        return b - 2 if self.scheme in ("x8", "x8z") else b      # 8-bit residual: 1 B read + 1 B written
 
     def hp(self):
         mpo = self.mpo
@@ -1458,7 +1458,7 @@ def main():
             line["secondary"]["split_reconstruct"] = split_reconstruct_secondary(hbm_peak)
         except Exception as ex:
             line["secondary"]["split_reconstruct"] = {"error": f"{type(ex).__name__}: {ex}"}
-        for sch in ("rtz", "sr", "x8"):    # paper variants of the storage scheme, GPT-2 AdamW set
+        for sch in ("rtz", "sr", "x8", "x8z"):    # paper variants of the storage scheme, GPT-2 AdamW set
             name = "gpt2_adamw"
             fmt_ok = sch != "sr" or WORKLOADS[name][1] == "fp16"
             key = f"{name}_{sch}" + ("" if fmt_ok else "_fp16")

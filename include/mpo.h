@@ -78,17 +78,20 @@ typedef enum {
  *                            upper 32 bits for even, lower for odd elements (R14)
  *   MPO_FP16_X8, _BF16_X8    RNE value + 8 extra bits: int8 residual ("keeping only part of
  *                            those bits"; P:134 fp16+8), reading R14
+ *   MPO_FP16_X8Z, _BF16_X8Z  the paper's own fp16+8 / bf16+8: round-to-zero value + the next 8
+ *                            significand bits, truncated: uint8 residual, R20
  * Gradients: MPO_FP16, MPO_BF16 or MPO_FP32 (variant formats: their base dtype or MPO_FP32). */
 typedef enum {
     MPO_FP16 = 0, MPO_BF16 = 1, MPO_FP32 = 2,
-    MPO_FP16_RTZ = 16, MPO_BF16_RTZ = 17, MPO_FP16_SR = 32, MPO_FP16_X8 = 48, MPO_BF16_X8 = 49
+    MPO_FP16_RTZ = 16, MPO_BF16_RTZ = 17, MPO_FP16_SR = 32, MPO_FP16_X8 = 48, MPO_BF16_X8 = 49,
+    MPO_FP16_X8Z = 64, MPO_BF16_X8Z = 65
 } mpo_dtype;
 typedef enum { MPO_SGD = 0, MPO_ADAM = 1 } mpo_optim;
 
 /* One parameter tensor of a multi-tensor table ("one only stream of values").
  *   value     : n 16-bit values (storage format vdt), updated in place
  *   resid     : n residuals, updated in place: int16 (MPO_FP16/BF16, FP16_SR), uint16 bit
- *               patterns (the RTZ formats) or int8 (the X8 formats)
+ *               patterns (the RTZ formats), int8 (the X8 formats) or uint8 (X8Z)
  *   grad      : n gradients (dtype gdt: FP16, BF16 or FP32), read-only
  *   m         : n fp32 -- SGD momentum buffer, or Adam first moment (NULL for SGD w/o momentum)
  *   v         : n fp32 -- Adam second moment (ignored by SGD)

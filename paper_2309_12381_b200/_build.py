@@ -23,7 +23,7 @@ INCLUDE = os.path.join(ROOT, "include")
 # translation units: the ABI layer, and the step kernels once per storage format (mpo_dtype code)
 ABI_TU = os.path.join(CSRC, "mpo.cu")
 INST_TU = os.path.join(CSRC, "mpo_inst.cu")
-FORMATS = (0, 1, 16, 17, 32, 48, 49)
+FORMATS = (0, 1, 16, 17, 32, 48, 49, 64, 65)
 SOURCES = [ABI_TU, INST_TU]
 DEPS = SOURCES + [os.path.join(CSRC, "mpo_device.cuh"), os.path.join(CSRC, "mpo_kernels.cuh"),
                   os.path.join(INCLUDE, "mpo.h"), __file__]

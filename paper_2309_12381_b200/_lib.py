@@ -17,7 +17,7 @@ STATUS_NAMES = {0: "MPO_OK", 1: "MPO_EINVAL", 2: "MPO_EALIGN", 3: "MPO_EDTYPE", 
 # dtype / optimizer enums (mpo_dtype, mpo_optim)
 MPO_FP16, MPO_BF16, MPO_FP32 = 0, 1, 2
 # storage schemes of the residual: code = base | scheme << 4 (include/mpo.h mpo_dtype)
-SCHEMES = {"rne": 0, "rtz": 1, "sr": 2, "x8": 3}
+SCHEMES = {"rne": 0, "rtz": 1, "sr": 2, "x8": 3, "x8z": 4}
 MPO_SGD, MPO_ADAM = 0, 1
 MPO_MAX_HP_GROUPS = 16
 

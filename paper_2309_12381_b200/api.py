@@ -29,7 +29,8 @@ def dtype_code(dt: torch.dtype) -> int:
 def format_code(value_dtype: torch.dtype, scheme: str = "rne") -> int:
     """Storage format code (include/mpo.h mpo_dtype) of a 16-bit value dtype under a scheme:
     'rne' (default), 'rtz' (round-to-zero + uint16 extra bits), 'sr' (fp16 stochastic rounding),
-    'x8' (8 extra bits, int8 residual)."""
+    'x8' (8 extra bits, int8 residual), 'x8z' (the paper's fp16+8: round-to-zero value + the next
+    8 bits truncated, uint8 residual)."""
     if value_dtype not in _VALUE_VIEW:
         raise MpoError(_lib.MPO_EDTYPE, f"value dtype must be fp16/bf16, got {value_dtype}")
     if scheme not in _lib.SCHEMES:
@@ -40,8 +41,9 @@ def format_code(value_dtype: torch.dtype, scheme: str = "rne") -> int:
 
 
 def resid_dtype(scheme: str = "rne") -> torch.dtype:
-    """Container dtype of the residual: int16 (rne, sr; rtz holds uint16 bit patterns), int8 (x8)."""
-    return torch.int8 if scheme == "x8" else torch.int16
+    """Container dtype of the residual: int16 (rne, sr; rtz holds uint16 bit patterns), int8 (x8),
+    uint8 (x8z)."""
+    return {"x8": torch.int8, "x8z": torch.uint8}.get(scheme, torch.int16)
 
 
 def step_seed(seed: int, step: int) -> int:

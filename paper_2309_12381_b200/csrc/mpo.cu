@@ -112,10 +112,10 @@ bool finite(double x) { return std::isfinite(x); }
 // storage formats (mpo_dtype codes) and their properties
 bool is_value_format(int f) {
     return f == MPO_FP16 || f == MPO_BF16 || f == MPO_FP16_RTZ || f == MPO_BF16_RTZ || f == MPO_FP16_SR ||
-           f == MPO_FP16_X8 || f == MPO_BF16_X8;
+           f == MPO_FP16_X8 || f == MPO_BF16_X8 || f == MPO_FP16_X8Z || f == MPO_BF16_X8Z;
 }
 int base_of(int f) { return f & 15; }
-int resid_bytes(int f) { return (f >> 4) == kX8 ? 1 : 2; }
+int resid_bytes(int f) { return ((f >> 4) == kX8 || (f >> 4) == kX8Z) ? 1 : 2; }
 
 AdamK derive_adam(const mpo_adam_hp& h) {
     AdamK c;
@@ -303,7 +303,7 @@ mpo_status table_sumsq(mpo_dtype gdt, const mpo_tensor* t, int nt, const float* 
 }
 
 // ---- dispatch to the per-format translation units ----
-#define MPO_FORMATS(X) X(MPO_FP16) X(MPO_BF16) X(MPO_FP16_RTZ) X(MPO_BF16_RTZ) X(MPO_FP16_SR) X(MPO_FP16_X8) X(MPO_BF16_X8)
+#define MPO_FORMATS(X) X(MPO_FP16) X(MPO_BF16) X(MPO_FP16_RTZ) X(MPO_BF16_RTZ) X(MPO_FP16_SR) X(MPO_FP16_X8) X(MPO_BF16_X8) X(MPO_FP16_X8Z) X(MPO_BF16_X8Z)
 
 mpo_status dispatch_sgd(int vdt, int gdt, const mpo_tensor* t, int nt, const HP<SgdK>& k, bool one_hp,
                         const double* sumsq, int skip, cudaStream_t s) {

@@ -231,13 +231,24 @@ __device__ __forceinline__ void st_resid(void* base, int64_t e, const ResidUnit<
 template <int SF>
 __device__ __forceinline__ int32_t code_at(const ResidUnit<SF>& r, int k) {
     const uint32_t* w = &r.v.x;
-    if constexpr (Fmt<SF>::rbytes == 1) {
+    if constexpr (Fmt<SF>::scheme == kX8Z) {
+        return static_cast<int32_t>((w[k >> 2] >> (8 * (k & 3))) & 0xFFu);              // uint8
+    } else if constexpr (Fmt<SF>::rbytes == 1) {
         return static_cast<int32_t>(static_cast<int8_t>((w[k >> 2] >> (8 * (k & 3))) & 0xFFu));
     } else if constexpr (Fmt<SF>::scheme == kRTZ) {
         return static_cast<int32_t>((w[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);
     } else {
         return (k & 1) ? shi16(w[k >> 1]) : slo16(w[k >> 1]);
     }
+}
+
+// One stored residual code (scalar paths: tails, ragged ends).
+template <int SF>
+__device__ __forceinline__ int32_t load_code(const void* resid, int64_t i) {
+    if constexpr (Fmt<SF>::scheme == kX8Z) return static_cast<const uint8_t*>(resid)[i];
+    else if constexpr (Fmt<SF>::rbytes == 1) return static_cast<const int8_t*>(resid)[i];
+    else if constexpr (Fmt<SF>::scheme == kRTZ) return static_cast<const uint16_t*>(resid)[i];
+    else return static_cast<const int16_t*>(resid)[i];
 }
 
 template <int SF>
@@ -278,7 +289,7 @@ __device__ __forceinline__ void split8_s(const float (&w)[8], uint32_t (&hv)[4],
     uint32_t p[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        if constexpr (FM::scheme == kRTZ) p[q] = rtz2<FM::base>(w[2 * q], w[2 * q + 1]);
+        if constexpr (FM::rtz_value) p[q] = rtz2<FM::base>(w[2 * q], w[2 * q + 1]);
         else p[q] = round2<FM::base>(w[2 * q], w[2 * q + 1]);
     }
     const uint32_t special = nonfinite_pair<FM::base>(p[0]) | nonfinite_pair<FM::base>(p[1]) |
@@ -364,9 +375,7 @@ __global__ void __launch_bounds__(kThreads) reconstruct_kernel(const uint16_t* _
     }
     const int64_t t = nunits * kUnitEl + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t < n && t < nunits * kUnitEl + kUnitEl) {
-        const int32_t code = Fmt<SF>::rbytes == 1 ? int32_t(static_cast<const int8_t*>(resid)[t])
-                           : (Fmt<SF>::scheme == kRTZ ? int32_t(static_cast<const uint16_t*>(resid)[t])
-                                                      : int32_t(static_cast<const int16_t*>(resid)[t]));
+        const int32_t code = load_code<SF>(resid, t);
         w[t] = reconstruct1_s<SF>(value[t], code);
     }
 }
@@ -625,9 +634,7 @@ __device__ __noinline__ void process_tail(const KT T, int64_t lo, int64_t hi, co
         if (c.clip_on) g = clamp_grad(g, c.clipv);
         if constexpr (CLIP) g = g * coef;
         int32_t code;
-        if constexpr (FM::rbytes == 1) code = static_cast<const int8_t*>(T.resid)[i];
-        else if constexpr (FM::scheme == kRTZ) code = static_cast<const uint16_t*>(T.resid)[i];
-        else code = static_cast<const int16_t*>(T.resid)[i];
+        code = load_code<SF>(T.resid, i);
         float w = reconstruct1_s<SF>(val[i], code);
         float mi = need_m ? T.m[i] : 0.0f;
         float vi = 0.0f;
@@ -1470,9 +1477,7 @@ __device__ __noinline__ void p2p_tail(const Peers& P, int world, int rank, void*
         g = g * c.gs;
         if (c.clip_on) g = clamp_grad(g, c.clipv);
         int32_t code;
-        if constexpr (FM::rbytes == 1) code = static_cast<const int8_t*>(resid)[i];
-        else if constexpr (FM::scheme == kRTZ) code = static_cast<const uint16_t*>(resid)[i];
-        else code = static_cast<const int16_t*>(resid)[i];
+        code = load_code<SF>(resid, i);
         float w = reconstruct1_s<SF>(P.v[rank][shard_base + i], code);
         float mi = need_m ? m[i] : 0.0f;
         float vi = 0.0f;

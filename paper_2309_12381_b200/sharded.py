@@ -187,7 +187,7 @@ class ShardedResidualOptimizer:
         if vdt not in (torch.float16, torch.bfloat16):
             raise MpoError(3, "fmt must be torch.float16 or torch.bfloat16")
         self.layout = L = ShardLayout([p.numel() for p in self.params], self.world,
-                                      align=2 * ALIGN if scheme == "x8" else ALIGN)
+                                      align=2 * ALIGN if scheme in ("x8", "x8z") else ALIGN)
         lo, hi = L.shard_range(self.rank)
         # fp32 source of the flat buffer (transient), split once on the device
         src = torch.zeros(L.total, dtype=torch.float32, device=dev)

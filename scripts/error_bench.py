@@ -22,7 +22,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-SCHEMES = ("rne", "rtz", "sr", "x8")   # fp16 + 16-bit residual (RNE / RTZ / SR) and fp16 + 8 bits
+SCHEMES = ("rne", "rtz", "sr", "x8", "x8z")   # fp16 + 16-bit residual (RNE / RTZ / SR), fp16 + 8 bits (RNE / RTZ)
 
 
 def _stored(mpo, w32, scheme, seed):

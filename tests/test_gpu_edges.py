@@ -23,8 +23,8 @@ import synth
 pytestmark = pytest.mark.gpu
 
 FORMATS = [("rne", "fp16"), ("rne", "bf16"), ("rtz", "fp16"), ("rtz", "bf16"), ("sr", "fp16"), ("x8", "fp16"),
-           ("x8", "bf16")]
-RDT = {"rne": np.int16, "rtz": np.uint16, "sr": np.int16, "x8": np.int8}
+           ("x8", "bf16"), ("x8z", "fp16"), ("x8z", "bf16")]
+RDT = {"rne": np.int16, "rtz": np.uint16, "sr": np.int16, "x8": np.int8, "x8z": np.uint8}
 
 EDGE_G = {
     # +-0, min / max subnormal, max finite (both signs), +-Inf, NaN, 1.0, a normal small value
@@ -76,14 +76,14 @@ def state(n, seed):
 
 
 def dev_resid(r):
-    if r.dtype == np.int8:
+    if r.dtype in (np.int8, np.uint8):
         return torch.from_numpy(r.copy()).cuda()
     return torch.from_numpy(np.ascontiguousarray(r).view(np.int16).copy()).cuda()
 
 
 def host_resid(t, scheme):
     a = t.cpu().numpy()
-    return a.view(RDT[scheme]) if scheme != "x8" else a
+    return a.view(RDT[scheme]) if scheme not in ("x8", "x8z") else a
 
 
 KINDS = ["adamw", "adam_l2", "adam_b1_0", "sgd_m", "sgd_nesterov"]

@@ -646,7 +646,7 @@ def _kw_adam(hp):
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
 @pytest.mark.parametrize("kind,fmt,scheme", [("adam", "bf16", "rne"), ("sgd", "fp16", "rne"),
-                                             ("adam", "fp16", "sr"), ("adam", "bf16", "x8")])
+                                             ("adam", "fp16", "sr"), ("adam", "bf16", "x8"), ("sgd", "fp16", "x8z")])
 def test_p2p_fused_sharded_step_emulated_peers(mpo, orc, world, kind, fmt, scheme, p2p_kernel):
     """SURVEY 8(f) row 1, P2P form: `world` ranks emulated on one device (each with its own
     gradient buffer and value replica; the kernel of rank r reads every rank's gradient shard r
@@ -666,7 +666,7 @@ def test_p2p_fused_sharded_step_emulated_peers(mpo, orc, world, kind, fmt, schem
     gs = [synth.grads(n, 1e-2, fmt, 0xC0FFEE, k) for k in range(world)]
     if world > 1:                                # a non-finite gradient on one rank only
         gs[1][S * (world - 1) + 40] = 0x7C00 if fmt == "fp16" else 0x7F80
-    rdt = torch.int8 if scheme == "x8" else torch.int16
+    rdt = {"x8": torch.int8, "x8z": torch.uint8}.get(scheme, torch.int16)
     tdt = TDT[fmt]
     V = [torch.from_numpy(h.view(np.int16).copy()).view(tdt).cuda() for _ in range(world)]   # replicas
     G = [torch.from_numpy(g.view(np.int16).copy()).view(tdt).cuda() for g in gs]
@@ -675,7 +675,7 @@ def test_p2p_fused_sharded_step_emulated_peers(mpo, orc, world, kind, fmt, schem
     vs = [np.abs(synth.normal_f32(S, 1e-5, 6, k)) for k in range(world)]
     for k in range(world):
         rk = r[k * S:(k + 1) * S].copy()
-        Rs.append(torch.from_numpy(rk.view(np.int8) if scheme == "x8" else rk.view(np.int16)).cuda().view(rdt))
+        Rs.append(torch.from_numpy(rk if scheme in ("x8", "x8z") else rk.view(np.int16)).cuda().view(rdt))
         Ms.append(torch.from_numpy(ms[k].copy()).cuda())
         Ws.append(torch.from_numpy(vs[k].copy()).cuda())
     seed = 1234
@@ -701,7 +701,7 @@ def test_p2p_fused_sharded_step_emulated_peers(mpo, orc, world, kind, fmt, schem
         for rep in V:
             assert np.array_equal(host16(rep)[sl], hk), (k, "value replica")
         got_r = Rs[k].cpu().numpy()
-        assert np.array_equal(got_r.view(rk.dtype) if scheme != "x8" else got_r, rk), (k, "residual")
+        assert np.array_equal(got_r.view(rk.dtype) if scheme not in ("x8", "x8z") else got_r, rk), (k, "residual")
         assert same_bits_nan_equal(Ms[k].cpu().numpy(), ms[k]), (k, "m")
         if kind == "adam":
             assert same_bits_nan_equal(Ws[k].cpu().numpy(), vs[k]), (k, "v")

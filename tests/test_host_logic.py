@@ -14,9 +14,10 @@ def test_format_codes_match_the_header():
     assert api.format_code(torch.float16, "rtz") == 16 and api.format_code(torch.bfloat16, "rtz") == 17
     assert api.format_code(torch.float16, "sr") == 32
     assert api.format_code(torch.float16, "x8") == 48 and api.format_code(torch.bfloat16, "x8") == 49
+    assert api.format_code(torch.float16, "x8z") == 64 and api.format_code(torch.bfloat16, "x8z") == 65
     header = open(__import__("os").path.join(__import__("os").path.dirname(__file__), "..", "include", "mpo.h")).read()
     for name, code in (("MPO_FP16_RTZ", 16), ("MPO_BF16_RTZ", 17), ("MPO_FP16_SR", 32), ("MPO_FP16_X8", 48),
-                       ("MPO_BF16_X8", 49)):
+                       ("MPO_BF16_X8", 49), ("MPO_FP16_X8Z", 64), ("MPO_BF16_X8Z", 65)):
         assert f"{name} = {code}" in header
 
 
@@ -31,7 +32,7 @@ def test_format_errors():
 
 def test_resid_containers_and_seeds():
     assert api.resid_dtype("rne") == api.resid_dtype("rtz") == api.resid_dtype("sr") == torch.int16
-    assert api.resid_dtype("x8") == torch.int8
+    assert api.resid_dtype("x8") == torch.int8 and api.resid_dtype("x8z") == torch.uint8
     seeds = {api.step_seed(7, t) for t in range(1000)}
     assert len(seeds) == 1000 and all(0 <= s < 2 ** 64 for s in seeds)
     assert api.step_seed(7, 3) != api.step_seed(8, 3)
