@@ -284,7 +284,7 @@ typedef struct {
  * decay).  Same collective sequence and arguments as mpo_sharded_step, plus:
  *   seg, nseg : HOST array partitioning THIS rank's shard [0, n_total/world) into pieces (seg[0].start
  *               == 0, starts strictly increasing and < the shard length; every start a multiple of 8
- *               elements, 16 for the X8 formats, so each piece's arrays stay 16-B aligned); ranks
+ *               elements, 16 for the 8-bit-residual formats (X8, X8Z), so each piece's arrays stay 16-B aligned); ranks
  *               pass their own tables
  *   hp, nhp   : nhp groups (mpo_sgd_hp* | mpo_adam_hp*, HOST), 1 <= nhp <= MPO_MAX_HP_GROUPS;
  *               grad_scale, max_grad_norm, clip_value and skip_nonfinite as for a multi-tensor call
