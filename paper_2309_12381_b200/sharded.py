@@ -165,7 +165,10 @@ class ShardedResidualOptimizer:
     NCCL all-gather).  ``transport='p2p'``: value and gradient buffers live in torch symmetric
     memory and one ``mpo_p2p_sharded_step`` kernel per rank reads every rank's gradient shard and
     writes the new values into every rank's replica over NVLink (no collective launches; no
-    global-norm clipping)."""
+    global-norm clipping).
+
+    The gradients are SUMMED over ranks (R13, R15): pass ``grad_scale = 1 / world`` in the
+    hyper-parameters for DistributedDataParallel's mean."""
 
     def __init__(self, params, kind: str = "adam", fmt: Optional[torch.dtype] = None, group=None,
                  hp=None, exact: bool = True, comm_ptr: Optional[int] = None, scheme: str = "rne",
