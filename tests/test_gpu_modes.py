@@ -998,3 +998,36 @@ def test_torch_grad_scaler_protocol(mpo, kind):
     scaler2.scale(_loss(b, idx)).backward()
     with pytest.raises(mpo.MpoError, match="GradScaler"):
         scaler2.step(oh)
+
+
+@pytest.mark.parametrize("native", [True, False])
+def test_empty_and_frozen_parameters(mpo, native):
+    """Zero-element parameters and parameters without gradients ride along: the multi-tensor step
+    and both hook modes skip them and step the rest exactly as without them."""
+    torch.manual_seed(41)
+    ref = [torch.randn(300, device="cuda") * 0.02, torch.randn(17, 5, device="cuda") * 0.02]
+    pa = [nn.Parameter(t.clone()) for t in ref]
+    pb = [nn.Parameter(t.clone()) for t in ref] + [nn.Parameter(torch.empty(0, device="cuda")),
+                                                   nn.Parameter(torch.randn(8, device="cuda"), requires_grad=False)]
+    oa = mpo.ResidualAdamW(pa, lr=1e-3, fmt=torch.bfloat16)
+    ob = mpo.ResidualAdamW(pb, lr=1e-3, fmt=torch.bfloat16)
+    oc_params = [nn.Parameter(t.clone()) for t in ref] + [nn.Parameter(torch.empty(0, device="cuda"))]
+    oc = mpo.ResidualAdamW(oc_params, lr=1e-3, fmt=torch.bfloat16)
+    oc.install_backward_hooks(native=native, batch_below=0)
+    frozen = pb[3].detach().clone()
+    x = torch.randn(300, device="cuda", dtype=torch.bfloat16)
+    y = torch.randn(17, 5, device="cuda", dtype=torch.bfloat16)
+    for _ in range(3):
+        for ps, o in ((pa, oa), (pb, ob), (oc_params, oc)):
+            loss = (ps[0] * x).float().sum() + (ps[1] * y).float().square().sum()
+            if len(ps) > 2:
+                loss = loss + ps[2].float().sum()
+            loss.backward()
+            if o is not oc:
+                o.step()
+                for p in ps:
+                    p.grad = None
+    for i in range(2):
+        assert torch.equal(pa[i].view(torch.int16), pb[i].view(torch.int16))
+        assert torch.equal(pa[i].view(torch.int16), oc_params[i].view(torch.int16))
+    assert torch.equal(pb[3], frozen) and pb[2].numel() == 0
