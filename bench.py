@@ -125,6 +125,14 @@ class ClockSampler:
         except Exception:
             self.p = None
         self.windows = []
+        # nvidia-smi takes a moment to start: wait (<= 5 s) for its first sample, so that even a
+        # timed region shorter than that has samples before and after it
+        t_end = time.time() + 5.0
+        while self.p is not None and time.time() < t_end:
+            self.f.flush()
+            if os.path.getsize(self.f.name) > 0:
+                break
+            time.sleep(0.02)
 
     def mark(self, t0, t1):
         self.windows.append((t0, t1))
