@@ -37,3 +37,23 @@ def test_bench_line_contract():
     sys.path.insert(0, ROOT)
     import bench
     assert d["config"] == json.loads(json.dumps(bench.workload_config("resnet50_sgd")))
+
+
+def test_bench_multi_gpu_breakdown_path_at_world1():
+    """The N > 1 code path of the bench at world 1 (--mg-breakdown; the fused P2P step through the
+    child-process route with MPO_BENCH_FUSED_CHILD=1): update-only timing, the two collectives'
+    busbw fields and the fused step all present, none of them an error."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, MPO_BENCH_FUSED_CHILD="1", MASTER_ADDR="127.0.0.1", MASTER_PORT="29931")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "gpt2_adamw", "--steps", "4",
+                        "--warmup", "3", "--no-secondary", "--no-cpu-baseline", "--e2e-steps", "2", "--mg-breakdown"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.strip()][-1])
+    mg = d["multi_gpu"]
+    assert "error" not in json.dumps(mg), json.dumps(mg)[:2000]
+    assert mg["update_only"]["ms_per_step"] > 0
+    for k in ("reduce_scatter_grad16", "all_gather_value16"):
+        assert k in mg and mg[k]["ms"] > 0
+    assert mg["p2p_fused_step"]["ms_per_step"] > 0 and mg["p2p_fused_step"]["launches_per_step"] == 1
