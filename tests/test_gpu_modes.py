@@ -313,7 +313,8 @@ def test_sharded_grouped_world1_equals_param_groups(mpo, nccl1, clip):
 
 @pytest.mark.parametrize("kind", ["adam", "sgd"])
 @pytest.mark.parametrize("bucketed", [False, True])
-def test_sharded_resume_is_bit_identical(mpo, nccl1, kind, bucketed):
+@pytest.mark.parametrize("scheme", ["sr", "x8z"])
+def test_sharded_resume_is_bit_identical(mpo, nccl1, kind, bucketed, scheme):
     """Checkpoint / resume of the sharded optimizers (R17): 3 steps -> torch.save(values, optimizer
     shard state) -> fresh parameters + optimizer -> load -> 3 steps == 6 uninterrupted, bitwise."""
     import io
@@ -328,8 +329,8 @@ def test_sharded_resume_is_bit_identical(mpo, nccl1, kind, bucketed):
         ps = [nn.Parameter(t.clone()) for t in init]
         if bucketed:
             return ps, mpo.BucketedShardedOptimizer(ps, kind=kind, fmt=torch.float16, hp=hp(), bucket_elems=2048,
-                                                    scheme="sr", seed=3)
-        return ps, mpo.ShardedResidualOptimizer(ps, kind=kind, fmt=torch.float16, hp=hp(), scheme="sr", seed=3)
+                                                    scheme=scheme, seed=3)
+        return ps, mpo.ShardedResidualOptimizer(ps, kind=kind, fmt=torch.float16, hp=hp(), scheme=scheme, seed=3)
 
     def run(ps, opt, steps):
         for g in steps:
