@@ -43,6 +43,8 @@ L2_BYTES = 126 * 1024 * 1024
 WORKLOADS = {
     # name: (synth workload, value fmt, optimizer, hyper-parameters, BASELINE config index)
     "resnet50_sgd": ("resnet50", "fp16", "sgd", dict(lr=0.3, momentum=0.9, weight_decay=2e-4), 1),
+    # plain SGD (no momentum buffer): the 10 B/param row of SURVEY 8(a)'s byte table
+    "resnet50_sgd_plain": ("resnet50", "fp16", "sgd", dict(lr=0.3, momentum=0.0, weight_decay=2e-4), 1),
     "gpt2_adamw": ("gpt2_small", "bf16", "adam", dict(lr=6e-4, beta1=0.9, beta2=0.95, eps=1e-8,
                                                       weight_decay=0.1, adamw=True), 2),
     "vit_l16_adam_clip": ("vit_l16", "fp16", "adam", dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8,
@@ -224,7 +226,8 @@ class Workload:
             # scale so the global norm is ~4 (clipping active)
             self.grad.mul_(4.0 / math.sqrt(self.P) / 1e-3)
         n_state = L.shard if world > 1 else L.total
-        self.m = torch.zeros(n_state, dtype=torch.float32, device=dev)
+        plain_sgd = kind == "sgd" and not hp.get("momentum", 0.0)
+        self.m = None if plain_sgd else torch.zeros(n_state, dtype=torch.float32, device=dev)
         self.v = torch.zeros(n_state, dtype=torch.float32, device=dev) if kind == "adam" else None
         self.norm_ws = torch.zeros(mpo.norm_ws_doubles(), dtype=torch.float64, device=dev)
         torch.cuda.synchronize()
@@ -236,7 +239,7 @@ class Workload:
             V = L.views(self.value, shapes)
             R = L.views(self.resid, shapes)
             G = L.views(self.grad, shapes)
-            M = L.views(self.m, shapes)
+            M = L.views(self.m, shapes) if self.m is not None else [None] * len(shapes)
             W = L.views(self.v, shapes) if self.v is not None else [None] * len(shapes)
             self.table = mpo.TensorTable(V, R, G, M, W, scheme=scheme)
         self.comm = None
@@ -254,6 +257,8 @@ class Workload:
     @property
     def bytes_per_param(self):
         b = BYTES_PER_PARAM["adam_clip" if self.clip else self.kind]
+        if self.kind == "sgd" and not self.hpkw.get("momentum", 0.0):
+            b = 10                                    # value + residual + grad in, value + residual out
         return b - 2 if self.scheme in ("x8", "x8z") else b      # 8-bit residual: 1 B read + 1 B written
 
     def hp(self):
@@ -1431,7 +1436,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_secondary:
         del wl
         torch.cuda.empty_cache()
-        line["secondary"] = secondary([n for n in ("resnet50_sgd", "gpt2_adamw", "vit_l16_adam_clip", "llama7b_adam")
+        line["secondary"] = secondary([n for n in ("resnet50_sgd", "resnet50_sgd_plain", "gpt2_adamw",
+                                                   "vit_l16_adam_clip", "llama7b_adam")
                                        if n != args.workload], 200, 5, hbm_peak)
         if args.workload == "llama7b_adam":
             # the same LLaMA-7B step through the sharded entry point at world 1 (one flat piece, the
