@@ -250,7 +250,7 @@ RAGGED = [0, 1, 7, 8, 9, 64, 4095, 4096, 4097, 12345, 65539, 3]
 
 @pytest.mark.parametrize("fmt", ["fp16", "bf16"])
 @pytest.mark.parametrize("gfmt", ["same", "fp32", "other"])
-@pytest.mark.parametrize("kind", ["adam", "sgd"])
+@pytest.mark.parametrize("kind", ["adam", "sgd", "sgd_plain"])
 def test_multi_tensor_ragged_bit_exact(mpo, orc, fmt, gfmt, kind, step_kernel):
     gf = fmt if gfmt == "same" else ("fp32" if gfmt == "fp32" else ("bf16" if fmt == "fp16" else "fp16"))
     sizes = RAGGED
@@ -270,14 +270,18 @@ def test_multi_tensor_ragged_bit_exact(mpo, orc, fmt, gfmt, kind, step_kernel):
         hps = [mpo.AdamParams(lr=1e-3, weight_decay=0.1, adamw=True, step=3),
                mpo.AdamParams(lr=2e-3, beta1=0.3, beta2=0.95, weight_decay=0.01, adamw=False, step=7, grad_scale=0.5),
                mpo.AdamParams(lr=5e-4, beta1=0.0, beta2=0.9, eps=1e-6, step=1)]
-    else:
+    elif kind == "sgd":
         hps = [mpo.SgdParams(lr=0.3, momentum=0.9, weight_decay=2e-4),
                mpo.SgdParams(lr=0.1, momentum=0.9, nesterov=True, grad_scale=0.25),
                mpo.SgdParams(lr=0.05, momentum=0.5, dampening=0.1, first_step=True, weight_decay=1e-3)]
+    else:   # plain SGD: no momentum buffer at all (m NULL; 10 B/param)
+        hps = [mpo.SgdParams(lr=0.3, weight_decay=2e-4), mpo.SgdParams(lr=0.1, grad_scale=0.25),
+               mpo.SgdParams(lr=0.05, first_step=True, weight_decay=1e-3, clip_value=5e-3)]
+        ms = [None] * len(sizes)
     V = [dev16(h, fmt) for h in hs]
     R = [devi16(r) for r in rs]
     G = [dev_grad(g, gf) for g in gs]
-    M = [devf(m) for m in ms]
+    M = [devf(m) if m is not None else None for m in ms]
     W = [devf(v) for v in vs]
     tab = mpo.TensorTable(V, R, G, M, W if kind == "adam" else [None] * len(sizes), grp)
     if kind == "adam":
@@ -291,10 +295,11 @@ def test_multi_tensor_ragged_bit_exact(mpo, orc, fmt, gfmt, kind, step_kernel):
         else:
             orc.sgd_step(fmt, gf, hs[i], rs[i], gs[i], ms[i], lr=hp.lr, momentum=hp.momentum,
                          dampening=hp.dampening, weight_decay=hp.weight_decay, grad_scale=hp.grad_scale,
-                         nesterov=hp.nesterov, first_step=hp.first_step)
+                         nesterov=hp.nesterov, first_step=hp.first_step, clip_value=hp.clip_value)
         assert np.array_equal(host16(V[i]), hs[i]), i
         assert np.array_equal(R[i].cpu().numpy(), rs[i]), i
-        assert same_bits_nan_equal(M[i].cpu().numpy(), ms[i]), i
+        if ms[i] is not None:
+            assert same_bits_nan_equal(M[i].cpu().numpy(), ms[i]), i
         if kind == "adam":
             assert same_bits_nan_equal(W[i].cpu().numpy(), vs[i]), i
 
