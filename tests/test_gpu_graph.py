@@ -31,7 +31,8 @@ def _opt(mpo, kind, ps, fmt, scheme="rne", clip=None):
 
 
 @pytest.mark.parametrize("kind,fmt,scheme,clip", [("adam", torch.bfloat16, "rne", None), ("adam", torch.float16, "sr", None),
-                                                  ("adam", torch.bfloat16, "rne", 0.05), ("sgd", torch.float16, "rne", None)])
+                                                  ("adam", torch.bfloat16, "rne", 0.05), ("sgd", torch.float16, "rne", None),
+                                                  ("sgd", torch.bfloat16, "x8z", None), ("adam", torch.float16, "x8", None)])
 def test_graph_step_equals_eager(mpo, step_kernel, kind, fmt, scheme, clip):
     """Only opt.step() captured; gradients copied into their (static) buffers before each replay;
     an LR schedule changes group 0's lr every step.  6 replays == 6 eager steps, bitwise."""
