@@ -275,7 +275,8 @@ def test_sharded_world1_equals_unsharded(mpo, nccl1, kind, clip):
 
 
 @pytest.mark.parametrize("clip", [False, True])
-def test_sharded_grouped_world1_equals_param_groups(mpo, nccl1, clip):
+@pytest.mark.parametrize("scheme", ["rne", "x8z"])
+def test_sharded_grouped_world1_equals_param_groups(mpo, nccl1, clip, scheme):
     """Per-parameter hyper-parameter groups in the sharded step (mpo_sharded_step_grouped: the
     shard's pieces as a segment table; P:19 unchanged hyper-parameters, e.g. no decay on 1-D
     tensors) == ResidualAdamW with the same two param groups, bitwise at world 1; the
@@ -289,11 +290,11 @@ def test_sharded_grouped_world1_equals_param_groups(mpo, nccl1, clip):
     mg = 0.05 if clip else None
     ref = mpo.ResidualAdamW([{"params": [p for p, d in zip(pa, decay) if d], "weight_decay": 0.1},
                              {"params": [p for p, d in zip(pa, decay) if not d], "weight_decay": 0.0}],
-                            lr=1e-3, fmt=torch.bfloat16, max_grad_norm=mg)
+                            lr=1e-3, fmt=torch.bfloat16, max_grad_norm=mg, scheme=scheme)
     hps = [mpo.AdamParams(lr=1e-3, weight_decay=0.1, max_grad_norm=mg or 0.0),
            mpo.AdamParams(lr=1e-3, weight_decay=0.0, max_grad_norm=mg or 0.0)]
     sh = mpo.ShardedResidualOptimizer(pb, kind="adam", fmt=torch.bfloat16, hp=hps,
-                                      hp_index=[0 if d else 1 for d in decay])
+                                      hp_index=[0 if d else 1 for d in decay], scheme=scheme)
     assert len(sh.segments) > 1
     for t in range(3):
         grads = [torch.randn(s, device="cuda").to(torch.bfloat16) * 1e-2 for s in shapes]
