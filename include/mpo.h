@@ -311,7 +311,8 @@ mpo_status mpo_comm_check(uintptr_t nccl_comm);
  *                       of the per-rank gradient buffers (a multicast object every rank bound)
  *   value_uc          : this rank's unicast address of its value replica (read)
  *   resid_shard, m_shard, v_shard : this rank's shard state (n_total/world entries)
- *   vdt               : MPO_FP16 | MPO_BF16 (RNE storage); grads of the same dtype
+ *   vdt               : any storage format (mpo_dtype); grads of its base 16-bit dtype;
+ *                       stochastic-rounding draws: stream = rank, index inside the shard
  *   hp                : mpo_sgd_hp* | mpo_adam_hp*; grad_scale 1/world for a mean; no global-norm
  *                       clipping and no skip_nonfinite (no pre-pass); clip_value allowed
  * The caller orders the call after every rank finished writing its gradients and before any
@@ -332,7 +333,7 @@ mpo_status mpo_nvls_sharded_step(mpo_optim kind, int32_t rank, int32_t world, mp
  *   multimem.st                      ->  a store into every rank's replica.
  * Arguments as mpo_p2p_sharded_step (value_peers / grad_peers: HOST arrays of `world` device
  * pointers, value_peers[rank] is the replica read), constraints as mpo_nvls_sharded_step
- * (MPO_FP16 | MPO_BF16 RNE storage, grads of the same dtype, no pre-pass); 1 <= world <= 8.
+ * (any storage format, grads of its base dtype, no pre-pass); 1 <= world <= 8.
  * Not a product path: the multi-GPU path is mpo_nvls_sharded_step on a real multicast object. */
 mpo_status mpo_nvls_emulated_step(mpo_optim kind, int32_t rank, int32_t world, mpo_dtype vdt,
                                   void* const* value_peers, const void* const* grad_peers,

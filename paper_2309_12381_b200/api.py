@@ -384,7 +384,8 @@ def mpo_nvls_sharded_step(kind: int, rank: int, world: int, vdt: int, value_mc: 
 
 def mpo_nvls_emulated_step(kind: int, rank: int, world: int, value_peers: Sequence[int], grad_peers: Sequence[int],
                            resid_shard: torch.Tensor, m_shard: Optional[torch.Tensor], v_shard: Optional[torch.Tensor],
-                           n_total: int, hp, value_dtype: torch.dtype, stream=None, exact: bool = True):
+                           n_total: int, hp, value_dtype: torch.dtype, stream=None, exact: bool = True,
+                           scheme: str = "rne"):
     """The NVLS kernel with its multicast operations emulated over peer addresses (validation on a
     box without a multicast object; include/mpo.h).  Arguments as mpo_p2p_sharded_step."""
     if len(value_peers) != world or len(grad_peers) != world:
@@ -393,7 +394,7 @@ def mpo_nvls_emulated_step(kind: int, rank: int, world: int, value_peers: Sequen
     chp = hp.c() if hasattr(hp, "c") else hp
     vp = (C.c_void_p * world)(*[C.c_void_p(int(a)) for a in value_peers])
     gp = (C.c_void_p * world)(*[C.c_void_p(int(a)) for a in grad_peers])
-    _lib.check(L, L.mpo_nvls_emulated_step(kind, rank, world, format_code(value_dtype), vp, gp, _ptr(resid_shard),
+    _lib.check(L, L.mpo_nvls_emulated_step(kind, rank, world, format_code(value_dtype, scheme), vp, gp, _ptr(resid_shard),
                                            _ptr(m_shard), _ptr(v_shard), n_total, C.byref(chp), _stream(stream)))
 
 

@@ -802,7 +802,8 @@ mpo_status nvls_step(mpo_optim kind, int32_t rank, int32_t world, mpo_dtype vdt,
     if (world < 1 || rank < 0 || rank >= world || (emu && world > kMaxPeers)) return fail(MPO_EINVAL, "bad rank / world");
     if (n_total < 0 || n_total % (int64_t(8) * world) != 0)
         return fail(MPO_EINVAL, "n_total must be a non-negative multiple of 8*world");
-    if (vdt != MPO_FP16 && vdt != MPO_BF16) return fail(MPO_EDTYPE, "the NVLS step takes MPO_FP16 or MPO_BF16 values");
+    if (!is_value_format(vdt)) return fail(MPO_EDTYPE, "unsupported storage format");
+    if ((st = check_dtypes(vdt, mpo_dtype(base_of(vdt)))) != MPO_OK) return st;
     if (!hp) return fail(MPO_EINVAL, "NULL hyper-parameters");
     if (n_total == 0) return MPO_OK;
     if ((!emu && (!value_mc || !grad_mc)) || !value_uc || !resid_shard) return fail(MPO_EINVAL, "NULL buffer");
@@ -817,11 +818,12 @@ mpo_status nvls_step(mpo_optim kind, int32_t rank, int32_t world, mpo_dtype vdt,
         if (!m_shard || !v_shard || !aligned16(m_shard) || !aligned16(v_shard))
             return fail(MPO_EALIGN, "m/v shards must be non-NULL and 16-byte aligned");
         const AdamK k = derive_adam(*h);
-        if (vdt == MPO_BF16)
-            return FormatOps<MPO_BF16>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, v_shard,
-                                             rank * shard, shard, nullptr, &k, emu, world, s);
-        return FormatOps<MPO_FP16>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, v_shard,
-                                         rank * shard, shard, nullptr, &k, emu, world, s);
+#define X(F)                                                                                                    \
+    if (vdt == F)                                                                                               \
+        return FormatOps<F>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, v_shard, rank * shard, \
+                                  shard, nullptr, &k, emu, world, rank, s);
+        MPO_FORMATS(X)
+#undef X
     }
     if (kind == MPO_SGD) {
         const mpo_sgd_hp* h = static_cast<const mpo_sgd_hp*>(hp);
@@ -830,11 +832,12 @@ mpo_status nvls_step(mpo_optim kind, int32_t rank, int32_t world, mpo_dtype vdt,
         if (h->momentum != 0.0 && (!m_shard || !aligned16(m_shard)))
             return fail(MPO_EALIGN, "momentum shard must be non-NULL and 16-byte aligned");
         const SgdK k = derive_sgd(*h);
-        if (vdt == MPO_BF16)
-            return FormatOps<MPO_BF16>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, nullptr,
-                                             rank * shard, shard, &k, nullptr, emu, world, s);
-        return FormatOps<MPO_FP16>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, nullptr,
-                                         rank * shard, shard, &k, nullptr, emu, world, s);
+#define X(F)                                                                                                    \
+    if (vdt == F)                                                                                               \
+        return FormatOps<F>::nvls(kind, value_mc, value_uc, grad_mc, resid_shard, m_shard, nullptr, rank * shard, \
+                                  shard, &k, nullptr, emu, world, rank, s);
+        MPO_FORMATS(X)
+#undef X
     }
     return fail(MPO_EINVAL, "unknown optimizer kind");
 }

@@ -61,27 +61,28 @@ mpo_status FormatOps<SF>::reconstruct(const void* value, const void* resid, floa
 
 template <class Op, class MC>
 static void launch_nvls(const MC& mc, const uint16_t* vu, void* resid, float* m, float* v, int64_t shard_base,
-                        int64_t n, const typename Op::K& k, cudaStream_t s) {
+                        int64_t n, uint32_t stream, const typename Op::K& k, cudaStream_t s) {
     auto kern = nvls_step_kernel<SF, Op, MC>;
     static const int per_sm = resident_blocks(kern);   // persistent: one wave of resident CTAs
     const int64_t grid = grid_for((n / kUnitEl + kThreads * kUnroll - 1) / (kThreads * kUnroll), per_sm);
-    kern<<<unsigned(grid), kThreads, 0, s>>>(mc, vu, resid, m, v, shard_base, n, k);
+    kern<<<unsigned(grid), kThreads, 0, s>>>(mc, vu, resid, m, v, shard_base, n, stream, k);
 }
 
 template <>
 mpo_status FormatOps<SF>::nvls(int kind, void* value_mc, const void* value_uc, const void* grad_mc, void* resid,
                                float* m, float* v, int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak,
-                               const Peers* emu, int world, cudaStream_t s) {
+                               const Peers* emu, int world, int rank, cudaStream_t s) {
     constexpr int B = Fmt<SF>::base;
+    const uint32_t st = uint32_t(rank);
     auto* vu = static_cast<const uint16_t*>(value_uc);
     if (emu) {
         const NvlsEmulated<B> mc{*emu, world};
-        if (kind == MPO_ADAM) launch_nvls<AdamOp>(mc, vu, resid, m, v, shard_base, n, *ak, s);
-        else launch_nvls<SgdOp>(mc, vu, resid, m, v, shard_base, n, *sk, s);
+        if (kind == MPO_ADAM) launch_nvls<AdamOp>(mc, vu, resid, m, v, shard_base, n, st, *ak, s);
+        else launch_nvls<SgdOp>(mc, vu, resid, m, v, shard_base, n, st, *sk, s);
     } else {
         const NvlsMulticast<B> mc{static_cast<uint16_t*>(value_mc), static_cast<const uint16_t*>(grad_mc)};
-        if (kind == MPO_ADAM) launch_nvls<AdamOp>(mc, vu, resid, m, v, shard_base, n, *ak, s);
-        else launch_nvls<SgdOp>(mc, vu, resid, m, v, shard_base, n, *sk, s);
+        if (kind == MPO_ADAM) launch_nvls<AdamOp>(mc, vu, resid, m, v, shard_base, n, st, *ak, s);
+        else launch_nvls<SgdOp>(mc, vu, resid, m, v, shard_base, n, st, *sk, s);
     }
     ++g_launches;
     return check_launch("nvls_step_kernel");

@@ -1307,7 +1307,7 @@ template <int SF, class Op, class MC>
 __global__ void __launch_bounds__(kThreads) nvls_step_kernel(const __grid_constant__ MC mc,
                                                              const uint16_t* __restrict__ value_uc, void* resid,
                                                              float* __restrict__ m, float* __restrict__ v,
-                                                             int64_t shard_base, int64_t n,
+                                                             int64_t shard_base, int64_t n, uint32_t stream,
                                                              const __grid_constant__ typename Op::K c) {
     constexpr int B = Fmt<SF>::base;
     const bool need_m = Op::reads_m(c), has_m = Op::writes_m(c);
@@ -1354,7 +1354,8 @@ __global__ void __launch_bounds__(kThreads) nvls_step_kernel(const __grid_consta
                 float vv[8] = {v0[j].x, v0[j].y, v0[j].z, v0[j].w, v1[j].x, v1[j].y, v1[j].z, v1[j].w};
                 uint4 ho;
                 ResidUnit<SF> ro;
-                process_unit<SF, B, Op, false>(hv[j], rv[j], gu[j], mm, vv, c, 1.0f, 0u, shard_base + e, ho, ro);
+                // stochastic-rounding draws keyed like mpo_sharded_step: stream = rank, index in the shard
+                process_unit<SF, B, Op, false>(hv[j], rv[j], gu[j], mm, vv, c, 1.0f, stream, e, ho, ro);
                 mc.store_value(shard_base + e, ho);             // all-gather: every rank's replica
                 st_resid<SF>(resid, e, ro);
                 if (has_m) {
@@ -1727,7 +1728,7 @@ struct FormatOps {
     // over emu's `world` peer buffers (value_mc / grad_mc unused)
     static mpo_status nvls(int kind, void* value_mc, const void* value_uc, const void* grad_mc, void* resid, float* m,
                            float* v, int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak,
-                           const Peers* emu, int world, cudaStream_t s);
+                           const Peers* emu, int world, int rank, cudaStream_t s);
     static mpo_status p2p(int kind, const Peers& peers, int world, int rank, void* resid, float* m, float* v,
                           int64_t shard_base, int64_t n, const SgdK* sk, const AdamK* ak, cudaStream_t s);
 };

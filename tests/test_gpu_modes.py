@@ -711,8 +711,10 @@ def test_p2p_fused_sharded_step_emulated_peers(mpo, orc, world, kind, fmt, schem
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
-@pytest.mark.parametrize("kind,fmt", [("adam", "bf16"), ("sgd", "fp16"), ("adam", "fp16")])
-def test_nvls_kernel_emulated_multicast(mpo, orc, world, kind, fmt):
+@pytest.mark.parametrize("kind,fmt,scheme", [("adam", "bf16", "rne"), ("sgd", "fp16", "rne"), ("adam", "fp16", "rne"),
+                                             ("adam", "fp16", "sr"), ("adam", "bf16", "x8"), ("sgd", "fp16", "x8z"),
+                                             ("adam", "bf16", "rtz")])
+def test_nvls_kernel_emulated_multicast(mpo, orc, world, kind, fmt, scheme):
     """SURVEY 8(f) row 1, NVLS form, on a box without a multicast object: the NVLS kernel with
     multimem.ld_reduce / multimem.st emulated over `world` ranks' buffers on one device (include/
     mpo.h mpo_nvls_emulated_step).  The emulated reduction is the fp32 sum in rank order rounded
@@ -729,40 +731,44 @@ def test_nvls_kernel_emulated_multicast(mpo, orc, world, kind, fmt):
     for k in range(world):
         w[k * S:k * S + 36] = synth.edge_f32() * np.float32(1e-3)
         w[k * S + 36:k * S + 72] = synth.edge_f32()
-    h, r = orc.split(fmt, w)
+    h, r = orc.split_s(scheme, fmt, w, seed=3, stream=0)
     gs = [synth.grads(n, 1e-2, fmt, 0xC0FFEE, 10 + k) for k in range(world)]
     if world > 1:
         gs[1][S * (world - 1) + 40] = 0x7C00 if fmt == "fp16" else 0x7F80
     tdt = TDT[fmt]
+    rdt = {"x8": torch.int8, "x8z": torch.uint8}.get(scheme, torch.int16)
     V = [torch.from_numpy(h.view(np.int16).copy()).view(tdt).cuda() for _ in range(world)]
     G = [torch.from_numpy(g.view(np.int16).copy()).view(tdt).cuda() for g in gs]
     ms = [synth.normal_f32(S, 1e-3, 15, k) for k in range(world)]
     vs = [np.abs(synth.normal_f32(S, 1e-5, 16, k)) for k in range(world)]
-    Rs = [torch.from_numpy(r[k * S:(k + 1) * S].copy()).cuda() for k in range(world)]
+    Rs = [torch.from_numpy(r[k * S:(k + 1) * S].copy() if scheme in ("x8", "x8z") else
+                           r[k * S:(k + 1) * S].view(np.int16).copy()).cuda().view(rdt) for k in range(world)]
     Ms = [torch.from_numpy(x.copy()).cuda() for x in ms]
     Ws = [torch.from_numpy(x.copy()).cuda() for x in vs]
+    seed = 4321
     if kind == "adam":
-        hp = mpo.AdamParams(lr=1e-3, weight_decay=0.1, step=3, grad_scale=1.0 / world)
+        hp = mpo.AdamParams(lr=1e-3, weight_decay=0.1, step=3, grad_scale=1.0 / world, seed=seed)
     else:
-        hp = mpo.SgdParams(lr=0.1, momentum=0.9, weight_decay=1e-4, grad_scale=1.0 / world)
+        hp = mpo.SgdParams(lr=0.1, momentum=0.9, weight_decay=1e-4, grad_scale=1.0 / world, seed=seed)
     vp = [t.data_ptr() for t in V]
     gp = [t.data_ptr() for t in G]
     for k in range(world):
         api.mpo_nvls_emulated_step(MPO_ADAM if kind == "adam" else MPO_SGD, k, world, vp, gp, Rs[k], Ms[k],
-                                   Ws[k] if kind == "adam" else None, n, hp, tdt, exact=True)
+                                   Ws[k] if kind == "adam" else None, n, hp, tdt, exact=True, scheme=scheme)
     torch.cuda.synchronize()
     for k in range(world):
         sl = slice(k * S, (k + 1) * S)
         g16 = orc.cast16(fmt, orc.reduce_sum16(fmt, [g[sl] for g in gs]))
         hk, rk = h[sl].copy(), r[sl].copy()
-        if kind == "adam":
-            orc.adam_step(fmt, fmt, hk, rk, g16, ms[k], vs[k], **_kw_adam(hp))
+        if kind == "adam":     # SR draws: stream = rank, index inside the shard (as the sharded step)
+            orc.adam_step_s(scheme, fmt, fmt, hk, rk, g16, ms[k], vs[k], seed=seed, stream=k, **_kw_adam(hp))
         else:
-            orc.sgd_step(fmt, fmt, hk, rk, g16, ms[k], lr=hp.lr, momentum=hp.momentum,
-                         weight_decay=hp.weight_decay, grad_scale=hp.grad_scale)
+            orc.sgd_step_s(scheme, fmt, fmt, hk, rk, g16, ms[k], lr=hp.lr, momentum=hp.momentum,
+                           weight_decay=hp.weight_decay, grad_scale=hp.grad_scale, seed=seed, stream=k)
         for rep in V:
             assert np.array_equal(host16(rep)[sl], hk), (k, "value replica")
-        assert np.array_equal(Rs[k].cpu().numpy(), rk), (k, "residual")
+        got_r = Rs[k].cpu().numpy()
+        assert np.array_equal(got_r.view(rk.dtype) if scheme not in ("x8", "x8z") else got_r, rk), (k, "residual")
         assert same_bits_nan_equal(Ms[k].cpu().numpy(), ms[k]), (k, "m")
         if kind == "adam":
             assert same_bits_nan_equal(Ws[k].cpu().numpy(), vs[k]), (k, "v")
@@ -786,13 +792,12 @@ def test_nvls_emulated_step_rejects(mpo):
     import ctypes as C
     from paper_2309_12381_b200 import _lib
     L = api._lib_of(True)
-    R8 = torch.zeros(n, dtype=torch.int8, device="cuda")
     arr = (C.c_void_p * 1)(C.c_void_p(v.data_ptr()))
     garr = (C.c_void_p * 1)(C.c_void_p(g.data_ptr()))
     chp = mpo.AdamParams(lr=1e-3).c()
-    st = L.mpo_nvls_emulated_step(MPO_ADAM, 0, 1, api.format_code(torch.bfloat16, "x8"), arr, garr, R8.data_ptr(),
-                                  M.data_ptr(), W.data_ptr(), n, C.byref(chp), None)
-    assert st == _lib.MPO_EDTYPE and b"FP16 or MPO_BF16" in L.mpo_last_error()
+    st = L.mpo_nvls_emulated_step(MPO_ADAM, 0, 1, 99, arr, garr, R.data_ptr(), M.data_ptr(), W.data_ptr(), n,
+                                  C.byref(chp), None)
+    assert st == _lib.MPO_EDTYPE and b"unsupported storage format" in L.mpo_last_error()
 
 
 def test_p2p_fused_sharded_step_rejects(mpo):
