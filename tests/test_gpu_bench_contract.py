@@ -45,7 +45,12 @@ def test_bench_multi_gpu_breakdown_path_at_world1():
     busbw fields and the fused step all present, none of them an error."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    env = dict(os.environ, MPO_BENCH_FUSED_CHILD="1", MASTER_ADDR="127.0.0.1", MASTER_PORT="29931")
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ, MPO_BENCH_FUSED_CHILD="1", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "gpt2_adamw", "--steps", "4",
                         "--warmup", "3", "--no-secondary", "--no-cpu-baseline", "--e2e-steps", "2", "--mg-breakdown"],
                        capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
