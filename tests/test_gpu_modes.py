@@ -648,7 +648,8 @@ def _kw_adam(hp):
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
 @pytest.mark.parametrize("kind,fmt,scheme", [("adam", "bf16", "rne"), ("sgd", "fp16", "rne"),
-                                             ("adam", "fp16", "sr"), ("adam", "bf16", "x8"), ("sgd", "fp16", "x8z")])
+                                             ("adam", "fp16", "sr"), ("adam", "bf16", "x8"), ("sgd", "fp16", "x8z"),
+                                             ("adam", "bf16", "rtz")])
 def test_p2p_fused_sharded_step_emulated_peers(mpo, orc, world, kind, fmt, scheme, p2p_kernel):
     """SURVEY 8(f) row 1, P2P form: `world` ranks emulated on one device (each with its own
     gradient buffer and value replica; the kernel of rank r reads every rank's gradient shard r
